@@ -1,0 +1,333 @@
+"""Generate golden fixtures by running the UNMODIFIED reference (kvpack).
+
+This script is the only place that touches /root/reference: it imports the
+reference package from a temporary copy and records its outputs as small
+``.npz`` fixtures (plus SHA-256 digests for the full-size BASELINE configs)
+under ``tests/golden/``.  The fixtures pin both the CPU oracle (``oracle/``)
+and the CUDA path; nothing at test/bench time needs the reference.
+
+    python tests/golden/make_golden.py            # small fixtures (seconds)
+    python tests/golden/make_golden.py --big      # + config-1/4 digests (~30 s)
+    python tests/golden/make_golden.py --cfg2     # + config-2 slice (~2 min)
+
+Reference call sites followed: kvcache.py:76-145 (prefill), :150-177
+(append_token), attention.py:176-188 (attention_step), :112-165
+(fused_v_output), kvcache.py:182-212 (fetch_dequantized), bench.py:77-95
+(collect_stats), quantizer.py:162-209 (quantize_block).
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import shutil
+import sys
+import tempfile
+from dataclasses import replace
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF = "/root/reference/pkg/src"
+
+
+def _import_reference():
+    tmp = tempfile.mkdtemp(prefix="kvpack_ref_")
+    shutil.copytree(REF, os.path.join(tmp, "src"))
+    sys.path.insert(0, os.path.join(tmp, "src"))
+    import kvpack  # noqa: E402
+
+    return kvpack
+
+
+kv = _import_reference()
+
+
+def _arena(a):
+    return np.frombuffer(a.snapshot(), dtype=np.uint8).copy(), a.block_offsets.astype(np.uint32)
+
+
+def _state_record(prefix, st):
+    rec = {}
+    ka, ko = _arena(st.k_arena)
+    va, vo = _arena(st.v_arena)
+    rec[prefix + "k_arena"] = ka
+    rec[prefix + "k_offsets"] = ko
+    rec[prefix + "v_arena"] = va
+    rec[prefix + "v_offsets"] = vo
+    rec[prefix + "k_lengths"] = st.k_codebook.code_lengths.astype(np.uint8)
+    rec[prefix + "v_lengths"] = st.v_codebook.code_lengths.astype(np.uint8)
+    rec[prefix + "k_words"] = st.k_codebook.code_words.astype(np.uint32)
+    rec[prefix + "v_words"] = st.v_codebook.code_words.astype(np.uint32)
+    rec[prefix + "k_tree_children"] = st.k_codebook.decode_tree.children.astype(np.int32)
+    rec[prefix + "v_tree_children"] = st.v_codebook.decode_tree.children.astype(np.int32)
+    rec[prefix + "counters"] = np.array(
+        [st.context_len, st.compressed_tokens, st.buffered,
+         st.k_arena.payload_bits, st.k_arena.payload_bytes, st.k_arena.n_slices,
+         st.v_arena.payload_bits, st.v_arena.payload_bytes, st.v_arena.n_slices],
+        dtype=np.int64)
+    rec[prefix + "k_buffer"] = st._k_buffer[: st.buffered].copy()
+    rec[prefix + "v_buffer"] = st._v_buffer[: st.buffered].copy()
+    s = kv.collect_stats(st)
+    rec[prefix + "stats"] = np.array(
+        [s.original_bytes, s.compressed_bytes, s.metadata_bytes, s.payload_bits,
+         s.quantized_values], dtype=np.int64)
+    rec[prefix + "ratio"] = np.float64(s.compression_ratio)
+    return rec
+
+
+def _prefill_hist(k_work, v_work, cfg_k, cfg_v, H):
+    """Raw (unsmoothed) prefill histograms, via the reference's own functions."""
+    n_full = (k_work.shape[0] // cfg_k.block_size) * cfg_k.block_size
+    hk = np.zeros(256, dtype=np.uint64)
+    hv = np.zeros(256, dtype=np.uint64)
+    kq, vq = [], []
+    if n_full:
+        from kvpack.kvcache import _quantize_tokens
+
+        kq = _quantize_tokens(k_work[:n_full], cfg_k, 0, H, None)
+        vq = _quantize_tokens(v_work[:n_full], cfg_v, 0, H, None)
+        hk += kv.build_histogram(np.concatenate([b.codes.ravel() for b in kq]))
+        hv += kv.build_histogram(np.concatenate([b.codes.ravel() for b in vq]))
+    return hk, hv, kq, vq
+
+
+def make_case(name, *, ctx, H, D, bs, buffer=None, rel_k=0.05, rel_v=0.15, dtype=np.float16,
+              seed=0, appended=0, inject=None, constant=None, synthetic=True, n_q=2):
+    cfg_k = kv.QuantConfig(kv.QuantMode.K_BLOCK, block_size=bs, rel_quant_scale=rel_k,
+                           buffer_size=buffer)
+    cfg_v = kv.QuantConfig(kv.QuantMode.V_TOKEN, block_size=bs, rel_quant_scale=rel_v,
+                           buffer_size=buffer)
+    total = ctx + appended
+    if constant is not None:
+        kfull = np.full((total, H, D), constant[0], dtype=np.float32)
+        vfull = np.full((total, H, D), constant[1], dtype=np.float32)
+    elif synthetic:
+        spec = kv.SyntheticSpec(total, H, D, seed=seed)
+        kfull = kv.generate_synthetic(spec).values
+        vfull = kv.generate_synthetic(replace(spec, seed=seed ^ 0x9E3779B9)).values
+    else:
+        rng = np.random.default_rng(seed)
+        kfull = rng.standard_normal((total, H, D)).astype(np.float32)
+        vfull = rng.standard_normal((total, H, D)).astype(np.float32)
+    k_in = kfull[:ctx].astype(dtype)
+    v_in = vfull[:ctx].astype(dtype)
+    codebooks = None
+    if inject is not None:
+        codebooks = tuple(kv.codebook_from_lengths if False else kv.deserialize_codebook(
+            bytes(np.asarray(x, dtype=np.uint8).tobytes())) for x in inject)
+    rec = {
+        "cfg": np.array([ctx, H, D, bs, cfg_k.buffer_size, appended], dtype=np.int64),
+        "rel": np.array([rel_k, rel_v], dtype=np.float64),
+        "k_in": k_in, "v_in": v_in,
+        "k_app": kfull[ctx:].astype(np.float32), "v_app": vfull[ctx:].astype(np.float32),
+    }
+    if inject is not None:
+        rec["inject_k"] = np.asarray(inject[0], dtype=np.uint8)
+        rec["inject_v"] = np.asarray(inject[1], dtype=np.uint8)
+    k_ct, v_ct = kv.CacheTensor(k_in), kv.CacheTensor(v_in)
+    hk, hv, kq, vq = _prefill_hist(k_ct.as_float32(), v_ct.as_float32(), cfg_k, cfg_v, H)
+    rec["k_hist"] = hk
+    rec["v_hist"] = hv
+    if kq:
+        rec["k_codes"] = np.stack([b.codes for b in kq])
+        rec["k_mins"] = np.stack([b.unit_mins for b in kq])
+        rec["k_scales"] = np.stack([b.unit_scales for b in kq])
+        rec["v_codes"] = np.stack([b.codes for b in vq])
+        rec["v_mins"] = np.stack([b.unit_mins for b in vq])
+        rec["v_scales"] = np.stack([b.unit_scales for b in vq])
+    st = kv.LayerCacheState.prefill(k_ct, v_ct, cfg_k, cfg_v, codebooks=codebooks)
+    rec.update(_state_record("pre_", st))
+    for t in range(appended):
+        st.append_token(kfull[ctx + t], vfull[ctx + t])
+    rec.update(_state_record("fin_", st))
+    # Fetch side on the final state.
+    qrng = np.random.default_rng([seed, 0x71726E67])
+    qs, outs, scores = [], [], []
+    for _ in range(n_q):
+        q = qrng.standard_normal((H, D), dtype=np.float32)
+        res = kv.attention_step(st, q)
+        qs.append(q)
+        outs.append(res.out)
+        scores.append(res.scores)
+    rec["q"] = np.stack(qs)
+    rec["att_out"] = np.stack(outs)
+    rec["att_scores"] = np.stack(scores)
+    w = qrng.random((H, st.context_len), dtype=np.float32)
+    rec["w"] = w
+    rec["vout_w"] = kv.fused_v_output(st, w)
+    kd, vd = st.fetch_dequantized()
+    rec["deq_k"] = kd.values
+    rec["deq_v"] = vd.values
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **rec)
+    print(f"{name}: ctx={ctx}+{appended} H={H} D={D} bs={bs} k_maxlen={int(st.k_codebook.max_code_length)} "
+          f"v_maxlen={int(st.v_codebook.max_code_length)} ratio={rec['fin_ratio']:.4f} "
+          f"size={os.path.getsize(path)}")
+
+
+def _fib_lengths(n):
+    h = np.zeros(256, dtype=np.uint64)
+    a, b = 1, 1
+    for s in range(n):
+        h[s] = a
+        a, b = b, a + b
+    return kv.build_codebook(h).code_lengths
+
+
+def kat_cases():
+    """Known-answer vectors from the reference tests (test_*.py), re-run here."""
+    out = {}
+    # test_quantizer.py:27-35 : [0,1,2,3] @ rel 0.5
+    c, m = kv.quantize_unit(np.array([0, 1, 2, 3], dtype=np.float32), 0.5)
+    out["kat_quant_codes"] = c.astype(np.uint8)
+    out["kat_quant_meta"] = np.array([m.min_value, m.scale], dtype=np.float64)
+    # test_codebook.py:77-82 : {4,2,1,1} -> lengths [1,2,3,3]
+    h = np.zeros(256, dtype=np.uint64)
+    h[:4] = [4, 2, 1, 1]
+    cb = kv.build_codebook(h)
+    out["kat_cb_lengths"] = cb.code_lengths.astype(np.uint8)
+    out["kat_cb_words"] = cb.code_words.astype(np.uint32)
+    # test_codec.py:125-139 style: encode [0,1,2,3] with that codebook
+    bits, count = kv.encode_slice(np.array([0, 1, 2, 3], dtype=np.uint8), cb)
+    out["kat_slice_bytes"] = np.packbits(bits)
+    out["kat_slice_count"] = np.int64(count)
+    # random histograms -> lengths (tie-breaking coverage)
+    rng = np.random.default_rng(1234)
+    hists, lens = [], []
+    for i in range(64):
+        hh = np.zeros(256, dtype=np.uint64)
+        n = int(rng.integers(1, 257))
+        sel = rng.choice(256, size=n, replace=False)
+        if i % 3 == 0:
+            hh[sel] = rng.integers(1, 5, size=n)        # many ties
+        elif i % 3 == 1:
+            hh[sel] = rng.integers(1, 1 << 20, size=n)
+        else:
+            hh[sel] = (1.6 ** rng.integers(0, 40, size=n)).astype(np.uint64)
+        hists.append(hh)
+        lens.append(kv.build_codebook(hh).code_lengths.astype(np.uint8))
+    out["kat_hists"] = np.stack(hists)
+    out["kat_hist_lengths"] = np.stack(lens)
+    # quantize edge cases: half-step grid (adversarial ties), constants, tiny ranges
+    grids = []
+    rng = np.random.default_rng(99)
+    for rel in (0.05, 0.15, 1 / 255, 0.5, 1.0, 0.3333):
+        x = rng.standard_normal((64, 128)).astype(np.float32)
+        x[:, :8] = np.float32(0.25) * rng.integers(-8, 8, size=(64, 8))   # half-step ties
+        x[:, 8] = 3.0                                                      # constant column
+        x[5, :] = -1.0                                                     # constant row
+        x[:, 9] = np.float32(1e-30) * rng.standard_normal(64)               # scale underflow
+        grids.append((rel, x))
+    out["kat_grid_x"] = np.stack([g[1] for g in grids])
+    out["kat_grid_rel"] = np.array([g[0] for g in grids])
+    kc, km, ks, vc, vm, vs = [], [], [], [], [], []
+    for rel, x in grids:
+        cfgk = kv.QuantConfig(kv.QuantMode.K_BLOCK, 64, rel)
+        cfgv = kv.QuantConfig(kv.QuantMode.V_TOKEN, 64, rel)
+        qk = kv.quantize_block(x, kv.QuantMode.K_BLOCK, cfgk, 0, 0, 1)
+        qv = kv.quantize_block(x, kv.QuantMode.V_TOKEN, cfgv, 0, 0, 1)
+        kc.append(qk.codes); km.append(qk.unit_mins); ks.append(qk.unit_scales)
+        vc.append(qv.codes); vm.append(qv.unit_mins); vs.append(qv.unit_scales)
+    out.update(kat_grid_kcodes=np.stack(kc), kat_grid_kmins=np.stack(km),
+               kat_grid_kscales=np.stack(ks), kat_grid_vcodes=np.stack(vc),
+               kat_grid_vmins=np.stack(vm), kat_grid_vscales=np.stack(vs))
+    np.savez_compressed(os.path.join(HERE, "kats.npz"), **out)
+    print("kats: written")
+
+
+def _digest(st):
+    h = {}
+    for nm, a in (("k", st.k_arena), ("v", st.v_arena)):
+        h[nm + "_arena_sha256"] = hashlib.sha256(a.snapshot()).hexdigest()
+        h[nm + "_offsets_sha256"] = hashlib.sha256(
+            a.block_offsets.astype("<u4").tobytes()).hexdigest()
+        h[nm + "_arena_bytes"] = a.size_bytes
+        h[nm + "_blocks"] = len(a)
+        h[nm + "_payload_bits"] = a.payload_bits
+    h["k_lengths"] = st.k_codebook.code_lengths.tolist()
+    h["v_lengths"] = st.v_codebook.code_lengths.tolist()
+    s = kv.collect_stats(st)
+    h["ratio"] = s.compression_ratio
+    h["stats"] = [s.original_bytes, s.compressed_bytes, s.metadata_bytes, s.payload_bits,
+                  s.quantized_values]
+    h["context_len"] = st.context_len
+    h["compressed_tokens"] = st.compressed_tokens
+    h["buffered"] = st.buffered
+    return h
+
+
+def big_digests(do_cfg2=False):
+    import time
+
+    res = {}
+    path = os.path.join(HERE, "big_digests.json")
+    if os.path.exists(path):
+        res = json.load(open(path))
+    # Config 1: H 32 x D 128, ctx 4096, fp16, seed 0, default scales.
+    spec = kv.SyntheticSpec(4096, 32, 128, seed=0)
+    k = kv.generate_synthetic(spec).values.astype(np.float16)
+    v = kv.generate_synthetic(replace(spec, seed=0 ^ 0x9E3779B9)).values.astype(np.float16)
+    cfg_k = kv.QuantConfig(kv.QuantMode.K_BLOCK)
+    cfg_v = kv.QuantConfig(kv.QuantMode.V_TOKEN)
+    t0 = time.time()
+    st = kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v), cfg_k, cfg_v)
+    d = _digest(st)
+    q = np.random.default_rng([0, 0x71726E67]).standard_normal((32, 128), dtype=np.float32)
+    r = kv.attention_step(st, q)
+    d["att_out"] = r.out.tolist()
+    d["att_scores_head0_first64"] = r.scores[0, :64].tolist()
+    res["cfg1"] = d
+    print(f"cfg1 done {time.time()-t0:.1f}s ratio={d['ratio']:.4f}")
+    # Config 4: prefill 4096 then 8192 appends (growing cache), H 32 x 128.
+    t0 = time.time()
+    spec = kv.SyntheticSpec(4096 + 8192, 32, 128, seed=0)
+    kf = kv.generate_synthetic(spec).values.astype(np.float16)
+    vf = kv.generate_synthetic(replace(spec, seed=0 ^ 0x9E3779B9)).values.astype(np.float16)
+    st = kv.LayerCacheState.prefill(kv.CacheTensor(kf[:4096]), kv.CacheTensor(vf[:4096]),
+                                    cfg_k, cfg_v)
+    for t in range(4096, 4096 + 8192):
+        st.append_token(kf[t], vf[t])
+    res["cfg4"] = _digest(st)
+    print(f"cfg4 done {time.time()-t0:.1f}s")
+    if do_cfg2:
+        t0 = time.time()
+        spec = kv.SyntheticSpec(32768, 40, 128, seed=0)
+        k = kv.generate_synthetic(spec).values.astype(np.float16)
+        v = kv.generate_synthetic(replace(spec, seed=0 ^ 0x9E3779B9)).values.astype(np.float16)
+        st = kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v), cfg_k, cfg_v)
+        res["cfg2_slice"] = _digest(st)
+        print(f"cfg2 slice done {time.time()-t0:.1f}s")
+    with open(path, "w") as fh:
+        json.dump(res, fh, indent=1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big", action="store_true")
+    ap.add_argument("--cfg2", action="store_true")
+    args = ap.parse_args()
+    kat_cases()
+    make_case("c_fp16_d128", ctx=64 * 3 + 37, H=2, D=128, bs=64, seed=3, appended=100)
+    make_case("c_f32_d32_bs16", ctx=16 * 5 + 3, H=4, D=32, bs=16, dtype=np.float32,
+              synthetic=False, seed=7, appended=40)
+    make_case("c_fine_scales", ctx=64 * 2 + 10, H=2, D=64, bs=64, rel_k=1 / 255, rel_v=1 / 255,
+              seed=5, appended=0)
+    make_case("c_coarse_scales", ctx=64 * 2 + 1, H=3, D=128, bs=64, rel_k=0.5, rel_v=1.0,
+              seed=6, appended=70)
+    make_case("c_odd_shapes", ctx=8 * 6 + 5, H=3, D=6, bs=8, buffer=16, dtype=np.float32,
+              synthetic=False, seed=8, appended=30)
+    make_case("c_injected_long", ctx=64 * 2 + 5, H=2, D=128, bs=64, seed=9, appended=64,
+              inject=(_fib_lengths(30), _fib_lengths(12)))
+    make_case("c_constant", ctx=32, H=2, D=8, bs=8, dtype=np.float32, constant=(7.5, -2.5),
+              appended=12, inject=(np.eye(256, dtype=np.uint8)[0], np.eye(256, dtype=np.uint8)[0]))
+    make_case("c_prefill_short", ctx=5, H=2, D=16, bs=8, dtype=np.float32, synthetic=False,
+              seed=10, appended=20)
+    if args.big or args.cfg2:
+        big_digests(args.cfg2)
+
+
+if __name__ == "__main__":
+    main()
