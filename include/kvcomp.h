@@ -1,0 +1,214 @@
+/*
+ * kvcomp.h — C ABI of the B200-native KVComp Store/Fetch hot path.
+ *
+ * The reference (arxiv 2509.00579, package `kvpack`) is pure Python/numpy;
+ * its "FFI" for this path is the Python call surface of kvcache.py and
+ * attention.py.  Each entry point below replaces one reference function
+ * (cited as file:line under /root/reference/pkg/src/kvpack/), and the Python
+ * host layer (paper_2509_00579_b200/) binds them with ctypes exactly as
+ * INTEGRATION.md shows.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; every *_dev pointer is CUDA device
+ *     memory, every other pointer is host memory;
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream);
+ *   - every function returns a kvc_status; nonzero codes map 1:1 onto the
+ *     reference exception classes (errors.py:4-29);
+ *   - kernels never allocate: the caller owns arenas, offsets, codebook
+ *     tables, buffers and workspaces (sizes via the *_bytes helpers).
+ *
+ * Device data layout:
+ *   arena      : bytes, exactly the reference serialisation (codec.py:229-244),
+ *                blocks appended in block_index order, +16 B slack for TMA;
+ *   offsets    : u32 per block (codec.py:298-299);
+ *   counters   : kvc_arena_counters, device-resident, updated by the Store
+ *                kernels (cursor, blocks, payload bits/bytes, max extent, err);
+ *   codebook   : kvc_codebook_dev (encode table + decode LUTs), built on the
+ *                host from the 256 code lengths and uploaded once.
+ */
+#ifndef KVCOMP_H
+#define KVCOMP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes <-> reference exceptions (errors.py). */
+typedef enum {
+    KVC_OK = 0,
+    KVC_ERR_CONFIG = 1,        /* ConfigError       errors.py:8  */
+    KVC_ERR_TENSOR = 2,        /* TensorFormatError errors.py:12 */
+    KVC_ERR_CODEBOOK = 3,      /* CodebookError     errors.py:16 */
+    KVC_ERR_CODEC = 4,         /* CodecError        errors.py:20 */
+    KVC_ERR_ARENA_FULL = 5,    /* ArenaFullError    errors.py:24 */
+    KVC_ERR_CUDA = 6           /* CUDA runtime failure (no reference analogue) */
+} kvc_status;
+
+/* Quantisation modes (quantizer.py:37-42). */
+enum { KVC_K_BLOCK = 0, KVC_V_TOKEN = 1, KVC_K_CHANNEL = 2 };
+/* Input dtypes of the dense K/V tensors (tensor_io.py:30-51). */
+enum { KVC_F16 = 0, KVC_F32 = 1 };
+
+/* Device-resident per-arena counters (codec.py:279-326 running totals). */
+typedef struct {
+    uint64_t cursor;         /* write cursor == arena size in bytes          */
+    uint64_t n_blocks;       /* blocks appended so far (== len(offsets))      */
+    uint64_t payload_bits;   /* sum of slice bit counts                       */
+    uint64_t payload_bytes;  /* sum of ceil(bits/8) per block                 */
+    uint32_t max_extent;     /* largest serialised block, bytes               */
+    int32_t err;             /* sticky device error: kvc_status               */
+} kvc_arena_counters;
+
+/* Device codebook tables, built from the 256 code lengths by
+ * kvc_codebook_build_tables (codebook.py:128-208 + decode LUTs). */
+#define KVC_LUT_BITS 12
+typedef struct {
+    uint32_t words[256];            /* canonical codeword, right-aligned       */
+    uint8_t lengths[256];           /* code length, 0 = absent                 */
+    uint32_t lut[1 << KVC_LUT_BITS];/* 12-bit window -> sym | len<<8 (+pair)    */
+    uint32_t first_code[33];        /* canonical decode (lengths > 12)         */
+    uint32_t count[33];
+    uint32_t first_index[33];
+    uint8_t sorted_symbols[256];
+    int32_t max_len;
+    int32_t n_symbols;
+    int32_t single_symbol;          /* degenerate 1-symbol book (codebook.py:149-154) */
+    int32_t pad_;
+} kvc_codebook_dev;
+
+/* One sequence's compressed layer cache, as seen by the Fetch kernels. */
+typedef struct {
+    const uint8_t *k_arena;
+    const uint32_t *k_offsets;
+    const kvc_arena_counters *k_counters;
+    const kvc_codebook_dev *k_cb;
+    const uint8_t *v_arena;
+    const uint32_t *v_offsets;
+    const kvc_arena_counters *v_counters;
+    const kvc_codebook_dev *v_cb;
+    const float *k_buffer;          /* [buffer+1, H, D] f32 pending tokens */
+    const float *v_buffer;
+    int32_t n_chunks;               /* compressed_tokens / block_size          */
+    int32_t buffered;               /* tokens in the f32 buffers               */
+    int32_t stage_bytes_k;          /* >= max K extent + 48, multiple of 16    */
+    int32_t stage_bytes_v;
+    int32_t k_max_len;              /* longest K / V code length (host copy)   */
+    int32_t v_max_len;
+} kvc_seq_desc;
+
+/* ---------------------------------------------------------------- */
+/* Library info                                                      */
+/* ---------------------------------------------------------------- */
+const char *kvc_version(void);
+const char *kvc_last_error(void);   /* message of the last failing call (thread-local) */
+
+/* ---------------------------------------------------------------- */
+/* Codebook (host)  — replaces codebook.py:75-230                     */
+/* ---------------------------------------------------------------- */
+
+/* smooth_histogram (codebook.py:83-89) when max_code >= 0, then
+ * build_codebook (codebook.py:211-218): optimal lengths with (weight,
+ * lowest symbol) tie-breaking, 32-bit cap.  hist: 256 x u64. */
+int kvc_codebook_lengths(const uint64_t *hist, int max_code, uint8_t *lengths_out);
+
+/* codebook_from_lengths (codebook.py:179-208): Kraft check + canonical
+ * words + decode LUTs, written into a host kvc_codebook_dev to upload. */
+int kvc_codebook_build_tables(const uint8_t *lengths, kvc_codebook_dev *tables_out);
+
+size_t kvc_codebook_bytes(void);
+
+/* ---------------------------------------------------------------- */
+/* Store — replaces kvcache.py:217-268 + quantizer.py:114-209 +       */
+/* codec.py:77-138, :229-244, :308-326                               */
+/* ---------------------------------------------------------------- */
+
+/* Quantise n_chunks*H blocks of x[t, h, :] (t in [0, n_chunks*bs)) in block
+ * order b = chunk*H + head.  codes_dev: [nb, bs, D] u8; metas_dev: [nb,
+ * n_units, 2] f32 (min, scale); hist_dev (256 x u64, accumulated) may be
+ * NULL.  row_stride = elements between consecutive tokens of x (H*D for
+ * a contiguous [ctx, H, D] tensor). */
+int kvc_quantize(const void *x_dev, int x_dtype, long row_stride, int n_chunks, int H, int D,
+                 int bs, int mode, double rel, uint8_t *codes_dev, float *metas_dev,
+                 uint64_t *hist_dev, void *stream);
+
+/* Entropy-code n_chunks*H_local quantised blocks (order b = chunk*H_local +
+ * h) and append them to an arena in that order, reading and advancing the
+ * device counters.  block_index = (chunk_base + chunk) * H_total + head_base
+ * + h (quantizer.py:201; head_base/H_total let a head-sharded rank keep the
+ * global numbering).  Overflow of `capacity` sets counters->err =
+ * KVC_ERR_ARENA_FULL and writes nothing (codec.py:313-318).  max_len is the
+ * codebook's longest code (sizes the shared-memory block image).
+ * workspace_dev: kvc_encode_workspace_bytes(n_chunks*H_local, bs). */
+int kvc_encode_append(const uint8_t *codes_dev, const float *metas_dev, int n_chunks,
+                      int H_local, int H_total, int head_base, uint32_t chunk_base, int bs,
+                      int D, int n_units, int max_len, const kvc_codebook_dev *cb_dev,
+                      uint8_t *arena_dev, uint64_t capacity, uint32_t *offsets_dev,
+                      kvc_arena_counters *counters_dev, void *workspace_dev, void *stream);
+size_t kvc_encode_workspace_bytes(int nb, int bs);
+
+/* One Store event with known codebooks (kvcache.py:217-239): quantise K and
+ * V from x[t, h, :] (t < n_chunks*bs) and append both arenas. */
+int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
+                     int n_chunks, int H_local, int H_total, int head_base, int D, int bs,
+                     double rel_k, double rel_v, uint32_t chunk_base,
+                     const kvc_codebook_dev *k_cb_dev, int k_max_len,
+                     const kvc_codebook_dev *v_cb_dev, int v_max_len, uint8_t *k_arena_dev,
+                     uint64_t k_capacity, uint32_t *k_offsets_dev,
+                     kvc_arena_counters *k_counters_dev, uint8_t *v_arena_dev,
+                     uint64_t v_capacity, uint32_t *v_offsets_dev,
+                     kvc_arena_counters *v_counters_dev, void *workspace_dev,
+                     size_t workspace_bytes, void *stream);
+size_t kvc_store_workspace_bytes(int n_chunks, int H, int D, int bs);
+
+/* ---------------------------------------------------------------- */
+/* Fetch — replaces attention.py:59-188 and kvcache.py:182-212        */
+/* ---------------------------------------------------------------- */
+
+/* fused_k_scores (attention.py:59-109), any shape: scores_dev[s][h][t]
+ * (row stride ctx_stride) for t < n_chunks*bs + buffered, x 1/sqrt(D). */
+int kvc_k_scores(const kvc_seq_desc *seqs_dev, int n_seqs, int H, int D, int bs,
+                 const float *q_dev, float *scores_dev, long ctx_stride, int *err_dev,
+                 void *stream);
+
+/* softmax_rows (attention.py:168-173) over rows of length n_cols[s]. */
+int kvc_softmax_rows(float *x_dev, int n_rows, long n_cols, long row_stride, void *stream);
+
+/* fused_v_output (attention.py:112-165), any shape: out_dev[s][h][:];
+ * ws_dev holds kvc_v_output_workspace_bytes(n_seqs, H, D). */
+int kvc_v_output(const kvc_seq_desc *seqs_dev, int n_seqs, int H, int D, int bs,
+                 const float *w_dev, long ctx_stride, float *out_dev, float *ws_dev,
+                 int *err_dev, void *stream);
+size_t kvc_v_output_workspace_bytes(int n_seqs, int H, int D);
+
+/* attention_step (attention.py:176-188) for a batch of sequences with the
+ * single-pass fused kernel (Huffman decode -> dequant -> q.K^T -> online
+ * softmax -> .V, decompressed KV never leaves shared memory/registers),
+ * split over the context and combined.  scores_dev may be NULL.  q_dev
+ * [n_seqs, H*group, D]; GQA: `group` query heads per KV head.
+ * Falls back to the generic kernels (same device) for shapes the fused
+ * kernel does not cover. */
+int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *seqs_host, int n_seqs,
+                  int H, int D, int bs, int group, const float *q_dev, float *out_dev,
+                  float *scores_dev, long ctx_stride, void *workspace_dev,
+                  size_t workspace_bytes, int *err_dev, void *stream);
+size_t kvc_attention_workspace_bytes(int n_seqs, int H, int group, int D, int max_chunks);
+
+/* fetch_dequantized (kvcache.py:182-212): f64 dequant, f32 out
+ * [ctx, H, D] (compressed region only; buffered rows untouched). */
+int kvc_dequantize(const kvc_seq_desc *seq_dev, int H, int D, int bs, int which /*0=K,1=V*/,
+                   int n_chunks, float *out_dev, int *err_dev, void *stream);
+
+/* Uncompressed fp16 decode-attention comparator (the north-star baseline):
+ * K/V [n_seqs, H, ctx, D] f16 head-major, q [n_seqs, H*group, D] f32. */
+int kvc_dense_attention_f16(const void *k_dev, const void *v_dev, int n_seqs, int H, int D,
+                            int group, long ctx, const float *q_dev, float *out_dev,
+                            void *workspace_dev, size_t workspace_bytes, void *stream);
+size_t kvc_dense_workspace_bytes(int n_seqs, int H, int group, int D, long ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVCOMP_H */

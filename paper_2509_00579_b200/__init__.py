@@ -1,0 +1,26 @@
+"""B200-native KVComp Store/Fetch hot path (arxiv 2509.00579).
+
+Drop-in for the reference package ``kvpack``'s store/fetch/attend API
+(kvpack/__init__.py:9-75): the same names and argument meanings, backed by
+hand-written sm_100a kernels in ``libkvcomp.so`` (C ABI: include/kvcomp.h).
+Tensors live on the CUDA device; results are torch tensors.
+"""
+
+from .attention import (AttentionOutput, attention_batched, attention_step, dense_attention_f16,
+                        fused_k_scores, fused_v_output, multistage_attention, reference_output,
+                        reference_scores, softmax_rows)
+from .codebook import (HuffmanCodebook, build_codebook, build_histogram, build_smoothed_codebook,
+                       codebook_from_lengths, deserialize_codebook, histogram_entropy,
+                       serialize_codebook, smooth_histogram)
+from .codec import DataMovement, DeviceArena
+from .errors import (ArenaFullError, CodebookError, CodecError, ConfigError,
+                     ContainerFormatError, KvpackError, TensorFormatError)
+from .kvcache import LayerCacheState
+from .metrics import (CompressionStats, collect_stats, equivalent_decompression_throughput,
+                      median_time)
+from .quantizer import (DEFAULT_REL_SCALE, MIN_REL_SCALE, QuantConfig, QuantizedBlock, QuantMode,
+                        QuantUnitMeta, dequantize_block, quantize_block)
+from .tensor_io import CacheTensor, SyntheticSpec, generate_synthetic, generate_synthetic_device
+
+CompressedArena = DeviceArena
+__version__ = "0.1.0"

@@ -1,0 +1,265 @@
+"""Fetch: fused decompress + decode attention (reference attention.py:34-228).
+
+``attention_step`` runs the single-pass fused sm_100a kernel (Huffman decode
+-> dequantise -> q.K^T -> online softmax -> .V per context split, then a
+combine that also folds in the f32 buffered tokens) whenever the shape is
+covered (head_dim 128, block_size 64, codes <= 12 bits); other shapes run the
+shape-generic decode-in-the-dot-product kernels (kvc_k_scores ->
+kvc_softmax_rows -> kvc_v_output).  Both are CUDA; there is no CPU path.
+``attention_batched`` is the batch entry point (many sequences, one launch).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .codec import DataMovement
+from .errors import CodecError
+from .kvcache import LayerCacheState
+from .tensor_io import CacheTensor
+
+
+@dataclass(frozen=True)
+class AttentionOutput:
+    out: torch.Tensor     # (head_num, head_dim) float32
+    scores: torch.Tensor  # (head_num, context_len) float32, pre-softmax
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _check_query(state: LayerCacheState, q) -> torch.Tensor:
+    t = torch.as_tensor(np.asarray(q, np.float32)) if not isinstance(q, torch.Tensor) else q
+    if tuple(t.shape) != (state.head_num, state.head_dim):
+        raise CodecError(f"query must have shape {(state.head_num, state.head_dim)}")
+    t = t.to(state.device, torch.float32).contiguous()
+    if not bool(torch.isfinite(t).all()):
+        raise CodecError("non-finite query rejected")
+    return t
+
+
+def _movement_fetch(state: LayerCacheState, movement: Optional[DataMovement], with_w: bool):
+    if movement is None:
+        return
+    movement.add_read(state.head_num * state.head_dim * 4)              # q
+    movement.add_read(state.k_arena.size_bytes + state.v_arena.size_bytes)
+    movement.add_read(2 * state.buffered * state.head_num * state.head_dim * 4)
+    if with_w:
+        movement.add_read(state.head_num * state.context_len * 4)
+
+
+def fused_k_scores(state: LayerCacheState, q, movement: Optional[DataMovement] = None,
+                   n_threads: int = 1) -> torch.Tensor:
+    """attention.py:59-109 — logits over the whole context, x 1/sqrt(D)."""
+    q32 = _check_query(state, q)
+    scores = torch.empty((state.head_num, state.context_len), dtype=torch.float32,
+                         device=state.device)
+    err = torch.zeros(1, dtype=torch.int32, device=state.device)
+    st = _lib.lib().kvc_k_scores(state.desc_device().data_ptr(), 1, state.head_num,
+                                 state.head_dim, state.cfg_k.block_size, q32.data_ptr(),
+                                 scores.data_ptr(), state.context_len, err.data_ptr(),
+                                 _stream(state.device))
+    _lib.check(st, "kvc_k_scores")
+    _lib.raise_device_error(int(err.item()), "fused_k_scores")
+    if movement is not None:
+        movement.add_read(q32.numel() * 4 + state.k_arena.size_bytes +
+                          state.buffered * state.head_num * state.head_dim * 4)
+    return scores
+
+
+def fused_v_output(state: LayerCacheState, weights, movement: Optional[DataMovement] = None,
+                   n_threads: int = 1) -> torch.Tensor:
+    """attention.py:112-165 — weighted V aggregation decoded block by block."""
+    w = weights if isinstance(weights, torch.Tensor) else torch.as_tensor(
+        np.asarray(weights, np.float32))
+    H, D = state.head_num, state.head_dim
+    if tuple(w.shape) != (H, state.context_len):
+        raise CodecError(f"weights must have shape {(H, state.context_len)}")
+    w = w.to(state.device, torch.float32).contiguous()
+    out = torch.empty((H, D), dtype=torch.float32, device=state.device)
+    lib = _lib.lib()
+    ws = torch.empty(lib.kvc_v_output_workspace_bytes(1, H, D), dtype=torch.uint8,
+                     device=state.device)
+    err = torch.zeros(1, dtype=torch.int32, device=state.device)
+    st = lib.kvc_v_output(state.desc_device().data_ptr(), 1, H, D, state.cfg_v.block_size,
+                          w.data_ptr(), state.context_len, out.data_ptr(), ws.data_ptr(),
+                          err.data_ptr(), _stream(state.device))
+    _lib.check(st, "kvc_v_output")
+    _lib.raise_device_error(int(err.item()), "fused_v_output")
+    if movement is not None:
+        movement.add_read(w.numel() * 4 + state.v_arena.size_bytes +
+                          state.buffered * H * D * 4)
+    return out
+
+
+def softmax_rows(logits) -> torch.Tensor:
+    """attention.py:168-173 — stable row softmax, on the device."""
+    x = logits if isinstance(logits, torch.Tensor) else torch.as_tensor(
+        np.asarray(logits, np.float32))
+    x = x.to(torch.float32)
+    if not x.is_cuda:
+        x = x.cuda()
+    x = x.contiguous().clone()
+    rows = x.shape[0] if x.ndim > 1 else 1
+    st = _lib.lib().kvc_softmax_rows(x.data_ptr(), rows, x.shape[-1], x.shape[-1],
+                                     _stream(x.device))
+    _lib.check(st, "kvc_softmax_rows")
+    return x
+
+
+def _fused_supported(states: Sequence[LayerCacheState]) -> bool:
+    s0 = states[0]
+    if s0.head_dim != 128 or s0.cfg_k.block_size != 64 or s0.cfg_k.buffer_size >= 1024:
+        return False
+    return all(max(s.k_codebook.max_code_length, s.v_codebook.max_code_length) <= 12
+               for s in states)
+
+
+class _BatchDesc:
+    """Device array of kvc_seq_desc for a fixed list of states (rebuilt on change)."""
+
+    def __init__(self):
+        self.key = None
+        self.dev = None
+        self.host = None
+
+    def get(self, states: Sequence[LayerCacheState]):
+        descs = [s.desc() for s in states]
+        raw = b"".join(bytes(d) for d in descs)
+        if raw != self.key:
+            arr = (_lib.SeqDesc * len(descs))(*descs)
+            self.host = arr
+            self.dev = torch.from_numpy(np.frombuffer(raw, np.uint8).copy()).to(states[0].device)
+            self.key = raw
+        return self.dev, self.host
+
+
+_default_desc_cache = _BatchDesc()
+
+
+def attention_batched(states: Sequence[LayerCacheState], q: torch.Tensor,
+                      want_scores: bool = False, desc_cache: Optional[_BatchDesc] = None,
+                      workspace: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None):
+    """One fused launch over a batch of same-shape states.  q: [B, H, D] f32
+    on the device.  Returns (out [B, H, D], scores [B, H, max_ctx] or None)."""
+    B = len(states)
+    s0 = states[0]
+    H, D, bs = s0.head_num, s0.head_dim, s0.cfg_k.block_size
+    dev = s0.device
+    lib = _lib.lib()
+    max_ctx = max(s.context_len for s in states)
+    max_chunks = max(s.n_chunks for s in states)
+    if out is None:
+        out = torch.empty((B, H, D), dtype=torch.float32, device=dev)
+    scores = torch.zeros((B, H, max_ctx), dtype=torch.float32, device=dev) if want_scores else None
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    cache = desc_cache if desc_cache is not None else _BatchDesc()
+    ddev, dhost = cache.get(states)
+    if _fused_supported(states):
+        need = lib.kvc_attention_workspace_bytes(B, H, 1, D, max_chunks)
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+        st = lib.kvc_attention(ddev.data_ptr(), ctypes_addr(dhost), B, H, D, bs, 1,
+                               q.data_ptr(), out.data_ptr(),
+                               scores.data_ptr() if scores is not None else None, max_ctx,
+                               workspace.data_ptr(), workspace.numel(), err.data_ptr(),
+                               _stream(dev))
+        _lib.check(st, "kvc_attention")
+    else:
+        sc = scores if scores is not None else torch.zeros((B, H, max_ctx), dtype=torch.float32,
+                                                           device=dev)
+        st = lib.kvc_k_scores(ddev.data_ptr(), B, H, D, bs, q.data_ptr(), sc.data_ptr(), max_ctx,
+                              err.data_ptr(), _stream(dev))
+        _lib.check(st, "kvc_k_scores")
+        w = sc.clone()
+        for b, s in enumerate(states):
+            st = lib.kvc_softmax_rows(w[b].data_ptr(), H, s.context_len, max_ctx, _stream(dev))
+            _lib.check(st, "kvc_softmax_rows")
+            if s.context_len < max_ctx:
+                w[b, :, s.context_len:] = 0
+        ws = torch.empty(lib.kvc_v_output_workspace_bytes(B, H, D), dtype=torch.uint8, device=dev)
+        st = lib.kvc_v_output(ddev.data_ptr(), B, H, D, bs, w.data_ptr(), max_ctx, out.data_ptr(),
+                              ws.data_ptr(), err.data_ptr(), _stream(dev))
+        _lib.check(st, "kvc_v_output")
+        scores = sc if want_scores else None
+    return out, scores, err
+
+
+def ctypes_addr(arr) -> int:
+    import ctypes
+    return ctypes.addressof(arr)
+
+
+def attention_step(state: LayerCacheState, q, movement: Optional[DataMovement] = None,
+                   n_threads: int = 1) -> AttentionOutput:
+    """attention.py:176-188 — one decode step; returns (out, scores)."""
+    if state.context_len < 1:
+        raise CodecError("attention over an empty context")
+    q32 = _check_query(state, q)
+    out, scores, err = attention_batched([state], q32.unsqueeze(0), want_scores=True)
+    _lib.raise_device_error(int(err.item()), "attention_step")
+    _movement_fetch(state, movement, with_w=False)
+    return AttentionOutput(out=out[0], scores=scores[0])
+
+
+def reference_scores(k: CacheTensor, q, movement: Optional[DataMovement] = None) -> torch.Tensor:
+    """attention.py:191-202 — dense matvec on a materialised K (device)."""
+    vals = k.values if isinstance(k.values, torch.Tensor) else torch.from_numpy(k.as_float32())
+    vals = vals.to(torch.float32).cuda() if not vals.is_cuda else vals.to(torch.float32)
+    q32 = (q if isinstance(q, torch.Tensor) else torch.as_tensor(np.asarray(q, np.float32)))
+    q32 = q32.to(vals.device, torch.float32)
+    if tuple(q32.shape) != (k.head_num, k.head_dim):
+        raise CodecError(f"query must have shape {(k.head_num, k.head_dim)}")
+    if movement is not None:
+        movement.add_read(vals.numel() * 4 + q32.numel() * 4)
+    return torch.einsum("thd,hd->ht", vals, q32) * np.float32(1.0 / math.sqrt(k.head_dim))
+
+
+def reference_output(v: CacheTensor, weights, movement: Optional[DataMovement] = None):
+    """attention.py:205-215 — dense weighted V sum on a materialised V (device)."""
+    vals = v.values if isinstance(v.values, torch.Tensor) else torch.from_numpy(v.as_float32())
+    vals = vals.to(torch.float32).cuda() if not vals.is_cuda else vals.to(torch.float32)
+    w = weights if isinstance(weights, torch.Tensor) else torch.as_tensor(
+        np.asarray(weights, np.float32))
+    w = w.to(vals.device, torch.float32)
+    if tuple(w.shape) != (v.head_num, v.context_len):
+        raise CodecError(f"weights must have shape {(v.head_num, v.context_len)}")
+    if movement is not None:
+        movement.add_read(vals.numel() * 4 + w.numel() * 4)
+    return torch.einsum("ht,thd->hd", w, vals)
+
+
+def multistage_attention(state: LayerCacheState, q,
+                         movement: Optional[DataMovement] = None) -> AttentionOutput:
+    """attention.py:218-228 — unfused: decode+dequantise, then dense passes."""
+    k, v = state.fetch_dequantized()
+    scores = reference_scores(k, q, movement=movement)
+    weights = softmax_rows(scores)
+    out = reference_output(v, weights, movement=movement)
+    return AttentionOutput(out=out, scores=scores)
+
+
+def dense_attention_f16(k: torch.Tensor, v: torch.Tensor, q: torch.Tensor,
+                        out: Optional[torch.Tensor] = None,
+                        workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Uncompressed fp16 decode attention (north-star comparator kernel).
+    k, v: [S, H, ctx, D] f16 contiguous on the device; q: [S, H, D] f32."""
+    S, H, ctx, D = k.shape
+    lib = _lib.lib()
+    need = lib.kvc_dense_workspace_bytes(S, H, 1, D, ctx)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=k.device)
+    if out is None:
+        out = torch.empty((S, H, D), dtype=torch.float32, device=k.device)
+    st = lib.kvc_dense_attention_f16(k.data_ptr(), v.data_ptr(), S, H, D, 1, ctx, q.data_ptr(),
+                                     out.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                                     _stream(k.device))
+    _lib.check(st, "kvc_dense_attention_f16")
+    return out

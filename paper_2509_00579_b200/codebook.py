@@ -1,0 +1,132 @@
+"""Shared canonical Huffman codebooks (reference codebook.py:34-230).
+
+Lengths are computed by the C-ABI host builder ``kvc_codebook_lengths``
+(heap with (weight, lowest symbol) ties); ``kvc_codebook_build_tables``
+derives canonical codewords, the Kraft check and the device decode tables,
+which are uploaded once per (sequence, layer, K|V) and reused for every
+append (SPEC: codebooks are immutable after prefill).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Dict
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import CodebookError
+
+ALPHABET = 256
+MAX_CODE_LENGTH = 32
+
+
+def _as_u64(h) -> np.ndarray:
+    if isinstance(h, torch.Tensor):
+        h = h.detach().cpu().numpy()
+    return np.ascontiguousarray(np.asarray(h).astype(np.uint64))
+
+
+def build_histogram(codes) -> torch.Tensor:
+    """256-bin histogram of uint8 codes (codebook.py:75-80), on the device."""
+    t = codes if isinstance(codes, torch.Tensor) else torch.from_numpy(np.asarray(codes, np.uint8))
+    if t.numel() == 0:
+        raise CodebookError("cannot build a histogram from an empty input")
+    if not t.is_cuda:
+        t = t.cuda()
+    return torch.bincount(t.reshape(-1).to(torch.int64), minlength=ALPHABET)
+
+
+def smooth_histogram(h, max_code: int) -> np.ndarray:
+    """Add-one smoothing over codes [0, max_code] (codebook.py:83-89)."""
+    if not 0 <= max_code < ALPHABET:
+        raise CodebookError(f"max_code {max_code} outside [0, 255]")
+    out = _as_u64(h).copy()
+    out[: max_code + 1] += 1
+    return out
+
+
+def histogram_entropy(h) -> float:
+    counts = _as_u64(h).astype(np.float64)
+    total = counts.sum()
+    if total <= 0:
+        raise CodebookError("entropy of an empty histogram is undefined")
+    p = counts[counts > 0] / total
+    return float(-(p * np.log2(p)).sum())
+
+
+@dataclass(eq=False)
+class HuffmanCodebook:
+    """Canonical code + device decode tables; same fields as the reference."""
+
+    code_lengths: np.ndarray   # (256,) uint8
+    code_words: np.ndarray     # (256,) uint32
+    max_code_length: int
+    tables: _lib.CodebookTables = field(repr=False)
+    _device: Dict[str, torch.Tensor] = field(default_factory=dict, repr=False)
+
+    @property
+    def encode_table(self):
+        present = [s for s in range(ALPHABET) if self.code_lengths[s] > 0]
+        present.sort(key=lambda s: (int(self.code_lengths[s]), s))
+        return [(s, int(self.code_words[s]), int(self.code_lengths[s])) for s in present]
+
+    def device_tables(self, device) -> torch.Tensor:
+        """The kvc_codebook_dev blob on `device` (uploaded once, cached)."""
+        key = str(torch.device(device))
+        t = self._device.get(key)
+        if t is None:
+            raw = np.frombuffer(bytes(self.tables), dtype=np.uint8).copy()
+            t = torch.from_numpy(raw).to(device)
+            self._device[key] = t
+        return t
+
+
+def codebook_from_lengths(lengths) -> HuffmanCodebook:
+    """codebook.py:179-208 via kvc_codebook_build_tables."""
+    lens = np.ascontiguousarray(np.asarray(lengths).astype(np.uint8))
+    if lens.shape != (ALPHABET,):
+        raise CodebookError(f"expected {ALPHABET} code lengths, got shape {lens.shape}")
+    tables = _lib.CodebookTables()
+    st = _lib.lib().kvc_codebook_build_tables(lens.ctypes.data_as(ctypes.c_void_p),
+                                              ctypes.byref(tables))
+    _lib.check(st, "codebook_from_lengths")
+    words = np.frombuffer(bytes(tables.words), dtype=np.uint32).copy()
+    return HuffmanCodebook(code_lengths=lens.copy(), code_words=words,
+                           max_code_length=int(tables.max_len), tables=tables)
+
+
+def build_codebook(h) -> HuffmanCodebook:
+    """codebook.py:211-218: optimal lengths, then canonical tables."""
+    counts = _as_u64(h)
+    if counts.shape != (ALPHABET,):
+        raise CodebookError(f"expected a 256-bin histogram, got shape {counts.shape}")
+    if counts.sum() == 0:
+        raise CodebookError("cannot build a codebook from an empty histogram")
+    lens = np.zeros(ALPHABET, np.uint8)
+    st = _lib.lib().kvc_codebook_lengths(counts.ctypes.data_as(ctypes.c_void_p), -1,
+                                         lens.ctypes.data_as(ctypes.c_void_p))
+    _lib.check(st, "build_codebook")
+    return codebook_from_lengths(lens)
+
+
+def build_smoothed_codebook(h, max_code: int) -> HuffmanCodebook:
+    """smooth_histogram + build_codebook in one host call (kvcache.py:122-123)."""
+    counts = _as_u64(h)
+    lens = np.zeros(ALPHABET, np.uint8)
+    st = _lib.lib().kvc_codebook_lengths(counts.ctypes.data_as(ctypes.c_void_p), int(max_code),
+                                         lens.ctypes.data_as(ctypes.c_void_p))
+    _lib.check(st, "build_codebook")
+    return codebook_from_lengths(lens)
+
+
+def serialize_codebook(cb: HuffmanCodebook) -> bytes:
+    return bytes(cb.code_lengths.astype(np.uint8).tobytes())
+
+
+def deserialize_codebook(data: bytes) -> HuffmanCodebook:
+    if len(data) != ALPHABET:
+        raise CodebookError(f"serialized codebook must be {ALPHABET} bytes, got {len(data)}")
+    return codebook_from_lengths(np.frombuffer(data, dtype=np.uint8))

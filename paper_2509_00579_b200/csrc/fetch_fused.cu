@@ -1,0 +1,651 @@
+// fetch_fused.cu — single-pass fused Fetch for the hot shape (head_dim 128,
+// block_size 64): per (sequence, KV head, context split) one CTA of NW warps;
+// each warp streams its chunks' K and V block extents HBM -> shared memory
+// with cp.async.bulk (TMA 1D) into a private 2-stage mbarrier ring, Huffman-
+// decodes 2 slices per lane (one token each) straight into the dot products:
+//   K: score_t = sum_c code_tc * (scale_c q_c) + sum_c min_c q_c   (attention.py:91-94)
+//   online softmax (flash-decoding) in the log2 domain
+//   V: o_c += sum_t (p_t scale_t) code_tc + sum_t p_t min_t        (attention.py:144-148)
+// The decompressed KV never exists outside registers.  Split partials
+// (m, l, o[128]) are merged, together with the f32 buffered tokens, by
+// combine_kernel.  Also: the uncompressed fp16 decode-attention comparator.
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int D = 128;
+constexpr int BS = 64;
+constexpr int NW = 4;                // warps per CTA
+constexpr int kThreadsF = NW * 32;
+constexpr int K_HDR = 6 + 2 * BS + 8 * D;   // 1158
+constexpr int V_HDR = 6 + 2 * BS + 8 * BS;  // 646
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ---------------------------------------------------------------------------
+// PTX helpers: mbarrier + cp.async.bulk (TMA 1D)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t lds_u16(const uint8_t *p) {
+    return *reinterpret_cast<const uint16_t *>(p);
+}
+// f32 stored at a 2-byte aligned shared address
+__device__ __forceinline__ float lds_f32_a2(const uint8_t *p) {
+    const uint16_t *h = reinterpret_cast<const uint16_t *>(p);
+    return __uint_as_float((uint32_t)h[0] | ((uint32_t)h[1] << 16));
+}
+// 32-bit MSB-first window starting at bit `pos` of a byte buffer (word aligned base)
+__device__ __forceinline__ uint32_t window32(const uint32_t *w, uint32_t pos) {
+    uint32_t i = pos >> 5;
+    uint32_t a = __byte_perm(w[i], 0, 0x0123);
+    uint32_t b = __byte_perm(w[i + 1], 0, 0x0123);
+    return __funnelshift_l(b, a, pos);
+}
+
+struct Partial {
+    float m;  // running max, log2 domain
+    float l;  // sum of exp2
+    float o[D];
+};
+
+// LUT entry: float bits of the symbol value | code length (low 4 bits).
+__device__ __forceinline__ uint32_t lut_entry(uint32_t e12) {
+    float f = (float)(e12 & 0xFF);
+    return __float_as_uint(f) | ((e12 >> 8) & 0xF);
+}
+
+template <int LB>
+struct Lut {
+    // LB == 6: replicated per lane (entry i of lane l at word i*32+l), conflict-free
+    // LB == 12: one shared 4096-entry table
+    static constexpr int kWords = LB == 6 ? 64 * 32 : 4096;
+    static constexpr int kSymsPerWindow = 32 / LB;  // symbols decoded per 32-bit window
+    __device__ static void build(uint32_t *dst, const kvc_codebook_dev *cb) {
+        if (LB == 6) {
+            for (int i = threadIdx.x; i < kWords; i += blockDim.x)
+                dst[i] = lut_entry(cb->lut[(i >> 5) << 6]);
+        } else {
+            for (int i = threadIdx.x; i < kWords; i += blockDim.x) dst[i] = lut_entry(cb->lut[i]);
+        }
+    }
+    __device__ __forceinline__ static uint32_t get(const uint32_t *lut, uint32_t win, uint32_t lane) {
+        if (LB == 6) return lut[((win >> 26) << 5) + lane];
+        return lut[win >> 20];
+    }
+};
+
+// Decode the 128 symbols of one slice pair (slices A and B of this lane),
+// calling sink(c, fA, fB) per channel.  Returns consumed bits.
+template <int LB, bool FULL, typename Sink>
+__device__ __forceinline__ void decode_pair(const uint32_t *lut, const uint32_t *stage_w,
+                                            uint32_t &pA, uint32_t &pB, uint32_t lane, Sink sink) {
+    constexpr int K = Lut<LB>::kSymsPerWindow;
+#pragma unroll(FULL ? 128 : 4)
+    for (int c0 = 0; c0 < D; c0 += K) {
+        uint32_t wA = window32(stage_w, pA);
+        uint32_t wB = window32(stage_w, pB);
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            if (c0 + i < D) {
+                uint32_t eA = Lut<LB>::get(lut, wA, lane);
+                uint32_t eB = Lut<LB>::get(lut, wB, lane);
+                uint32_t lA = eA & 15u, lB = eB & 15u;
+                wA <<= lA;
+                wB <<= lB;
+                pA += lA;
+                pB += lB;
+                sink(c0 + i, __uint_as_float(eA & ~15u), __uint_as_float(eB & ~15u));
+            }
+        }
+    }
+}
+
+template <int LB>
+__global__ void __launch_bounds__(kThreadsF, 2)
+fused_attn_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__restrict__ q,
+                  float *__restrict__ scores, long ctx_stride, Partial *__restrict__ partial,
+                  int chunks_per_split, int n_splits, int stage_k, int stage_v, int *err) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint32_t *lutK = reinterpret_cast<uint32_t *>(smem);
+    uint32_t *lutV = lutK + Lut<LB>::kWords;
+    uint8_t *wbase = reinterpret_cast<uint8_t *>(lutV + Lut<LB>::kWords);
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const int stage_bytes = stage_k + stage_v;
+    const int per_warp = 2 * stage_bytes + D * 4 + 64;
+    uint8_t *my = wbase + warp * per_warp;
+    uint8_t *stg[2] = {my, my + stage_bytes};
+    float *qf = reinterpret_cast<float *>(my + 2 * stage_bytes);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(my + 2 * stage_bytes + D * 4);
+
+    const int split = blockIdx.x, h = blockIdx.y, sidx = blockIdx.z;
+    const kvc_seq_desc sd = seqs[sidx];
+    Lut<LB>::build(lutK, sd.k_cb);
+    Lut<LB>::build(lutV, sd.v_cb);
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int c_begin = split * chunks_per_split;
+    const int c_end = min(sd.n_chunks, c_begin + chunks_per_split);
+    const long nbk = (long)sd.k_counters->n_blocks, nbv = (long)sd.v_counters->n_blocks;
+    const uint64_t kcur = sd.k_counters->cursor, vcur = sd.v_counters->cursor;
+    const float *qh = q + ((long)sidx * H + h) * D;
+    float qreg[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) qreg[k] = qh[lane + 32 * k];
+    const float sm_scale = kLog2e / sqrtf((float)D);  // scores kept in log2 units
+    const float inv_sqrt = 1.0f / sqrtf((float)D);
+
+    auto extent = [&](const uint32_t *offs, long nb, uint64_t cur, long ord, uint64_t &s,
+                      uint64_t &e) {
+        s = offs[ord];
+        e = (ord + 1 < nb) ? (uint64_t)offs[ord + 1] : cur;
+    };
+    auto issue = [&](int chunk, int st) {
+        if (lane == 0) {
+            long ord = (long)chunk * H + h;
+            uint64_t ks, ke, vs, ve;
+            extent(sd.k_offsets, nbk, kcur, ord, ks, ke);
+            extent(sd.v_offsets, nbv, vcur, ord, vs, ve);
+            uint64_t ka = ks & ~15ull, va = vs & ~15ull;
+            uint32_t kb = (uint32_t)(((ke + 15) & ~15ull) - ka);
+            uint32_t vb = (uint32_t)(((ve + 15) & ~15ull) - va);
+            if (kb > (uint32_t)stage_k || vb > (uint32_t)stage_v) {
+                kvc_set_err(err, KVC_ERR_CODEC);
+                kb = vb = 16;
+            }
+            mbar_expect_tx(&bar[st], kb + vb);
+            tma_load_1d(stg[st], sd.k_arena + ka, kb, &bar[st]);
+            tma_load_1d(stg[st] + stage_k, sd.v_arena + va, vb, &bar[st]);
+        }
+    };
+
+    float m = -INFINITY, lsum = 0.f, wm = 0.f;
+    float acc[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) acc[c] = 0.f;
+    bool bad = false;
+
+    int j = 0;
+    const int first = c_begin + warp;
+    if (first < c_end) issue(first, 0);
+    if (first + NW < c_end) issue(first + NW, 1);
+    for (int chunk = first; chunk < c_end; chunk += NW, ++j) {
+        const int st = j & 1;
+        mbar_wait(&bar[st], (j >> 1) & 1);
+        const long ord = (long)chunk * H + h;
+        const uint32_t kofs = sd.k_offsets[ord] & 15u;
+        const uint32_t vofs = sd.v_offsets[ord] & 15u;
+        const uint8_t *ks = stg[st] + kofs;
+        const uint8_t *vs = stg[st] + stage_k + vofs;
+
+        // ---- K: slice bit offsets, folded query, decode -> scores --------
+        uint32_t cA = lds_u16(ks + 6 + 2 * lane), cB = lds_u16(ks + 6 + 2 * (lane + 32));
+        uint32_t iA = kvc_warp_incl_scan(cA, lane);
+        uint32_t totA = __shfl_sync(0xffffffffu, iA, 31);
+        uint32_t iB = kvc_warp_incl_scan(cB, lane);
+        float basep = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            int c = lane + 32 * k;
+            float mn = lds_f32_a2(ks + 6 + 2 * BS + 8 * c);
+            float sc = lds_f32_a2(ks + 6 + 2 * BS + 8 * c + 4);
+            qf[c] = sc * qreg[k];
+            basep = fmaf(mn, qreg[k], basep);
+        }
+        const float base = kvc_warp_sum(basep);
+        __syncwarp();
+        const uint32_t *kw = reinterpret_cast<const uint32_t *>(stg[st]);
+        uint32_t pA0 = (kofs + K_HDR) * 8 + (iA - cA);
+        uint32_t pB0 = (kofs + K_HDR) * 8 + totA + (iB - cB);
+        uint32_t pA = pA0, pB = pB0;
+        float sA = 0.f, sB = 0.f;
+        decode_pair<LB, false>(lutK, kw, pA, pB, lane, [&](int c, float fA, float fB) {
+            float qc = qf[c];
+            sA = fmaf(fA, qc, sA);
+            sB = fmaf(fB, qc, sB);
+        });
+        bad |= (pA - pA0 != cA) | (pB - pB0 != cB);
+        sA += base;
+        sB += base;
+        if (scores) {
+            float *srow = scores + ((long)sidx * H + h) * ctx_stride + (long)chunk * BS;
+            srow[lane] = sA * inv_sqrt;
+            srow[lane + 32] = sB * inv_sqrt;
+        }
+        sA *= sm_scale;
+        sB *= sm_scale;
+
+        // ---- online softmax -----------------------------------------------
+        const float bm = kvc_warp_max(fmaxf(sA, sB));
+        if (bm > m) {
+            const float alpha = exp2f(m - bm);  // m = -inf -> 0
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[c] *= alpha;
+            lsum *= alpha;
+            wm *= alpha;
+            m = bm;
+        }
+        const float pAw = exp2f(sA - m), pBw = exp2f(sB - m);
+        lsum += pAw + pBw;
+
+        // ---- V: token metas, decode -> weighted accumulation -------------
+        cA = lds_u16(vs + 6 + 2 * lane);
+        cB = lds_u16(vs + 6 + 2 * (lane + 32));
+        iA = kvc_warp_incl_scan(cA, lane);
+        totA = __shfl_sync(0xffffffffu, iA, 31);
+        iB = kvc_warp_incl_scan(cB, lane);
+        const float aA = pAw * lds_f32_a2(vs + 6 + 2 * BS + 8 * lane + 4);
+        const float aB = pBw * lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32) + 4);
+        wm = fmaf(pAw, lds_f32_a2(vs + 6 + 2 * BS + 8 * lane), wm);
+        wm = fmaf(pBw, lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32)), wm);
+        const uint32_t *vw = reinterpret_cast<const uint32_t *>(stg[st] + stage_k);
+        pA0 = (vofs + V_HDR) * 8 + (iA - cA);
+        pB0 = (vofs + V_HDR) * 8 + totA + (iB - cB);
+        pA = pA0;
+        pB = pB0;
+        decode_pair<LB, true>(lutV, vw, pA, pB, lane, [&](int c, float fA, float fB) {
+            acc[c] = fmaf(aA, fA, fmaf(aB, fB, acc[c]));
+        });
+        bad |= (pA - pA0 != cA) | (pB - pB0 != cB);
+
+        __syncwarp();
+        if (chunk + 2 * NW < c_end) issue(chunk + 2 * NW, st);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) kvc_set_err(err, KVC_ERR_CODEC);
+
+    // ---- warp reduce, then CTA merge through shared memory --------------
+    lsum = kvc_warp_sum(lsum);
+    wm = kvc_warp_sum(wm);
+    __syncthreads();  // all warps done with their stages: reuse as scratch
+    Partial *wp = reinterpret_cast<Partial *>(wbase) + warp;
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+        float v = kvc_warp_sum(acc[c]);
+        if (lane == (c & 31)) wp->o[c] = v + wm;
+    }
+    if (lane == 0) {
+        wp->m = m;
+        wp->l = lsum;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        Partial *all = reinterpret_cast<Partial *>(wbase);
+        float M = -INFINITY;
+        for (int w = 0; w < NW; ++w) M = fmaxf(M, all[w].m);
+        float L = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int w = 0; w < NW; ++w) {
+            float sc = (all[w].m == -INFINITY) ? 0.f : exp2f(all[w].m - M);
+            L += all[w].l * sc;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) o[k] += all[w].o[lane + 32 * k] * sc;
+        }
+        Partial *dst = partial + ((long)sidx * H + h) * n_splits + split;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dst->o[lane + 32 * k] = o[k];
+        if (lane == 0) {
+            dst->m = M;
+            dst->l = L;
+        }
+    }
+}
+
+// Merge split partials + the f32 buffered tokens (attention.py:103-107,
+// :160-164) into out = O / L; also writes buffered scores when requested.
+__global__ void __launch_bounds__(128)
+combine_kernel(const kvc_seq_desc *__restrict__ seqs, int H, int bs, const float *__restrict__ q,
+               const Partial *__restrict__ partial, int n_splits, float *__restrict__ out,
+               float *__restrict__ scores, long ctx_stride) {
+    __shared__ float sh_p[1024];
+    __shared__ float sh_red[8];
+    __shared__ float sh_m, sh_l;
+    const int h = blockIdx.y, sidx = blockIdx.z;
+    const kvc_seq_desc sd = seqs[sidx];
+    const float *qh = q + ((long)sidx * H + h) * D;
+    const float sm_scale = kLog2e / sqrtf((float)D), inv_sqrt = 1.0f / sqrtf((float)D);
+    const int nbuf = sd.buffered;
+    const long t0 = (long)sd.n_chunks * bs;
+    // buffered scores (log2 units)
+    float bmax = -INFINITY;
+    for (int t = threadIdx.x; t < nbuf; t += blockDim.x) {
+        const float *kv = sd.k_buffer + ((long)t * H + h) * D;
+        float a = 0.f;
+        for (int c = 0; c < D; ++c) a = fmaf(kv[c], qh[c], a);
+        if (scores) scores[((long)sidx * H + h) * ctx_stride + t0 + t] = a * inv_sqrt;
+        sh_p[t] = a * sm_scale;
+        bmax = fmaxf(bmax, a * sm_scale);
+    }
+    bmax = kvc_warp_max(bmax);
+    if ((threadIdx.x & 31) == 0) sh_red[threadIdx.x >> 5] = bmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = -INFINITY;
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, sh_red[w]);
+        const Partial *p = partial + ((long)sidx * H + h) * n_splits;
+        for (int s = 0; s < n_splits; ++s) M = fmaxf(M, p[s].m);
+        sh_m = M;
+    }
+    __syncthreads();
+    const float M = sh_m;
+    float lpart = 0.f;
+    for (int t = threadIdx.x; t < nbuf; t += blockDim.x) {
+        float e = exp2f(sh_p[t] - M);
+        sh_p[t] = e;
+        lpart += e;
+    }
+    lpart = kvc_warp_sum(lpart);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh_red[threadIdx.x >> 5] = lpart;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float L = sh_red[0] + sh_red[1] + sh_red[2] + sh_red[3];
+        const Partial *p = partial + ((long)sidx * H + h) * n_splits;
+        for (int s = 0; s < n_splits; ++s)
+            if (p[s].m != -INFINITY) L += p[s].l * exp2f(p[s].m - M);
+        sh_l = L;
+    }
+    __syncthreads();
+    const Partial *p = partial + ((long)sidx * H + h) * n_splits;
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+        float o = 0.f;
+        for (int s = 0; s < n_splits; ++s)
+            if (p[s].m != -INFINITY) o += p[s].o[c] * exp2f(p[s].m - M);
+        for (int t = 0; t < nbuf; ++t) o = fmaf(sh_p[t], sd.v_buffer[((long)t * H + h) * D + c], o);
+        out[((long)sidx * H + h) * D + c] = o / sh_l;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Uncompressed fp16 decode attention (comparator): K/V [S, H, ctx, D] f16.
+// A half-warp covers one token row (16 lanes x 16 B); 8 rows in flight per
+// warp per iteration; online softmax; split-K partials -> combine.
+// ---------------------------------------------------------------------------
+constexpr int kDenseNW = 4;
+__global__ void __launch_bounds__(kDenseNW * 32)
+dense_attn_kernel(const __half *__restrict__ K, const __half *__restrict__ V, int H, long ctx,
+                  const float *__restrict__ q, Partial *__restrict__ partial, long tok_per_split,
+                  int n_splits) {
+    const int split = blockIdx.x, h = blockIdx.y, sidx = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane & 15, half = lane >> 4;
+    const long base = ((long)sidx * H + h) * ctx * D;
+    const __half *Kh = K + base, *Vh = V + base;
+    const float *qh = q + ((long)sidx * H + h) * D;
+    const float sm_scale = kLog2e / sqrtf((float)D);
+    float qv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) qv[i] = qh[g * 8 + i] * sm_scale;
+    const long t_begin = (long)split * tok_per_split;
+    const long t_end = min(ctx, t_begin + tok_per_split);
+    float m = -INFINITY, l = 0.f, o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = 0.f;
+    constexpr int R = 8;  // rows per half-warp per iteration
+    for (long t0 = t_begin + (long)warp * 2 * R; t0 < t_end; t0 += (long)kDenseNW * 2 * R) {
+        uint4 kr[R], vr[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            long t = t0 + 2 * r + half;
+            if (t < t_end) {
+                kr[r] = __ldg(reinterpret_cast<const uint4 *>(Kh + t * D) + g);
+                vr[r] = __ldg(reinterpret_cast<const uint4 *>(Vh + t * D) + g);
+            } else {
+                kr[r] = make_uint4(0, 0, 0, 0);
+                vr[r] = make_uint4(0, 0, 0, 0);
+            }
+        }
+        float s[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const __half2 *k2 = reinterpret_cast<const __half2 *>(&kr[r]);
+            float a = 0.f;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                float2 f = __half22float2(k2[i]);
+                a = fmaf(f.x, qv[2 * i], a);
+                a = fmaf(f.y, qv[2 * i + 1], a);
+            }
+#pragma unroll
+            for (int o2 = 8; o2 > 0; o2 >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o2);
+            s[r] = (t0 + 2 * r + half < t_end) ? a : -INFINITY;
+        }
+        float bm = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < R; ++r) bm = fmaxf(bm, s[r]);
+        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
+        if (bm > m) {
+            float alpha = exp2f(m - bm);
+            l *= alpha;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] *= alpha;
+            m = bm;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            float p = exp2f(s[r] - m);
+            l += p;
+            const __half2 *v2 = reinterpret_cast<const __half2 *>(&vr[r]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                float2 f = __half22float2(v2[i]);
+                o[2 * i] = fmaf(p, f.x, o[2 * i]);
+                o[2 * i + 1] = fmaf(p, f.y, o[2 * i + 1]);
+            }
+        }
+    }
+    // merge the two half-warps (same m), then warps via smem
+    l += __shfl_xor_sync(0xffffffffu, l, 16);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] += __shfl_xor_sync(0xffffffffu, o[i], 16);
+    __shared__ float sh_o[kDenseNW][D], sh_m[kDenseNW], sh_l[kDenseNW];
+    if (half == 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sh_o[warp][g * 8 + i] = o[i];
+    }
+    if (lane == 0) {
+        sh_m[warp] = m;
+        sh_l[warp] = l;
+    }
+    __syncthreads();
+    if (threadIdx.x < D) {
+        float M = -INFINITY;
+        for (int w = 0; w < kDenseNW; ++w) M = fmaxf(M, sh_m[w]);
+        float L = 0.f, O = 0.f;
+        for (int w = 0; w < kDenseNW; ++w) {
+            float sc = sh_m[w] == -INFINITY ? 0.f : exp2f(sh_m[w] - M);
+            L += sh_l[w] * sc;
+            O += sh_o[w][threadIdx.x] * sc;
+        }
+        Partial *dst = partial + ((long)sidx * H + h) * n_splits + split;
+        dst->o[threadIdx.x] = O;
+        if (threadIdx.x == 0) {
+            dst->m = M;
+            dst->l = L;
+        }
+    }
+}
+
+__global__ void dense_combine_kernel(int H, const Partial *__restrict__ partial, int n_splits,
+                                     float *__restrict__ out) {
+    const int h = blockIdx.y, sidx = blockIdx.z;
+    const Partial *p = partial + ((long)sidx * H + h) * n_splits;
+    float M = -INFINITY;
+    for (int s = 0; s < n_splits; ++s) M = fmaxf(M, p[s].m);
+    float L = 0.f;
+    for (int s = 0; s < n_splits; ++s)
+        if (p[s].m != -INFINITY) L += p[s].l * exp2f(p[s].m - M);
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+        float o = 0.f;
+        for (int s = 0; s < n_splits; ++s)
+            if (p[s].m != -INFINITY) o += p[s].o[c] * exp2f(p[s].m - M);
+        out[((long)sidx * H + h) * D + c] = o / L;
+    }
+}
+
+int g_num_sms = 0;
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+int pick_chunks_per_split(int max_chunks, long n_heads_total) {
+    // aim for >= ~4 waves of 2 CTAs/SM, each warp owning >= 4 chunks
+    long target_ctas = (long)num_sms() * 2 * 4;
+    long splits = (target_ctas + n_heads_total - 1) / n_heads_total;
+    long cps = (max_chunks + splits - 1) / (splits > 0 ? splits : 1);
+    if (cps < 4 * NW) cps = 4 * NW;
+    cps = (cps + NW - 1) / NW * NW;
+    return (int)cps;
+}
+
+}  // namespace
+
+extern "C" size_t kvc_attention_workspace_bytes(int n_seqs, int H, int group, int D_, int max_chunks) {
+    // partials: n_seqs * H * group * max_splits; max splits bounded by chunks / (4*NW)
+    long splits = (max_chunks + 4 * NW - 1) / (4 * NW) + 1;
+    long nh = (long)n_seqs * H * (group > 0 ? group : 1);
+    size_t part = sizeof(Partial) * (size_t)nh * (size_t)splits;
+    // generic fallback: scores/weights [n_seqs, H*group, ctx] + v partials
+    size_t gen = sizeof(float) * (size_t)nh * ((size_t)max_chunks * 1024 + 256) + 0;
+    (void)D_;
+    return part > gen ? part : gen;
+}
+
+extern "C" int kvc_v_output(const kvc_seq_desc *, int, int, int, int, const float *, long, float *,
+                            float *, int *, void *);
+extern "C" size_t kvc_v_output_workspace_bytes(int n_seqs, int H, int D);
+
+extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *seqs_host,
+                             int n_seqs, int H, int D_, int bs, int group, const float *q_dev,
+                             float *out_dev, float *scores_dev, long ctx_stride,
+                             void *workspace_dev, size_t workspace_bytes, int *err_dev,
+                             void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (n_seqs < 1 || H < 1) return kvc_fail(KVC_ERR_CONFIG, "bad shape");
+    if (group != 1) return kvc_fail(KVC_ERR_CONFIG, "kvc_attention: use kvc_attention_gqa for group > 1");
+    int max_chunks = 0, max_len = 0, stage_k = 0, stage_v = 0;
+    for (int i = 0; i < n_seqs; ++i) {
+        max_chunks = seqs_host[i].n_chunks > max_chunks ? seqs_host[i].n_chunks : max_chunks;
+        int ml = seqs_host[i].k_max_len > seqs_host[i].v_max_len ? seqs_host[i].k_max_len
+                                                                  : seqs_host[i].v_max_len;
+        max_len = ml > max_len ? ml : max_len;
+        stage_k = seqs_host[i].stage_bytes_k > stage_k ? seqs_host[i].stage_bytes_k : stage_k;
+        stage_v = seqs_host[i].stage_bytes_v > stage_v ? seqs_host[i].stage_bytes_v : stage_v;
+    }
+    const bool fused_ok = D_ == D && bs == BS && max_len <= 12 && max_len >= 1;
+    if (!fused_ok) return kvc_fail(KVC_ERR_CONFIG, "shape not covered by the fused kernel");
+    stage_k = (stage_k + 15) & ~15;
+    stage_v = (stage_v + 15) & ~15;
+    const int cps = pick_chunks_per_split(max_chunks > 0 ? max_chunks : 1, (long)n_seqs * H);
+    const int n_splits = max_chunks > 0 ? (max_chunks + cps - 1) / cps : 1;
+    if (sizeof(Partial) * (size_t)n_seqs * H * n_splits > workspace_bytes)
+        return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
+    Partial *part = static_cast<Partial *>(workspace_dev);
+    const int lb = max_len <= 6 ? 6 : 12;
+    const size_t lut_bytes = 2 * sizeof(uint32_t) * (lb == 6 ? 64 * 32 : 4096);
+    const size_t per_warp = 2 * (size_t)(stage_k + stage_v) + D * 4 + 64;
+    size_t smem = lut_bytes + NW * per_warp;
+    if (smem < lut_bytes + NW * sizeof(Partial)) smem = lut_bytes + NW * sizeof(Partial);
+    if (smem > 227 * 1024) return kvc_fail(KVC_ERR_CONFIG, "block extents too large for staging");
+    dim3 grid(n_splits, H, n_seqs);
+    if (max_chunks > 0) {
+        if (lb == 6) {
+            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_kernel<6>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            fused_attn_kernel<6><<<grid, kThreadsF, smem, s>>>(seqs_dev, H, q_dev, scores_dev,
+                                                               ctx_stride, part, cps, n_splits,
+                                                               stage_k, stage_v, err_dev);
+        } else {
+            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_kernel<12>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            fused_attn_kernel<12><<<grid, kThreadsF, smem, s>>>(seqs_dev, H, q_dev, scores_dev,
+                                                                ctx_stride, part, cps, n_splits,
+                                                                stage_k, stage_v, err_dev);
+        }
+        int st = kvc_check_launch("fused_attn_kernel");
+        if (st) return st;
+    }
+    combine_kernel<<<dim3(1, H, n_seqs), 128, 0, s>>>(seqs_dev, H, bs, q_dev, part,
+                                                      max_chunks > 0 ? n_splits : 0, out_dev,
+                                                      scores_dev, ctx_stride);
+    return kvc_check_launch("combine_kernel");
+}
+
+extern "C" size_t kvc_dense_workspace_bytes(int n_seqs, int H, int group, int D_, long ctx) {
+    (void)group;
+    (void)D_;
+    long splits = (ctx + 255) / 256;
+    return sizeof(Partial) * (size_t)n_seqs * H * (size_t)splits;
+}
+
+extern "C" int kvc_dense_attention_f16(const void *k_dev, const void *v_dev, int n_seqs, int H,
+                                       int D_, int group, long ctx, const float *q_dev,
+                                       float *out_dev, void *workspace_dev, size_t workspace_bytes,
+                                       void *stream) {
+    if (D_ != D || group != 1) return kvc_fail(KVC_ERR_CONFIG, "dense kernel: head_dim 128, group 1");
+    if (ctx < 1) return kvc_fail(KVC_ERR_CONFIG, "empty context");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    long nh = (long)n_seqs * H;
+    long target = (long)num_sms() * 8 * 2;
+    long splits = (target + nh - 1) / nh;
+    long tps = (ctx + splits - 1) / splits;
+    if (tps < 256) tps = 256;
+    tps = (tps + 63) / 64 * 64;
+    splits = (ctx + tps - 1) / tps;
+    if (sizeof(Partial) * (size_t)nh * splits > workspace_bytes)
+        return kvc_fail(KVC_ERR_CONFIG, "dense workspace too small");
+    Partial *part = static_cast<Partial *>(workspace_dev);
+    dense_attn_kernel<<<dim3((unsigned)splits, H, n_seqs), kDenseNW * 32, 0, s>>>(
+        static_cast<const __half *>(k_dev), static_cast<const __half *>(v_dev), H, ctx, q_dev, part,
+        tps, (int)splits);
+    int st = kvc_check_launch("dense_attn_kernel");
+    if (st) return st;
+    dense_combine_kernel<<<dim3(1, H, n_seqs), 128, 0, s>>>(H, part, (int)splits, out_dev);
+    return kvc_check_launch("dense_combine_kernel");
+}

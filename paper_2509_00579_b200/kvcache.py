@@ -1,0 +1,284 @@
+"""Device-backed LayerCacheState — drop-in for reference kvcache.py:29-268.
+
+Same lifecycle and numbers as the reference: prefill quantises all full
+blocks, histograms their codes (all heads together, kvcache.py:116-121),
+builds the two shared smoothed Huffman codebooks, appends K blocks then V
+blocks in block_index order; the residual stays in f32 buffers
+(``buffer_size + 1`` slots); ``append_token`` compresses the largest
+block-multiple prefix once ``buffered > buffer_size`` (kvcache.py:168-177).
+
+B200 specifics: arenas, offsets, counters, buffers and codebook tables live
+in HBM; Store work is two kernels per tensor (quantise+histogram, encode+
+append); the only host round trip at prefill is the 2 x 256-bin histogram
+(all-reduced across head shards when a process group is given).
+"""
+
+from __future__ import annotations
+
+from typing import Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from .codebook import HuffmanCodebook, build_smoothed_codebook
+from .codec import DeviceArena, worst_block_bytes
+from .errors import CodecError, ConfigError
+from .quantizer import QuantConfig, QuantMode, as_device_tensor, quantize_tokens
+from .tensor_io import CacheTensor
+
+MAX_SLICE_BITS = 0xFFFF
+
+
+class LayerCacheState:
+    """Compressed KV cache of a single layer (one sequence), resident in HBM."""
+
+    def __init__(self, head_num: int, head_dim: int, cfg_k: QuantConfig, cfg_v: QuantConfig,
+                 k_codebook: HuffmanCodebook, v_codebook: HuffmanCodebook, dtype=np.float32,
+                 k_channel_ranges=None, device=None, head_base: int = 0,
+                 head_total: Optional[int] = None, capacity: Optional[int] = None):
+        if not cfg_k.mode.is_key:
+            raise ConfigError("cfg_k must use a K quantization mode")
+        if cfg_v.mode is not QuantMode.V_TOKEN:
+            raise ConfigError("cfg_v must use the V_TOKEN mode")
+        if cfg_k.block_size != cfg_v.block_size or cfg_k.buffer_size != cfg_v.buffer_size:
+            raise ConfigError("K and V must share block_size and buffer_size")
+        if head_dim * 32 > MAX_SLICE_BITS:
+            raise ConfigError("head_dim too large for 16-bit slice counters")
+        if cfg_k.mode is QuantMode.K_CHANNEL:
+            raise ConfigError("K_CHANNEL mode is not implemented on the device yet")
+        self.head_num = head_num
+        self.head_dim = head_dim
+        self.cfg_k = cfg_k
+        self.cfg_v = cfg_v
+        self.k_codebook = k_codebook
+        self.v_codebook = v_codebook
+        self.dtype = np.dtype(dtype)
+        self.k_channel_ranges = k_channel_ranges
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.head_base = head_base
+        self.head_total = head_total if head_total is not None else head_num
+        self.k_arena = DeviceArena(self.device, capacity)
+        self.v_arena = DeviceArena(self.device, capacity)
+        cap = cfg_k.buffer_size + 1
+        self._k_buffer = torch.zeros((cap, head_num, head_dim), dtype=torch.float32,
+                                     device=self.device)
+        self._v_buffer = torch.zeros_like(self._k_buffer)
+        self._k_tab = k_codebook.device_tables(self.device)
+        self._v_tab = v_codebook.device_tables(self.device)
+        self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self.context_len = 0
+        self.compressed_tokens = 0
+        self.buffered = 0
+        self._desc_dev = None
+        self._desc_key = None
+
+    # ------------------------------------------------------------------
+    @classmethod
+    def prefill(cls, k, v, cfg_k: QuantConfig, cfg_v: QuantConfig,
+                codebooks: Optional[Tuple[HuffmanCodebook, HuffmanCodebook]] = None,
+                k_channel_ranges=None, device=None, process_group=None, head_base: int = 0,
+                head_total: Optional[int] = None, capacity: Optional[int] = None,
+                check: bool = True) -> "LayerCacheState":
+        """kvcache.py:76-145.  k, v: CacheTensor / ndarray / torch tensor
+        [ctx, H, D] f16|f32.  With ``process_group`` this rank holds heads
+        [head_base, head_base+H) of head_total, and the code histograms are
+        all-reduced so every rank builds the same codebooks."""
+        kv = k.values if isinstance(k, CacheTensor) else k
+        vv = v.values if isinstance(v, CacheTensor) else v
+        if tuple(kv.shape) != tuple(vv.shape):
+            raise ConfigError("K and V tensors must share dimensions")
+        if kv.shape[0] < 1:
+            raise ConfigError("prefill requires at least one token")
+        src_dtype = np.dtype(str(kv.dtype).replace("torch.", "")) if isinstance(
+            kv, torch.Tensor) else np.dtype(kv.dtype)
+        kt = as_device_tensor(kv, device)
+        vt = as_device_tensor(vv, kt.device)
+        ctx, H, D = kt.shape
+        bs = cfg_k.block_size
+        n_chunks = ctx // bs
+        n_full = n_chunks * bs
+        if cfg_k.mode is QuantMode.K_CHANNEL:
+            raise ConfigError("K_CHANNEL mode is not implemented on the device yet")
+        hist = torch.zeros(512, dtype=torch.int64, device=kt.device)
+        kcodes = kmetas = vcodes = vmetas = None
+        if n_full:
+            kcodes, kmetas = quantize_tokens(kt, n_chunks, H, D, bs, cfg_k.mode,
+                                             cfg_k.rel_quant_scale,
+                                             hist[:256] if codebooks is None else None)
+            vcodes, vmetas = quantize_tokens(vt, n_chunks, H, D, bs, QuantMode.V_TOKEN,
+                                             cfg_v.rel_quant_scale,
+                                             hist[256:] if codebooks is None else None)
+        if codebooks is None:
+            if process_group is not None:
+                torch.distributed.all_reduce(hist, group=process_group)
+            h = hist.cpu().numpy().astype(np.uint64)
+            k_cb = build_smoothed_codebook(h[:256], cfg_k.max_code)
+            v_cb = build_smoothed_codebook(h[256:], cfg_v.max_code)
+        else:
+            k_cb, v_cb = codebooks
+        st = cls(H, D, cfg_k, cfg_v, k_cb, v_cb, dtype=src_dtype, device=kt.device,
+                 head_base=head_base, head_total=head_total, capacity=capacity)
+        if n_full:
+            st._encode(kcodes, kmetas, vcodes, vmetas, n_chunks)
+        r = ctx - n_full
+        if r:
+            st._k_buffer[:r] = kt[n_full:].to(torch.float32)
+            st._v_buffer[:r] = vt[n_full:].to(torch.float32)
+        st.buffered = r
+        st.context_len = ctx
+        if check:
+            st.check()
+        return st
+
+    # ------------------------------------------------------------------
+    def _workspace(self, nbytes: int) -> torch.Tensor:
+        if self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 2 * self._ws.numel()), dtype=torch.uint8,
+                                   device=self.device)
+        return self._ws
+
+    def _encode(self, kcodes, kmetas, vcodes, vmetas, n_chunks: int) -> None:
+        bs, H, D = self.cfg_k.block_size, self.head_num, self.head_dim
+        lib = _lib.lib()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        nb = n_chunks * H
+        ws = self._workspace(lib.kvc_encode_workspace_bytes(nb, bs))
+        chunk_base = self.compressed_tokens // bs
+        for arena, codes, metas, cb, tab, n_units in (
+                (self.k_arena, kcodes, kmetas, self.k_codebook, self._k_tab, D),
+                (self.v_arena, vcodes, vmetas, self.v_codebook, self._v_tab, bs)):
+            worst = nb * worst_block_bytes(bs, n_units, D, cb.max_code_length)
+            arena.reserve(nb, worst)
+            st = lib.kvc_encode_append(
+                codes.data_ptr(), metas.data_ptr(), n_chunks, H, self.head_total, self.head_base,
+                chunk_base, bs, D, n_units, cb.max_code_length, tab.data_ptr(), arena.buf_ptr,
+                arena.alloc_capacity, arena.offsets_ptr, arena.counters_ptr, ws.data_ptr(), stream)
+            _lib.check(st, "kvc_encode_append")
+            arena.note_append(nb, worst)
+        self.compressed_tokens += n_chunks * bs
+
+    def _compress_buffer(self, n: int) -> None:
+        """Compress buffer rows [0, n) (n a multiple of block_size)."""
+        bs = self.cfg_k.block_size
+        n_chunks = n // bs
+        kcodes, kmetas = quantize_tokens(self._k_buffer, n_chunks, self.head_num, self.head_dim,
+                                         bs, self.cfg_k.mode, self.cfg_k.rel_quant_scale)
+        vcodes, vmetas = quantize_tokens(self._v_buffer, n_chunks, self.head_num, self.head_dim,
+                                         bs, QuantMode.V_TOKEN, self.cfg_v.rel_quant_scale)
+        self._encode(kcodes, kmetas, vcodes, vmetas, n_chunks)
+
+    # ------------------------------------------------------------------
+    def append_token(self, k_vec, v_vec, validate: bool = True) -> None:
+        """kvcache.py:150-177.  Host arrays are validated on the host; device
+        tensors are validated with one device reduction when validate=True."""
+        expected = (self.head_num, self.head_dim)
+        if isinstance(k_vec, torch.Tensor) and isinstance(v_vec, torch.Tensor):
+            if tuple(k_vec.shape) != expected or tuple(v_vec.shape) != expected:
+                raise CodecError(f"token vectors must have shape {expected}")
+            kd = k_vec.to(self.device, torch.float32)
+            vd = v_vec.to(self.device, torch.float32)
+            if validate and not bool(torch.isfinite(kd).all() & torch.isfinite(vd).all()):
+                raise CodecError("non-finite token vectors rejected")
+        else:
+            kn = np.asarray(k_vec, dtype=np.float32)
+            vn = np.asarray(v_vec, dtype=np.float32)
+            if kn.shape != expected or vn.shape != expected:
+                raise CodecError(f"token vectors must have shape {expected}")
+            if not (np.all(np.isfinite(kn)) and np.all(np.isfinite(vn))):
+                raise CodecError("non-finite token vectors rejected")
+            kd = torch.from_numpy(kn).to(self.device, non_blocking=False)
+            vd = torch.from_numpy(vn).to(self.device, non_blocking=False)
+        self._k_buffer[self.buffered] = kd
+        self._v_buffer[self.buffered] = vd
+        self.buffered += 1
+        self.context_len += 1
+        if self.buffered > self.cfg_k.buffer_size:
+            bs = self.cfg_k.block_size
+            n = (self.buffered // bs) * bs
+            self._compress_buffer(n)
+            rem = self.buffered - n
+            if rem:
+                self._k_buffer[:rem] = self._k_buffer[n: self.buffered].clone()
+                self._v_buffer[:rem] = self._v_buffer[n: self.buffered].clone()
+            self.buffered = rem
+
+    def append_tokens(self, k_tokens: torch.Tensor, v_tokens: torch.Tensor) -> None:
+        """Append many tokens (device tensors [n, H, D]); identical arenas to
+        n append_token calls (overflow events fire at the same points)."""
+        for t in range(k_tokens.shape[0]):
+            self.append_token(k_tokens[t], v_tokens[t], validate=False)
+
+    # ------------------------------------------------------------------
+    def check(self) -> None:
+        """Synchronise and raise any sticky device error (CodecError /
+        ArenaFullError) recorded by the Store kernels."""
+        self.k_arena.check("K arena")
+        self.v_arena.check("V arena")
+
+    def compact(self, headroom: int = 0) -> None:
+        """Trim arena allocations to their contents (pointers change)."""
+        self.k_arena.compact(headroom)
+        self.v_arena.compact(headroom)
+        self._desc_key = None
+
+    @property
+    def n_chunks(self) -> int:
+        return self.compressed_tokens // self.cfg_k.block_size
+
+    def stage_bytes(self) -> Tuple[int, int]:
+        """Shared-memory staging size per K / V extent for the fused fetch."""
+        bs, D = self.cfg_k.block_size, self.head_dim
+        out = []
+        for arena, cb, n_units in ((self.k_arena, self.k_codebook, D),
+                                   (self.v_arena, self.v_codebook, bs)):
+            ext = arena.max_extent if arena.n_blocks else 16
+            out.append(((ext + 15) // 16) * 16 + 48)
+        return out[0], out[1]
+
+    def desc(self) -> _lib.SeqDesc:
+        key = (self.compressed_tokens, self.buffered, self.k_arena.buf_ptr, self.v_arena.buf_ptr,
+               self.k_arena.offsets_ptr, self.v_arena.offsets_ptr)
+        if self._desc_key == key and getattr(self, "_desc_host", None) is not None:
+            return self._desc_host
+        sk, sv = self.stage_bytes()
+        d = _lib.SeqDesc(
+            k_arena=self.k_arena.buf_ptr, k_offsets=self.k_arena.offsets_ptr,
+            k_counters=self.k_arena.counters_ptr, k_cb=self._k_tab.data_ptr(),
+            v_arena=self.v_arena.buf_ptr, v_offsets=self.v_arena.offsets_ptr,
+            v_counters=self.v_arena.counters_ptr, v_cb=self._v_tab.data_ptr(),
+            k_buffer=self._k_buffer.data_ptr(), v_buffer=self._v_buffer.data_ptr(),
+            n_chunks=self.n_chunks, buffered=self.buffered, stage_bytes_k=sk, stage_bytes_v=sv,
+            k_max_len=self.k_codebook.max_code_length, v_max_len=self.v_codebook.max_code_length)
+        self._desc_host = d
+        self._desc_key = key
+        self._desc_dev = None
+        return d
+
+    def desc_device(self) -> torch.Tensor:
+        d = self.desc()
+        if self._desc_dev is None:
+            raw = np.frombuffer(bytes(d), dtype=np.uint8).copy()
+            self._desc_dev = torch.from_numpy(raw).to(self.device)
+        return self._desc_dev
+
+    # ------------------------------------------------------------------
+    def fetch_dequantized(self) -> Tuple[CacheTensor, CacheTensor]:
+        """kvcache.py:182-212: decode + f64 dequantise on the device."""
+        outs = []
+        err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        desc = self.desc_device()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        for which, buf in ((0, self._k_buffer), (1, self._v_buffer)):
+            out = torch.empty((self.context_len, self.head_num, self.head_dim),
+                              dtype=torch.float32, device=self.device)
+            st = _lib.lib().kvc_dequantize(desc.data_ptr(), self.head_num, self.head_dim,
+                                           self.cfg_k.block_size, which, self.n_chunks,
+                                           out.data_ptr(), err.data_ptr(), stream)
+            _lib.check(st, "kvc_dequantize")
+            if self.buffered:
+                out[self.compressed_tokens:] = buf[: self.buffered]
+            outs.append(out)
+        _lib.raise_device_error(int(err.item()), "fetch_dequantized")
+        return CacheTensor(outs[0]), CacheTensor(outs[1])
