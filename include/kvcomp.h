@@ -68,15 +68,20 @@ typedef struct {
 typedef struct {
     uint32_t words[256];            /* canonical codeword, right-aligned       */
     uint8_t lengths[256];           /* code length, 0 = absent                 */
-    uint32_t lut[1 << KVC_LUT_BITS];/* 12-bit window -> sym | len<<8 (+pair)    */
+    uint32_t lut[1 << KVC_LUT_BITS];/* 12-bit window -> sym | len<<8            */
+    /* Fused-fetch LUT over 12-bit windows (16-byte aligned for TMA): when
+     * max_len <= 6 each entry decodes exactly two symbols:
+     * (l0+l1) | s0<<16 | s1<<24; otherwise one: l0 | s0<<16.  Low 4 bits =
+     * bits consumed, bits 4..15 zero. */
+    uint32_t fetch_lut[1 << KVC_LUT_BITS];
     uint32_t first_code[33];        /* canonical decode (lengths > 12)         */
     uint32_t count[33];
     uint32_t first_index[33];
     uint8_t sorted_symbols[256];
+    int32_t fetch_syms;             /* 2 (pair LUT) or 1                      */
     int32_t max_len;
     int32_t n_symbols;
     int32_t single_symbol;          /* degenerate 1-symbol book (codebook.py:149-154) */
-    int32_t pad_;
 } kvc_codebook_dev;
 
 /* One sequence's compressed layer cache, as seen by the Fetch kernels. */

@@ -47,11 +47,13 @@ class ArenaCounters(ctypes.Structure):
 
 class CodebookTables(ctypes.Structure):
     _fields_ = [("words", ctypes.c_uint32 * 256), ("lengths", ctypes.c_uint8 * 256),
-                ("lut", ctypes.c_uint32 * (1 << LUT_BITS)), ("first_code", ctypes.c_uint32 * 33),
+                ("lut", ctypes.c_uint32 * (1 << LUT_BITS)),
+                ("fetch_lut", ctypes.c_uint32 * (1 << LUT_BITS)),
+                ("first_code", ctypes.c_uint32 * 33),
                 ("count", ctypes.c_uint32 * 33), ("first_index", ctypes.c_uint32 * 33),
-                ("sorted_symbols", ctypes.c_uint8 * 256), ("max_len", ctypes.c_int32),
-                ("n_symbols", ctypes.c_int32), ("single_symbol", ctypes.c_int32),
-                ("pad_", ctypes.c_int32)]
+                ("sorted_symbols", ctypes.c_uint8 * 256), ("fetch_syms", ctypes.c_int32),
+                ("max_len", ctypes.c_int32), ("n_symbols", ctypes.c_int32),
+                ("single_symbol", ctypes.c_int32)]
 
 
 class SeqDesc(ctypes.Structure):

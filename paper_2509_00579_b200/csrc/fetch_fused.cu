@@ -85,213 +85,338 @@ struct Partial {
     float o[D];
 };
 
-// LUT entry: float bits of the symbol value | code length (low 4 bits).
-__device__ __forceinline__ uint32_t lut_entry(uint32_t e12) {
-    float f = (float)(e12 & 0xFF);
-    return __float_as_uint(f) | ((e12 >> 8) & 0xF);
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
 }
+__device__ __forceinline__ float2 lds64f(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
-template <int LB>
-struct Lut {
-    // LB == 6: replicated per lane (entry i of lane l at word i*32+l), conflict-free
-    // LB == 12: one shared 4096-entry table
-    static constexpr int kWords = LB == 6 ? 64 * 32 : 4096;
-    static constexpr int kSymsPerWindow = 32 / LB;  // symbols decoded per 32-bit window
-    __device__ static void build(uint32_t *dst, const kvc_codebook_dev *cb) {
-        if (LB == 6) {
-            for (int i = threadIdx.x; i < kWords; i += blockDim.x)
-                dst[i] = lut_entry(cb->lut[(i >> 5) << 6]);
-        } else {
-            for (int i = threadIdx.x; i < kWords; i += blockDim.x) dst[i] = lut_entry(cb->lut[i]);
-        }
-    }
-    __device__ __forceinline__ static uint32_t get(const uint32_t *lut, uint32_t win, uint32_t lane) {
-        if (LB == 6) return lut[((win >> 26) << 5) + lane];
-        return lut[win >> 20];
-    }
+// One slice's bit cursor.  `base` = shared byte address of the word holding
+// the slice's first bit; `p` = bit position relative to base.  Only the low
+// 16 bits of p are meaningful: the cursor advances by whole LUT entries
+// (consumed bits in bits 0..3, symbols in bits 16..31), so the high half
+// collects garbage that is masked off where p is used.
+struct Cursor {
+    uint32_t win;
+    uint32_t p;
+    uint32_t base;
 };
 
-// Decode the 128 symbols of one slice pair (slices A and B of this lane),
-// calling sink(c, fA, fB) per channel.  Returns consumed bits.
-template <int LB, bool FULL, typename Sink>
-__device__ __forceinline__ void decode_pair(const uint32_t *lut, const uint32_t *stage_w,
-                                            uint32_t &pA, uint32_t &pB, uint32_t lane, Sink sink) {
-    constexpr int K = Lut<LB>::kSymsPerWindow;
-#pragma unroll(FULL ? 128 : 4)
-    for (int c0 = 0; c0 < D; c0 += K) {
-        uint32_t wA = window32(stage_w, pA);
-        uint32_t wB = window32(stage_w, pB);
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            if (c0 + i < D) {
-                uint32_t eA = Lut<LB>::get(lut, wA, lane);
-                uint32_t eB = Lut<LB>::get(lut, wB, lane);
-                uint32_t lA = eA & 15u, lB = eB & 15u;
-                wA <<= lA;
-                wB <<= lB;
-                pA += lA;
-                pB += lB;
-                sink(c0 + i, __uint_as_float(eA & ~15u), __uint_as_float(eB & ~15u));
-            }
-        }
+__device__ __forceinline__ void cursor_init(Cursor &c, uint32_t stage_addr, uint32_t bit) {
+    c.base = stage_addr + ((bit >> 5) << 2);
+    c.p = bit & 31u;
+    c.win = 0;
+}
+__device__ __forceinline__ void cursor_reload(Cursor &c) {
+    const uint32_t a = c.base + ((c.p >> 3) & 0x1FFCu);
+    const uint32_t w0 = bswap32(lds32(a)), w1 = bswap32(lds32(a + 4));
+    c.win = __funnelshift_l(w1, w0, c.p);
+}
+constexpr uint32_t kMagicBits = 0x4B000000u;  // float 2^23
+__device__ __forceinline__ float sym_hi_byte(uint32_t e, uint32_t sel) {
+    return __uint_as_float(__byte_perm(e, kMagicBits, sel));
+}
+// ---------------------------------------------------------------------------
+// Decoder policies (selected per launch):
+//   MODE 0  lane-replicated 64-entry single-symbol LUT (codes <= 6 bits):
+//           entry i of lane l at word i*32+l, so every lookup is bank-
+//           conflict-free; entry = float bits of the symbol | code length.
+//   MODE 1  shared 4096-entry pair LUT (codes <= 6 bits): one lookup decodes
+//           two symbols; entry = (l0+l1) | s0<<16 | s1<<24.
+//   MODE 2  shared 4096-entry single-symbol LUT (codes <= 12 bits), float|len.
+// In every format the low 4 bits are the bits consumed and bits 4..15 are
+// zero, so `win <<= e` (funnel shift masks to 5 bits) and `p += e` need no
+// field extraction.
+// ---------------------------------------------------------------------------
+template <int MODE>
+struct Dec {
+    static constexpr int kLutWords = MODE == 0 ? 64 * 32 : (1 << KVC_LUT_BITS);
+    static constexpr int kSymsPerWin = MODE == 0 ? 5 : (MODE == 1 ? 4 : 2);
+};
+
+template <int MODE>
+__device__ __forceinline__ uint32_t lut_addr(uint32_t win, uint32_t lut_s, uint32_t lane_s) {
+    if (MODE == 0) return lane_s + ((win >> 26) << 7);   // lane_s = lut_s + 4*lane
+    return lut_s + ((win >> 20) << 2);
+}
+
+// Builds the per-CTA LUT from the codebook's 12-bit decode table.
+template <int MODE>
+__device__ void build_lut(uint32_t *dst, const kvc_codebook_dev *cb) {
+    for (int i = threadIdx.x; i < Dec<MODE>::kLutWords; i += blockDim.x) {
+        uint32_t e12;
+        if (MODE == 0) e12 = cb->lut[(i >> 5) << 6];
+        else if (MODE == 2) e12 = cb->lut[i];
+        else { dst[i] = cb->fetch_lut[i]; continue; }
+        dst[i] = __float_as_uint((float)(e12 & 0xFF)) | ((e12 >> 8) & 0xF);
     }
 }
 
-template <int LB>
+// ---------------------------------------------------------------------------
+// Fused fetch-attention.  Per warp, iteration i decodes K(chunk i) and
+// V(chunk i-1) together (four independent cursors per lane), so the K scores
+// of chunk i update the online softmax while chunk i-1's weights drive the V
+// accumulation.  K and V extents have separate 2-slot TMA rings: at the end
+// of iteration i, K(i+2) and V(i+1) are issued into the slots just freed.
+// Iteration 0 has no V and iteration n has no K: those halves decode a stable
+// dummy stream (the LUT itself) with zero weights and are discarded.
+// ---------------------------------------------------------------------------
+template <int MODE>
 __global__ void __launch_bounds__(kThreadsF, 2)
 fused_attn_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__restrict__ q,
                   float *__restrict__ scores, long ctx_stride, Partial *__restrict__ partial,
                   int chunks_per_split, int n_splits, int stage_k, int stage_v, int *err) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    uint32_t *lutK = reinterpret_cast<uint32_t *>(smem);
-    uint32_t *lutV = lutK + Lut<LB>::kWords;
-    uint8_t *wbase = reinterpret_cast<uint8_t *>(lutV + Lut<LB>::kWords);
+    constexpr int W = Dec<MODE>::kSymsPerWin;
+    __shared__ __align__(128) uint32_t s_lut[2][Dec<MODE>::kLutWords];
+    __shared__ uint64_t s_lbar[1];
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t *lutK = s_lut[0];
+    uint32_t *lutV = s_lut[1];
+    uint8_t *wbase = smem;
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
-    const int stage_bytes = stage_k + stage_v;
-    const int per_warp = 2 * stage_bytes + D * 4 + 64;
+    const int per_warp = 2 * (stage_k + stage_v) + D * 4 + 64;
     uint8_t *my = wbase + warp * per_warp;
-    uint8_t *stg[2] = {my, my + stage_bytes};
-    float *qf = reinterpret_cast<float *>(my + 2 * stage_bytes);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(my + 2 * stage_bytes + D * 4);
+    float *qf = reinterpret_cast<float *>(my + 2 * (stage_k + stage_v));
+    uint64_t *bar = reinterpret_cast<uint64_t *>(my + 2 * (stage_k + stage_v) + D * 4);
+    const uint32_t my_s = smem_u32(my);
+    const uint32_t kslot0 = my_s, vslot0 = my_s + 2 * stage_k;
+    const uint32_t qf_s = smem_u32(qf);
+    const uint32_t lutK_s = smem_u32(lutK), lutV_s = smem_u32(lutV);
+    const uint32_t laneK_s = lutK_s + 4 * lane, laneV_s = lutV_s + 4 * lane;
 
     const int split = blockIdx.x, h = blockIdx.y, sidx = blockIdx.z;
     const kvc_seq_desc sd = seqs[sidx];
-    Lut<LB>::build(lutK, sd.k_cb);
-    Lut<LB>::build(lutV, sd.v_cb);
     if (lane == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mbar_init(&bar[k], 1);
     }
+    if (MODE == 1 && threadIdx.x == 0) mbar_init(s_lbar, 1);
+    fence_mbar_init();
     __syncthreads();
+    if (MODE == 1) {
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(s_lbar, 2u * (4u << KVC_LUT_BITS));
+            tma_load_1d(lutK, sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+            tma_load_1d(lutV, sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+        }
+    } else {
+        build_lut<MODE>(lutK, sd.k_cb);
+        build_lut<MODE>(lutV, sd.v_cb);
+    }
 
     const int c_begin = split * chunks_per_split;
     const int c_end = min(sd.n_chunks, c_begin + chunks_per_split);
+    const int first = c_begin + warp;
+    const int n = first < c_end ? (c_end - first + NW - 1) / NW : 0;
     const long nbk = (long)sd.k_counters->n_blocks, nbv = (long)sd.v_counters->n_blocks;
     const uint64_t kcur = sd.k_counters->cursor, vcur = sd.v_counters->cursor;
     const float *qh = q + ((long)sidx * H + h) * D;
     float qreg[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) qreg[k] = qh[lane + 32 * k];
-    const float sm_scale = kLog2e / sqrtf((float)D);  // scores kept in log2 units
+    const float sm_scale = kLog2e / sqrtf((float)D);
     const float inv_sqrt = 1.0f / sqrtf((float)D);
 
-    auto extent = [&](const uint32_t *offs, long nb, uint64_t cur, long ord, uint64_t &s,
-                      uint64_t &e) {
-        s = offs[ord];
-        e = (ord + 1 < nb) ? (uint64_t)offs[ord + 1] : cur;
-    };
-    auto issue = [&](int chunk, int st) {
+    auto issue = [&](bool is_v, int i) {
         if (lane == 0) {
-            long ord = (long)chunk * H + h;
-            uint64_t ks, ke, vs, ve;
-            extent(sd.k_offsets, nbk, kcur, ord, ks, ke);
-            extent(sd.v_offsets, nbv, vcur, ord, vs, ve);
-            uint64_t ka = ks & ~15ull, va = vs & ~15ull;
-            uint32_t kb = (uint32_t)(((ke + 15) & ~15ull) - ka);
-            uint32_t vb = (uint32_t)(((ve + 15) & ~15ull) - va);
-            if (kb > (uint32_t)stage_k || vb > (uint32_t)stage_v) {
+            const long ord = (long)(first + NW * i) * H + h;
+            const uint32_t *offs = is_v ? sd.v_offsets : sd.k_offsets;
+            const long nb = is_v ? nbv : nbk;
+            const uint64_t s0 = offs[ord];
+            const uint64_t e0 = (ord + 1 < nb) ? (uint64_t)offs[ord + 1] : (is_v ? vcur : kcur);
+            const uint64_t a = s0 & ~15ull;
+            uint32_t bytes = (uint32_t)(((e0 + 15) & ~15ull) - a);
+            const int cap = is_v ? stage_v : stage_k;
+            if (bytes > (uint32_t)cap) {
                 kvc_set_err(err, KVC_ERR_CODEC);
-                kb = vb = 16;
+                bytes = 16;
             }
-            mbar_expect_tx(&bar[st], kb + vb);
-            tma_load_1d(stg[st], sd.k_arena + ka, kb, &bar[st]);
-            tma_load_1d(stg[st] + stage_k, sd.v_arena + va, vb, &bar[st]);
+            uint64_t *b = &bar[(is_v ? 2 : 0) + (i & 1)];
+            uint8_t *dst = my + (is_v ? 2 * stage_k + (i & 1) * stage_v : (i & 1) * stage_k);
+            mbar_expect_tx(b, bytes);
+            tma_load_1d(dst, (is_v ? sd.v_arena : sd.k_arena) + a, bytes, b);
         }
     };
+    if (n > 0) {
+        issue(false, 0);
+        issue(true, 0);
+    }
+    if (n > 1) issue(false, 1);
 
     float m = -INFINITY, lsum = 0.f, wm = 0.f;
-    float acc[D];
+    float2 acc[D / 2];
 #pragma unroll
-    for (int c = 0; c < D; ++c) acc[c] = 0.f;
+    for (int c = 0; c < D / 2; ++c) acc[c] = make_float2(0.f, 0.f);
+    float pwA = 0.f, pwB = 0.f;  // softmax weights of the previous chunk's tokens
     bool bad = false;
+    if (MODE == 1) mbar_wait(s_lbar, 0);
+    else __syncthreads();
 
-    int j = 0;
-    const int first = c_begin + warp;
-    if (first < c_end) issue(first, 0);
-    if (first + NW < c_end) issue(first + NW, 1);
-    for (int chunk = first; chunk < c_end; chunk += NW, ++j) {
-        const int st = j & 1;
-        mbar_wait(&bar[st], (j >> 1) & 1);
-        const long ord = (long)chunk * H + h;
-        const uint32_t kofs = sd.k_offsets[ord] & 15u;
-        const uint32_t vofs = sd.v_offsets[ord] & 15u;
-        const uint8_t *ks = stg[st] + kofs;
-        const uint8_t *vs = stg[st] + stage_k + vofs;
-
-        // ---- K: slice bit offsets, folded query, decode -> scores --------
-        uint32_t cA = lds_u16(ks + 6 + 2 * lane), cB = lds_u16(ks + 6 + 2 * (lane + 32));
-        uint32_t iA = kvc_warp_incl_scan(cA, lane);
-        uint32_t totA = __shfl_sync(0xffffffffu, iA, 31);
-        uint32_t iB = kvc_warp_incl_scan(cB, lane);
-        float basep = 0.f;
+    for (int i = 0; i <= n; ++i) {
+        const bool hasK = i < n, hasV = i > 0;
+        Cursor cur[4];  // kA, kB, vA, vB
+        uint32_t cnt[4] = {0, 0, 0, 0};
+        float base = 0.f;
+        float2 aA2 = make_float2(0.f, 0.f), aB2 = aA2;
+        if (hasK) {
+            mbar_wait(&bar[i & 1], (i >> 1) & 1);
+            const long ord = (long)(first + NW * i) * H + h;
+            const uint32_t kofs = sd.k_offsets[ord] & 15u;
+            const uint8_t *ks = my + (i & 1) * stage_k + kofs;
+            cnt[0] = lds_u16(ks + 6 + 2 * lane);
+            cnt[1] = lds_u16(ks + 6 + 2 * (lane + 32));
+            const uint32_t iA = kvc_warp_incl_scan(cnt[0], lane);
+            const uint32_t totA = __shfl_sync(0xffffffffu, iA, 31);
+            const uint32_t iB = kvc_warp_incl_scan(cnt[1], lane);
+            float basep = 0.f;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            int c = lane + 32 * k;
-            float mn = lds_f32_a2(ks + 6 + 2 * BS + 8 * c);
-            float sc = lds_f32_a2(ks + 6 + 2 * BS + 8 * c + 4);
-            qf[c] = sc * qreg[k];
-            basep = fmaf(mn, qreg[k], basep);
+            for (int k = 0; k < 4; ++k) {
+                const int c = lane + 32 * k;
+                const float mn = lds_f32_a2(ks + 6 + 2 * BS + 8 * c);
+                const float sc = lds_f32_a2(ks + 6 + 2 * BS + 8 * c + 4);
+                qf[c] = sc * qreg[k];
+                basep = fmaf(mn, qreg[k], basep);
+            }
+            base = kvc_warp_sum(basep);
+            const uint32_t bit0 = (kofs + K_HDR) * 8;
+            const uint32_t slot = kslot0 + (i & 1) * stage_k;
+            cursor_init(cur[0], slot, bit0 + iA - cnt[0]);
+            cursor_init(cur[1], slot, bit0 + totA + iB - cnt[1]);
+        } else {
+            cursor_init(cur[0], lutK_s, 0);
+            cursor_init(cur[1], lutK_s, 0);
         }
-        const float base = kvc_warp_sum(basep);
-        __syncwarp();
-        const uint32_t *kw = reinterpret_cast<const uint32_t *>(stg[st]);
-        uint32_t pA0 = (kofs + K_HDR) * 8 + (iA - cA);
-        uint32_t pB0 = (kofs + K_HDR) * 8 + totA + (iB - cB);
-        uint32_t pA = pA0, pB = pB0;
-        float sA = 0.f, sB = 0.f;
-        decode_pair<LB, false>(lutK, kw, pA, pB, lane, [&](int c, float fA, float fB) {
-            float qc = qf[c];
-            sA = fmaf(fA, qc, sA);
-            sB = fmaf(fB, qc, sB);
-        });
-        bad |= (pA - pA0 != cA) | (pB - pB0 != cB);
-        sA += base;
-        sB += base;
-        if (scores) {
-            float *srow = scores + ((long)sidx * H + h) * ctx_stride + (long)chunk * BS;
-            srow[lane] = sA * inv_sqrt;
-            srow[lane + 32] = sB * inv_sqrt;
+        if (hasV) {
+            const int j = i - 1;
+            mbar_wait(&bar[2 + (j & 1)], (j >> 1) & 1);
+            const long ord = (long)(first + NW * j) * H + h;
+            const uint32_t vofs = sd.v_offsets[ord] & 15u;
+            const uint8_t *vs = my + 2 * stage_k + (j & 1) * stage_v + vofs;
+            cnt[2] = lds_u16(vs + 6 + 2 * lane);
+            cnt[3] = lds_u16(vs + 6 + 2 * (lane + 32));
+            const uint32_t iA = kvc_warp_incl_scan(cnt[2], lane);
+            const uint32_t totA = __shfl_sync(0xffffffffu, iA, 31);
+            const uint32_t iB = kvc_warp_incl_scan(cnt[3], lane);
+            const float aA = pwA * lds_f32_a2(vs + 6 + 2 * BS + 8 * lane + 4);
+            const float aB = pwB * lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32) + 4);
+            wm = fmaf(pwA, lds_f32_a2(vs + 6 + 2 * BS + 8 * lane), wm);
+            wm = fmaf(pwB, lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32)), wm);
+            aA2 = make_float2(aA, aA);
+            aB2 = make_float2(aB, aB);
+            const uint32_t bit0 = (vofs + V_HDR) * 8;
+            const uint32_t slot = vslot0 + (j & 1) * stage_v;
+            cursor_init(cur[2], slot, bit0 + iA - cnt[2]);
+            cursor_init(cur[3], slot, bit0 + totA + iB - cnt[3]);
+        } else {
+            cursor_init(cur[2], lutV_s, 0);
+            cursor_init(cur[3], lutV_s, 0);
         }
-        sA *= sm_scale;
-        sB *= sm_scale;
-
-        // ---- online softmax -----------------------------------------------
-        const float bm = kvc_warp_max(fmaxf(sA, sB));
-        if (bm > m) {
-            const float alpha = exp2f(m - bm);  // m = -inf -> 0
+        uint32_t p0[4];
 #pragma unroll
-            for (int c = 0; c < D; ++c) acc[c] *= alpha;
-            lsum *= alpha;
-            wm *= alpha;
-            m = bm;
-        }
-        const float pAw = exp2f(sA - m), pBw = exp2f(sB - m);
-        lsum += pAw + pBw;
-
-        // ---- V: token metas, decode -> weighted accumulation -------------
-        cA = lds_u16(vs + 6 + 2 * lane);
-        cB = lds_u16(vs + 6 + 2 * (lane + 32));
-        iA = kvc_warp_incl_scan(cA, lane);
-        totA = __shfl_sync(0xffffffffu, iA, 31);
-        iB = kvc_warp_incl_scan(cB, lane);
-        const float aA = pAw * lds_f32_a2(vs + 6 + 2 * BS + 8 * lane + 4);
-        const float aB = pBw * lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32) + 4);
-        wm = fmaf(pAw, lds_f32_a2(vs + 6 + 2 * BS + 8 * lane), wm);
-        wm = fmaf(pBw, lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32)), wm);
-        const uint32_t *vw = reinterpret_cast<const uint32_t *>(stg[st] + stage_k);
-        pA0 = (vofs + V_HDR) * 8 + (iA - cA);
-        pB0 = (vofs + V_HDR) * 8 + totA + (iB - cB);
-        pA = pA0;
-        pB = pB0;
-        decode_pair<LB, true>(lutV, vw, pA, pB, lane, [&](int c, float fA, float fB) {
-            acc[c] = fmaf(aA, fA, fmaf(aB, fB, acc[c]));
-        });
-        bad |= (pA - pA0 != cA) | (pB - pB0 != cB);
-
+        for (int k = 0; k < 4; ++k) p0[k] = cur[k].p;
         __syncwarp();
-        if (chunk + 2 * NW < c_end) issue(chunk + 2 * NW, st);
+
+        float2 sA2 = make_float2(0.f, 0.f), sB2 = sA2;
+        if (MODE == 1) {
+#pragma unroll
+            for (int c2 = 0; c2 < D / 2; ++c2) {
+                if (c2 % 2 == 0) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) cursor_reload(cur[k]);
+                }
+                uint32_t e[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    e[k] = lds32(lut_addr<1>(cur[k].win, k < 2 ? lutK_s : lutV_s, 0));
+                    cur[k].win = __funnelshift_l(0u, cur[k].win, e[k]);
+                    cur[k].p += e[k];
+                }
+                const float2 magic = make_float2(-8388608.f, -8388608.f);
+                float2 f[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    f[k] = __fadd2_rn(make_float2(sym_hi_byte(e[k], 0x7652),
+                                                  sym_hi_byte(e[k], 0x7653)), magic);
+                const float2 q2 = lds64f(qf_s + 8 * c2);
+                sA2 = __ffma2_rn(f[0], q2, sA2);
+                sB2 = __ffma2_rn(f[1], q2, sB2);
+                acc[c2] = __ffma2_rn(f[2], aA2, acc[c2]);
+                acc[c2] = __ffma2_rn(f[3], aB2, acc[c2]);
+            }
+        } else {
+            uint32_t e0[4];
+#pragma unroll
+            for (int s = 0; s < D; ++s) {
+                if (s % W == 0) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) cursor_reload(cur[k]);
+                }
+                uint32_t e[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    e[k] = lds32(lut_addr<MODE>(cur[k].win, k < 2 ? lutK_s : lutV_s,
+                                                k < 2 ? laneK_s : laneV_s));
+                    cur[k].win = __funnelshift_l(0u, cur[k].win, e[k]);
+                    cur[k].p += e[k];
+                }
+                if (s & 1) {
+                    float2 f[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        f[k] = make_float2(__uint_as_float(e0[k] & ~15u),
+                                           __uint_as_float(e[k] & ~15u));
+                    const float2 q2 = lds64f(qf_s + 4 * (s - 1));
+                    sA2 = __ffma2_rn(f[0], q2, sA2);
+                    sB2 = __ffma2_rn(f[1], q2, sB2);
+                    acc[s / 2] = __ffma2_rn(f[2], aA2, acc[s / 2]);
+                    acc[s / 2] = __ffma2_rn(f[3], aB2, acc[s / 2]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) e0[k] = e[k];
+                }
+            }
+        }
+        if (hasK)
+            bad |= (((cur[0].p - p0[0]) & 0xFFFFu) != cnt[0]) |
+                   (((cur[1].p - p0[1]) & 0xFFFFu) != cnt[1]);
+        if (hasV)
+            bad |= (((cur[2].p - p0[2]) & 0xFFFFu) != cnt[2]) |
+                   (((cur[3].p - p0[3]) & 0xFFFFu) != cnt[3]);
+        __syncwarp();
+        if (hasK && i + 2 < n) issue(false, i + 2);
+        if (i + 1 < n) issue(true, i + 1);
+
+        if (hasK) {
+            const int chunk = first + NW * i;
+            float sA = sA2.x + sA2.y + base, sB = sB2.x + sB2.y + base;
+            if (scores) {
+                float *srow = scores + ((long)sidx * H + h) * ctx_stride + (long)chunk * BS;
+                srow[lane] = sA * inv_sqrt;
+                srow[lane + 32] = sB * inv_sqrt;
+            }
+            sA *= sm_scale;
+            sB *= sm_scale;
+            const float bm = kvc_warp_max(fmaxf(sA, sB));
+            if (bm > m) {
+                const float alpha = exp2f(m - bm);
+                const float2 al2 = make_float2(alpha, alpha);
+#pragma unroll
+                for (int c = 0; c < D / 2; ++c) acc[c] = __fmul2_rn(acc[c], al2);
+                lsum *= alpha;
+                wm *= alpha;
+                m = bm;
+            }
+            pwA = exp2f(sA - m);
+            pwB = exp2f(sB - m);
+            lsum += pwA + pwB;
+        }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) kvc_set_err(err, KVC_ERR_CODEC);
 
@@ -301,9 +426,13 @@ fused_attn_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__r
     __syncthreads();  // all warps done with their stages: reuse as scratch
     Partial *wp = reinterpret_cast<Partial *>(wbase) + warp;
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
-        float v = kvc_warp_sum(acc[c]);
-        if (lane == (c & 31)) wp->o[c] = v + wm;
+    for (int c = 0; c < D / 2; ++c) {
+        const float vx = kvc_warp_sum(acc[c].x);
+        const float vy = kvc_warp_sum(acc[c].y);
+        if (lane == ((2 * c) & 31)) {
+            wp->o[2 * c] = vx + wm;
+            wp->o[2 * c + 1] = vy + wm;
+        }
     }
     if (lane == 0) {
         wp->m = m;
@@ -316,7 +445,7 @@ fused_attn_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__r
         for (int w = 0; w < NW; ++w) M = fmaxf(M, all[w].m);
         float L = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
         for (int w = 0; w < NW; ++w) {
-            float sc = (all[w].m == -INFINITY) ? 0.f : exp2f(all[w].m - M);
+            const float sc = (all[w].m == -INFINITY) ? 0.f : exp2f(all[w].m - M);
             L += all[w].l * sc;
 #pragma unroll
             for (int k = 0; k < 4; ++k) o[k] += all[w].o[lane + 32 * k] * sc;
@@ -587,27 +716,34 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
     if (sizeof(Partial) * (size_t)n_seqs * H * n_splits > workspace_bytes)
         return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
     Partial *part = static_cast<Partial *>(workspace_dev);
-    const int lb = max_len <= 6 ? 6 : 12;
-    const size_t lut_bytes = 2 * sizeof(uint32_t) * (lb == 6 ? 64 * 32 : 4096);
+    // decoder: pair LUT12 when every code is <= 6 bits (measured fastest, see
+    // profiles/), else single-symbol LUT12; env KVC_FUSED_MODE=0|1 overrides.
+    int mode = max_len <= 6 ? 1 : 2;
+    if (max_len <= 6) {
+        const char *env = getenv("KVC_FUSED_MODE");
+        if (env && (env[0] == '0' || env[0] == '1')) mode = env[0] - '0';
+    }
     const size_t per_warp = 2 * (size_t)(stage_k + stage_v) + D * 4 + 64;
-    size_t smem = lut_bytes + NW * per_warp;
-    if (smem < lut_bytes + NW * sizeof(Partial)) smem = lut_bytes + NW * sizeof(Partial);
-    if (smem > 227 * 1024) return kvc_fail(KVC_ERR_CONFIG, "block extents too large for staging");
+    size_t smem = NW * per_warp;  // dynamic part (LUTs are static)
+    if (smem < NW * sizeof(Partial)) smem = NW * sizeof(Partial);
+    const size_t lut_bytes = mode == 0 ? 2 * 8192 : 2 * 16384;
+    if (smem + lut_bytes + 256 > 227 * 1024)
+        return kvc_fail(KVC_ERR_CONFIG, "block extents too large for staging");
     dim3 grid(n_splits, H, n_seqs);
     if (max_chunks > 0) {
-        if (lb == 6) {
-            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_kernel<6>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            fused_attn_kernel<6><<<grid, kThreadsF, smem, s>>>(seqs_dev, H, q_dev, scores_dev,
-                                                               ctx_stride, part, cps, n_splits,
-                                                               stage_k, stage_v, err_dev);
-        } else {
-            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_kernel<12>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            fused_attn_kernel<12><<<grid, kThreadsF, smem, s>>>(seqs_dev, H, q_dev, scores_dev,
-                                                                ctx_stride, part, cps, n_splits,
-                                                                stage_k, stage_v, err_dev);
-        }
+#define KVC_LAUNCH_FUSED(M)                                                                   \
+    do {                                                                                      \
+        KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_kernel<M>,                               \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                          (int)smem));                                        \
+        fused_attn_kernel<M><<<grid, kThreadsF, smem, s>>>(seqs_dev, H, q_dev, scores_dev,    \
+                                                           ctx_stride, part, cps, n_splits,   \
+                                                           stage_k, stage_v, err_dev);        \
+    } while (0)
+        if (mode == 0) KVC_LAUNCH_FUSED(0);
+        else if (mode == 1) KVC_LAUNCH_FUSED(1);
+        else KVC_LAUNCH_FUSED(2);
+#undef KVC_LAUNCH_FUSED
         int st = kvc_check_launch("fused_attn_kernel");
         if (st) return st;
     }

@@ -91,6 +91,29 @@ extern "C" int kvc_codebook_lengths(const uint64_t *hist, int max_code, uint8_t 
     return KVC_OK;
 }
 
+// Fused-fetch LUT (see kvcomp.h): two symbols per 12-bit window when every
+// code is <= 6 bits (the second code then always fits the remaining bits).
+static void build_fetch_lut(kvc_codebook_dev *t) {
+    const int pair = t->max_len <= 6;
+    t->fetch_syms = pair ? 2 : 1;
+    for (uint32_t i = 0; i < (1u << KVC_LUT_BITS); ++i) {
+        uint32_t e0 = t->lut[i];
+        uint32_t l0 = (e0 >> 8) & 0xFF, s0 = e0 & 0xFF;
+        if (!l0 || t->max_len > KVC_LUT_BITS) {
+            t->fetch_lut[i] = 0;
+            continue;
+        }
+        if (pair) {
+            uint32_t rest = (i << l0) & ((1u << KVC_LUT_BITS) - 1);
+            uint32_t e1 = t->lut[rest];
+            uint32_t l1 = (e1 >> 8) & 0xFF, s1 = e1 & 0xFF;
+            t->fetch_lut[i] = (l0 + l1) | (s0 << 16) | (s1 << 24);
+        } else {
+            t->fetch_lut[i] = l0 | (s0 << 16);
+        }
+    }
+}
+
 extern "C" int kvc_codebook_build_tables(const uint8_t *lengths, kvc_codebook_dev *t) {
     if (!lengths || !t) return kvc_fail(KVC_ERR_CONFIG, "null argument");
     std::memset(t, 0, sizeof(*t));
@@ -117,6 +140,7 @@ extern "C" int kvc_codebook_build_tables(const uint8_t *lengths, kvc_codebook_de
         t->first_index[1] = 0;
         t->sorted_symbols[0] = (uint8_t)only;
         t->sorted_symbols[1] = (uint8_t)only;
+        build_fetch_lut(t);
         return KVC_OK;
     }
     uint64_t kraft = 0;
@@ -149,5 +173,6 @@ extern "C" int kvc_codebook_build_tables(const uint8_t *lengths, kvc_codebook_de
         uint32_t hi = (t->words[s] + 1) << (KVC_LUT_BITS - l);
         for (uint32_t i = lo; i < hi; ++i) t->lut[i] = (uint32_t)s | ((uint32_t)l << 8);
     }
+    build_fetch_lut(t);
     return KVC_OK;
 }
