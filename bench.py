@@ -167,7 +167,8 @@ def run_reference(args, rank, world):
 # GPU side
 # ---------------------------------------------------------------------------
 
-def build_cache(kv, torch, layers, batch, ctx, heads_total, head_base, heads_local, device):
+def build_cache(kv, torch, layers, batch, ctx, heads_total, head_base, heads_local, device,
+                group=None):
     """Prefill layers x batch compressed states (this rank's head shard)."""
     cfg_k = kv.QuantConfig(kv.QuantMode.K_BLOCK)
     cfg_v = kv.QuantConfig(kv.QuantMode.V_TOKEN)
@@ -190,7 +191,8 @@ def build_cache(kv, torch, layers, batch, ctx, heads_total, head_base, heads_loc
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             st = kv.LayerCacheState.prefill(ks, vs, cfg_k, cfg_v, head_base=head_base,
-                                            head_total=heads_total, check=False)
+                                            head_total=heads_total, check=False,
+                                            process_group=group)
             torch.cuda.synchronize()
             store_times.append(time.perf_counter() - t0)
             store_bytes = 2 * ctx * heads_local * 128 * 2
@@ -238,7 +240,8 @@ def main():
     hb = rank * hl
     L, B, T, H = args.layers, args.batch, args.ctx, args.heads
 
-    states, store_times, store_bytes = build_cache(kv, torch, L, B, T, H, hb, hl, device)
+    states, store_times, store_bytes = build_cache(kv, torch, L, B, T, H, hb, hl, device,
+                                                   group=dist.group.WORLD if world > 1 else None)
     comp_bytes_layer = []
     for row in states:
         comp_bytes_layer.append(sum(s.k_arena.size_bytes + s.v_arena.size_bytes +

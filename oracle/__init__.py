@@ -58,6 +58,8 @@ def lib():
             "orc_encode_block": (i, [P, i, i, P, P, i, ctypes.c_uint32, P, P, P, P]),
             "orc_decode_block": (i, [P, l, i, i, P, P, P, P, P, P]),
             "orc_compress_tokens": (i, [P, i, i, i, i, i, d, ctypes.c_uint32, P, P, l, P, P, P, i]),
+            "orc_compress_tokens_shard": (i, [P, i, i, i, i, i, d, ctypes.c_uint32, i, i, P, P, l,
+                                              P, P, P, i]),
             "orc_tokens_histogram": (i, [P, i, i, i, i, i, d, P, i]),
             "orc_k_scores": (i, [P, P, l, l, i, i, i, P, P, P, i, l, P, i]),
             "orc_softmax_rows": (None, [P, l, l, P]),
@@ -319,6 +321,37 @@ class OracleState:
     def compression_ratio(self):
         o, c, m, _, _ = self.stats()
         return o / (c + m)
+
+
+def compress_shard(tokens, bs, mode, rel, lengths, H_total, head_base, chunk_base=0,
+                   n_threads=1):
+    """Encode a head shard [n, H_local, D] into (arena bytes, offsets) with global
+    block indices."""
+    tokens = np.ascontiguousarray(tokens, np.float32)
+    n, H, D = tokens.shape
+    m = 1 if mode == "vtoken" else 0
+    nb = (n // bs) * H
+    n_units = bs if m else D
+    buf = np.zeros(nb * (6 + 2 * bs + 8 * n_units + bs * D * 4 + 4) + 16, np.uint8)
+    cursor = ctypes.c_long(0)
+    offs = np.zeros(max(nb, 1), np.uint32)
+    bits = np.zeros(max(nb, 1), np.uint64)
+    lengths = np.ascontiguousarray(lengths, np.uint8)
+    _chk(lib().orc_compress_tokens_shard(_p(tokens), n, H, D, bs, m, float(rel), chunk_base,
+                                         H_total, head_base, _p(lengths), _p(buf), -1,
+                                         ctypes.byref(cursor), _p(offs), _p(bits), n_threads),
+         "compress_shard")
+    return buf[: cursor.value].tobytes(), offs[:nb].copy()
+
+
+def tokens_histogram(tokens, bs, mode, rel, n_threads=1):
+    tokens = np.ascontiguousarray(tokens, np.float32)
+    n, H, D = tokens.shape
+    h = np.zeros(256, np.uint64)
+    _chk(lib().orc_tokens_histogram(_p(tokens), (n // bs) * bs, H, D, bs,
+                                    1 if mode == "vtoken" else 0, float(rel), _p(h), n_threads),
+         "histogram")
+    return h
 
 
 def softmax_rows(x):

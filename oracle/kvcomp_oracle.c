@@ -386,6 +386,7 @@ int orc_decode_block(const uint8_t *ext, long len, int n_units, int D, const uin
 
 typedef struct {
     const float *tokens; int H, D, bs, mode, n_units; double rel; uint32_t chunk_base;
+    int H_total, head_base;
     const uint8_t *lengths; const uint32_t *words; uint8_t *tmp; long max_block;
     long *sizes; uint64_t *pbits; int err;
 } compress_ctx;
@@ -403,7 +404,8 @@ static void compress_range(long lo, long hi, int tid, void *p)
         long len = 0;
         uint8_t *dst = c->tmp + b * c->max_block;
         int s = orc_encode_block(codes, c->bs, c->D, mins, scales, c->n_units,
-                                 (uint32_t)((c->chunk_base + (uint32_t)chunk) * (uint32_t)c->H + head),
+                                 (uint32_t)((c->chunk_base + (uint32_t)chunk) * (uint32_t)c->H_total +
+                                            (uint32_t)(c->head_base + head)),
                                  c->lengths, c->words, dst, &len);
         if (s) c->err = s;
         c->sizes[b] = len;
@@ -414,18 +416,20 @@ static void compress_range(long lo, long hi, int tid, void *p)
     free(codes); free(mins); free(scales);
 }
 
-/* tokens: [n_tok, H, D] f32.  Appends n_tok/bs*H blocks at *cursor. */
-int orc_compress_tokens(const float *tokens, int n_tok, int H, int D, int bs, int mode,
-                        double rel, uint32_t chunk_base, const uint8_t *lengths,
-                        uint8_t *arena, long capacity, long *cursor, uint32_t *offsets_out,
-                        uint64_t *payload_bits_out, int n_threads)
+/* tokens: [n_tok, H, D] f32 holding heads [head_base, head_base+H) of H_total
+ * (a head shard).  Appends n_tok/bs*H blocks at *cursor with
+ * block_index = (chunk_base + chunk) * H_total + head_base + h. */
+int orc_compress_tokens_shard(const float *tokens, int n_tok, int H, int D, int bs, int mode,
+                              double rel, uint32_t chunk_base, int H_total, int head_base,
+                              const uint8_t *lengths, uint8_t *arena, long capacity, long *cursor,
+                              uint32_t *offsets_out, uint64_t *payload_bits_out, int n_threads)
 {
     uint32_t words[256];
     int st = orc_canonical_words(lengths, words);
     if (st) return st;
     long nb = (long)(n_tok / bs) * H;
-    compress_ctx c = {tokens, H, D, bs, mode, mode == 1 ? bs : D, rel, chunk_base, lengths, words,
-                      NULL, 0, NULL, NULL, ORC_OK};
+    compress_ctx c = {tokens, H, D, bs, mode, mode == 1 ? bs : D, rel, chunk_base, H_total,
+                      head_base, lengths, words, NULL, 0, NULL, NULL, ORC_OK};
     c.max_block = block_header_bytes(bs, c.n_units) + (long)bs * D * 4 + 4;
     c.tmp = (uint8_t *)malloc((size_t)(nb ? nb : 1) * (size_t)c.max_block);
     c.sizes = (long *)calloc((size_t)(nb ? nb : 1), sizeof(long));
@@ -448,6 +452,17 @@ int orc_compress_tokens(const float *tokens, int n_tok, int H, int D, int bs, in
     }
     free(c.tmp); free(c.sizes); free(c.pbits);
     return err;
+}
+
+/* tokens: [n_tok, H, D] f32.  Appends n_tok/bs*H blocks at *cursor. */
+int orc_compress_tokens(const float *tokens, int n_tok, int H, int D, int bs, int mode,
+                        double rel, uint32_t chunk_base, const uint8_t *lengths,
+                        uint8_t *arena, long capacity, long *cursor, uint32_t *offsets_out,
+                        uint64_t *payload_bits_out, int n_threads)
+{
+    return orc_compress_tokens_shard(tokens, n_tok, H, D, bs, mode, rel, chunk_base, H, 0,
+                                     lengths, arena, capacity, cursor, offsets_out,
+                                     payload_bits_out, n_threads);
 }
 
 typedef struct {

@@ -274,3 +274,24 @@ def test_dense_fp16_kernel(kv):
     s = torch.einsum("shtd,shd->sht", k.float(), q) / math.sqrt(D)
     ref = torch.einsum("sht,shtd->shd", torch.softmax(s, -1), v.float())
     assert max_relative_error(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-5
+
+
+def test_head_sharded_store_reassembles_bit_exact(kv):
+    """Two head shards (as two ranks would build them, codebooks from the
+    global histogram) reassemble into the single-state arena byte-for-byte."""
+    from paper_2509_00579_b200.sharded import HeadShard, interleave_shard_arenas
+    g = load("c_fp16_d128")
+    ck, cv = _cfgs(kv, g)
+    full = _prefill(kv, g)
+    cbs = (full.k_codebook, full.v_codebook)
+    parts_k, parts_v = [], []
+    for r in range(2):
+        sh = HeadShard(r, 2, 2)
+        st = kv.LayerCacheState.prefill(sh.slice(g["k_in"]), sh.slice(g["v_in"]), ck, cv,
+                                        codebooks=cbs, head_base=sh.head_base, head_total=2)
+        parts_k.append((st.k_arena.snapshot(), st.k_arena.block_offsets.tolist()))
+        parts_v.append((st.v_arena.snapshot(), st.v_arena.block_offsets.tolist()))
+    ka, ko = interleave_shard_arenas(parts_k)
+    va, vo = interleave_shard_arenas(parts_v)
+    assert ka == full.k_arena.snapshot() and np.array_equal(ko, full.k_arena.block_offsets)
+    assert va == full.v_arena.snapshot() and np.array_equal(vo, full.v_arena.block_offsets)
