@@ -15,7 +15,7 @@ from .errors import (ArenaFullError, CodebookError, CodecError, ConfigError, Kvp
                      TensorFormatError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkvcomp.so")
+LIB_PATH = os.environ.get("KVC_LIB_PATH") or os.path.join(_HERE, "libkvcomp.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 KVC_OK, KVC_ERR_CONFIG, KVC_ERR_TENSOR, KVC_ERR_CODEBOOK, KVC_ERR_CODEC, KVC_ERR_ARENA_FULL, \

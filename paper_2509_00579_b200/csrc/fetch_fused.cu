@@ -85,14 +85,23 @@ struct Partial {
     float o[D];
 };
 
+// Shared loads on the decode path are `ld.volatile`: ptxas keeps volatile
+// accesses in program order, which pins the per-step interleave of the four
+// cursor chains written below (without it ptxas runs two chains far ahead of
+// the other two and exposes the LDS latency).
+#ifdef KVC_NONVOLATILE_LDS
+#define KVC_LD_SHARED "ld.shared"
+#else
+#define KVC_LD_SHARED "ld.volatile.shared"
+#endif
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    asm volatile(KVC_LD_SHARED ".u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ float2 lds64f(uint32_t addr) {
     float2 v;
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    asm volatile(KVC_LD_SHARED ".v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
@@ -137,7 +146,9 @@ __device__ __forceinline__ float sym_hi_byte(uint32_t e, uint32_t sel) {
 template <int MODE>
 struct Dec {
     static constexpr int kLutWords = MODE == 0 ? 64 * 32 : (1 << KVC_LUT_BITS);
-    static constexpr int kSymsPerWin = MODE == 0 ? 5 : (MODE == 1 ? 4 : 2);
+    // symbols decodable from one 32-bit window; MODE 0 uses 4 (not 5) so the
+    // reload cadence divides the unrolled loop (24 of 32 bits)
+    static constexpr int kSymsPerWin = MODE == 0 ? 4 : (MODE == 1 ? 4 : 2);
 };
 
 template <int MODE>
@@ -347,8 +358,13 @@ fused_attn_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__r
                 const float2 q2 = lds64f(qf_s + 8 * c2);
                 sA2 = __ffma2_rn(f[0], q2, sA2);
                 sB2 = __ffma2_rn(f[1], q2, sB2);
+#ifdef KVC_EXPERIMENT_VREG
+                acc[c2 % KVC_EXPERIMENT_VREG] = __ffma2_rn(f[2], aA2, acc[c2 % KVC_EXPERIMENT_VREG]);
+                acc[c2 % KVC_EXPERIMENT_VREG] = __ffma2_rn(f[3], aB2, acc[c2 % KVC_EXPERIMENT_VREG]);
+#else
                 acc[c2] = __ffma2_rn(f[2], aA2, acc[c2]);
                 acc[c2] = __ffma2_rn(f[3], aB2, acc[c2]);
+#endif
             }
         } else {
             uint32_t e0[4];
@@ -449,6 +465,387 @@ fused_attn_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__r
             L += all[w].l * sc;
 #pragma unroll
             for (int k = 0; k < 4; ++k) o[k] += all[w].o[lane + 32 * k] * sc;
+        }
+        Partial *dst = partial + ((long)sidx * H + h) * n_splits + split;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dst->o[lane + 32 * k] = o[k];
+        if (lane == 0) {
+            dst->m = M;
+            dst->l = L;
+        }
+    }
+}
+
+// 64-bit window cursor for the pair decoder: `hi` holds the next 32 stream
+// bits, `lo` the following 32.  A reload (3 shared words) refills 64 valid
+// bits, enough for 4 pair steps (<= 48 bits at max_len 6), so reloads cost
+// 0.75 loads per pair step instead of 1.
+struct Cursor2 {
+    uint32_t hi, lo;
+    uint32_t p;
+    uint32_t base;
+};
+__device__ __forceinline__ void cursor2_init(Cursor2 &c, uint32_t stage_addr, uint32_t bit) {
+    c.base = stage_addr + ((bit >> 5) << 2);
+    c.p = bit & 31u;
+    c.hi = c.lo = 0;
+}
+__device__ __forceinline__ void cursor2_reload(Cursor2 &c) {
+    const uint32_t a = c.base + ((c.p >> 3) & 0x1FFCu);
+    const uint32_t w0 = bswap32(lds32(a)), w1 = bswap32(lds32(a + 4)), w2 = bswap32(lds32(a + 8));
+    c.hi = __funnelshift_l(w1, w0, c.p);
+    c.lo = __funnelshift_l(w2, w1, c.p);
+}
+__device__ __forceinline__ float2 cursor2_pair(Cursor2 &c, uint32_t lut_s) {
+    const uint32_t e = lds32(lut_s + ((c.hi >> 20) << 2));
+    c.hi = __funnelshift_l(c.lo, c.hi, e);
+    c.lo = __funnelshift_l(0u, c.lo, e);
+    c.p += e;
+    return __fadd2_rn(make_float2(sym_hi_byte(e, 0x7652), sym_hi_byte(e, 0x7653)),
+                      make_float2(-8388608.f, -8388608.f));
+}
+
+// Decode the 128 symbols of two slices (cursors c[0], c[1]) in lockstep and
+// hand each channel pair to sink(c2, f[slice0], f[slice1]).  Fully unrolled so
+// the sink can index register arrays with c2.
+template <int MODE, bool FULL, typename Sink>
+__device__ __forceinline__ void decode_two(Cursor *c, uint32_t lut_s, uint32_t lane_s, Sink sink) {
+    const float2 magic = make_float2(-8388608.f, -8388608.f);
+    if (MODE == 1) {
+#pragma unroll(FULL ? 64 : 8)
+        for (int c2 = 0; c2 < D / 2; ++c2) {
+            if (c2 % 2 == 0) {
+                cursor_reload(c[0]);
+                cursor_reload(c[1]);
+            }
+            float2 f[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const uint32_t e = lds32(lut_addr<1>(c[k].win, lut_s, 0));
+                c[k].win = __funnelshift_l(0u, c[k].win, e);
+                c[k].p += e;
+                f[k] = __fadd2_rn(make_float2(sym_hi_byte(e, 0x7652), sym_hi_byte(e, 0x7653)), magic);
+            }
+            sink(c2, f[0], f[1]);
+        }
+    } else {
+        constexpr int W = Dec<MODE>::kSymsPerWin;
+        uint32_t e0[2];
+#pragma unroll(FULL ? 128 : 16)
+        for (int sy = 0; sy < D; ++sy) {
+            if (sy % W == 0) {
+                cursor_reload(c[0]);
+                cursor_reload(c[1]);
+            }
+            uint32_t e[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                e[k] = lds32(lut_addr<MODE>(c[k].win, lut_s, lane_s));
+                c[k].win = __funnelshift_l(0u, c[k].win, e[k]);
+                c[k].p += e[k];
+            }
+            if (sy & 1) {
+                sink(sy / 2, make_float2(__uint_as_float(e0[0] & ~15u), __uint_as_float(e[0] & ~15u)),
+                     make_float2(__uint_as_float(e0[1] & ~15u), __uint_as_float(e[1] & ~15u)));
+            } else {
+                e0[0] = e[0];
+                e0[1] = e[1];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialized fused fetch-attention (default).  CTA = 2 warpgroups:
+// warps 0-3 decode K, warps 4-7 decode V; K warp w and V warp w+4 form a pair
+// that walks chunks first+4j of this CTA's context split.  Per pair: a K TMA
+// ring (2 slots), a V TMA ring (2 slots) and a 2-slot score ring; the K warp
+// publishes each chunk's 64 log2-scaled scores through mbarriers (sfull /
+// sempty), the V warp runs the online softmax and the weighted V decode.
+// setmaxnreg moves registers from the K warpgroup (2 cursors, no arrays) to
+// the V warpgroup (128 f32 accumulators per lane), which lets 2 CTAs = 16
+// warps share an SM; every warp runs two independent decode chains.
+// ---------------------------------------------------------------------------
+constexpr int WS_PAIRS = 4;
+constexpr int kThreadsWS = 2 * WS_PAIRS * 32;
+constexpr int kRegK = 80, kRegV = 176;  // (80 + 176) * 128 threads = 32768 regs per CTA
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreadsWS, 2)
+fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__restrict__ q,
+                     float *__restrict__ scores, long ctx_stride, Partial *__restrict__ partial,
+                     int chunks_per_split, int n_splits, int stage_k, int stage_v, int *err) {
+    __shared__ __align__(128) uint32_t s_lut[2][Dec<MODE>::kLutWords];
+    __shared__ uint64_t s_lbar[1];
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const bool is_v = warp >= WS_PAIRS;
+    const int pair = warp & (WS_PAIRS - 1);
+    const int per_pair = 2 * (stage_k + stage_v) + 1024 + 64;
+    uint8_t *pb = smem + pair * per_pair;
+    uint8_t *kring = pb, *vring = pb + 2 * stage_k;
+    float *qf = reinterpret_cast<float *>(pb + 2 * (stage_k + stage_v));
+    float *sring = qf + D;  // [2][64]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(pb + 2 * (stage_k + stage_v) + 1024);
+    uint64_t *kfull = bar, *vfull = bar + 2, *sfull = bar + 4, *sempty = bar + 6;
+
+    const int split = blockIdx.x, h = blockIdx.y, sidx = blockIdx.z;
+    const kvc_seq_desc sd = seqs[sidx];
+    if (!is_v && lane == 0) {
+        mbar_init(&kfull[0], 1);
+        mbar_init(&kfull[1], 1);
+        mbar_init(&vfull[0], 1);
+        mbar_init(&vfull[1], 1);
+        mbar_init(&sfull[0], 32);
+        mbar_init(&sfull[1], 32);
+        mbar_init(&sempty[0], 32);
+        mbar_init(&sempty[1], 32);
+    }
+    if (MODE == 1 && threadIdx.x == 0) mbar_init(s_lbar, 1);
+    fence_mbar_init();
+    __syncthreads();
+    if (MODE == 1) {
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(s_lbar, 2u * (4u << KVC_LUT_BITS));
+            tma_load_1d(s_lut[0], sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+            tma_load_1d(s_lut[1], sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+        }
+    } else {
+        build_lut<MODE>(s_lut[0], sd.k_cb);
+        build_lut<MODE>(s_lut[1], sd.v_cb);
+        __syncthreads();
+    }
+
+    const int c_begin = split * chunks_per_split;
+    const int c_end = min(sd.n_chunks, c_begin + chunks_per_split);
+    const int first = c_begin + pair;
+    const int n = first < c_end ? (c_end - first + WS_PAIRS - 1) / WS_PAIRS : 0;
+    const float sm_scale = kLog2e / sqrtf((float)D);
+    const float inv_sqrt = 1.0f / sqrtf((float)D);
+
+    // TMA of chunk j's K or V extent into ring slot j&1 (lane 0 only).
+    auto issue = [&](bool v, int j) {
+        const long ord = (long)(first + WS_PAIRS * j) * H + h;
+        const uint32_t *offs = v ? sd.v_offsets : sd.k_offsets;
+        const kvc_arena_counters *ct = v ? sd.v_counters : sd.k_counters;
+        const long nb = (long)ct->n_blocks;
+        const uint64_t s0 = offs[ord];
+        const uint64_t e0 = (ord + 1 < nb) ? (uint64_t)offs[ord + 1] : ct->cursor;
+        const uint64_t a = s0 & ~15ull;
+        uint32_t bytes = (uint32_t)(((e0 + 15) & ~15ull) - a);
+        const int cap = v ? stage_v : stage_k;
+        if (bytes > (uint32_t)cap) {
+            kvc_set_err(err, KVC_ERR_CODEC);
+            bytes = 16;
+        }
+        uint64_t *b = v ? &vfull[j & 1] : &kfull[j & 1];
+        uint8_t *dst = v ? vring + (j & 1) * stage_v : kring + (j & 1) * stage_k;
+        mbar_expect_tx(b, bytes);
+        tma_load_1d(dst, (v ? sd.v_arena : sd.k_arena) + a, bytes, b);
+    };
+    const uint32_t lut_s = smem_u32(s_lut[is_v ? 1 : 0]);
+    const uint32_t lane_s = lut_s + 4 * lane;
+    bool bad = false;
+
+    if (!is_v) {
+        // =================== K warp: scores producer ===================
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegK));
+        if (lane == 0) {
+            if (n > 0) issue(false, 0);
+            if (n > 1) issue(false, 1);
+        }
+        const float *qh = q + ((long)sidx * H + h) * D;
+        float qreg[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) qreg[k] = qh[lane + 32 * k];
+        const uint32_t qf_s = smem_u32(qf);
+        if (MODE == 1) mbar_wait(s_lbar, 0);
+        for (int j = 0; j < n; ++j) {
+            const int u = j >> 1, sl = j & 1;
+            mbar_wait(&kfull[sl], u & 1);
+            const long ord = (long)(first + WS_PAIRS * j) * H + h;
+            const uint32_t kofs = sd.k_offsets[ord] & 15u;
+            const uint8_t *ks = kring + sl * stage_k + kofs;
+            const uint32_t cA = lds_u16(ks + 6 + 2 * lane), cB = lds_u16(ks + 6 + 2 * (lane + 32));
+            const uint32_t iA = kvc_warp_incl_scan(cA, lane);
+            const uint32_t totA = __shfl_sync(0xffffffffu, iA, 31);
+            const uint32_t iB = kvc_warp_incl_scan(cB, lane);
+            float basep = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int c = lane + 32 * k;
+                qf[c] = lds_f32_a2(ks + 6 + 2 * BS + 8 * c + 4) * qreg[k];
+                basep = fmaf(lds_f32_a2(ks + 6 + 2 * BS + 8 * c), qreg[k], basep);
+            }
+            const float base = kvc_warp_sum(basep);
+            __syncwarp();
+            const uint32_t bit0 = (kofs + K_HDR) * 8, slot = smem_u32(kring + sl * stage_k);
+            Cursor cur[2];
+            cursor_init(cur[0], slot, bit0 + iA - cA);
+            cursor_init(cur[1], slot, bit0 + totA + iB - cB);
+            const uint32_t p0A = cur[0].p, p0B = cur[1].p;
+            float2 sA2 = make_float2(0.f, 0.f), sB2 = sA2;
+            if (MODE == 1) {
+                Cursor2 c2c[2];
+                cursor2_init(c2c[0], slot, bit0 + iA - cA);
+                cursor2_init(c2c[1], slot, bit0 + totA + iB - cB);
+#pragma unroll 1
+                for (int g = 0; g < D / 16; ++g) {   // 8 pair steps = 16 channels per group
+                    float4 qv[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        asm volatile(KVC_LD_SHARED ".v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(qv[k].x), "=f"(qv[k].y), "=f"(qv[k].z), "=f"(qv[k].w)
+                                     : "r"(qf_s + 64 * g + 16 * k));
+                    }
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        if (t % 4 == 0) {
+                            cursor2_reload(c2c[0]);
+                            cursor2_reload(c2c[1]);
+                        }
+                        const float4 qq = qv[t / 2];
+                        const float2 q2 = (t & 1) ? make_float2(qq.z, qq.w) : make_float2(qq.x, qq.y);
+                        sA2 = __ffma2_rn(cursor2_pair(c2c[0], lut_s), q2, sA2);
+                        sB2 = __ffma2_rn(cursor2_pair(c2c[1], lut_s), q2, sB2);
+                    }
+                }
+                cur[0].p = c2c[0].p;
+                cur[1].p = c2c[1].p;
+            } else {
+                decode_two<MODE, false>(cur, lut_s, lane_s, [&](int c2, float2 fA, float2 fB) {
+                    const float2 q2 = lds64f(qf_s + 8 * c2);
+                    sA2 = __ffma2_rn(fA, q2, sA2);
+                    sB2 = __ffma2_rn(fB, q2, sB2);
+                });
+            }
+            bad |= (((cur[0].p - p0A) & 0xFFFFu) != cA) | (((cur[1].p - p0B) & 0xFFFFu) != cB);
+            const float sA = sA2.x + sA2.y + base, sB = sB2.x + sB2.y + base;
+            if (scores) {
+                float *srow = scores + ((long)sidx * H + h) * ctx_stride +
+                              (long)(first + WS_PAIRS * j) * BS;
+                srow[lane] = sA * inv_sqrt;
+                srow[lane + 32] = sB * inv_sqrt;
+            }
+            mbar_wait(&sempty[sl], (u & 1) ^ 1);
+            sring[sl * 64 + lane] = sA * sm_scale;
+            sring[sl * 64 + lane + 32] = sB * sm_scale;
+            mbar_arrive(&sfull[sl]);
+            __syncwarp();
+            if (lane == 0 && j + 2 < n) issue(false, j + 2);
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) kvc_set_err(err, KVC_ERR_CODEC);
+        __syncthreads();
+        __syncthreads();
+        return;
+    }
+
+    // =================== V warp: softmax + weighted V ===================
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegV));
+    if (lane == 0) {
+        if (n > 0) issue(true, 0);
+        if (n > 1) issue(true, 1);
+    }
+    float m = -INFINITY, lsum = 0.f, wm = 0.f;
+    float2 acc[D / 2];
+#pragma unroll
+    for (int c = 0; c < D / 2; ++c) acc[c] = make_float2(0.f, 0.f);
+    if (MODE == 1) mbar_wait(s_lbar, 0);
+    for (int j = 0; j < n; ++j) {
+        const int u = j >> 1, sl = j & 1;
+        mbar_wait(&sfull[sl], u & 1);
+        const float sA = sring[sl * 64 + lane], sB = sring[sl * 64 + lane + 32];
+        mbar_arrive(&sempty[sl]);
+        const float bm = kvc_warp_max(fmaxf(sA, sB));
+        if (bm > m) {
+            const float alpha = exp2f(m - bm);
+            const float2 al2 = make_float2(alpha, alpha);
+#pragma unroll
+            for (int c = 0; c < D / 2; ++c) acc[c] = __fmul2_rn(acc[c], al2);
+            lsum *= alpha;
+            wm *= alpha;
+            m = bm;
+        }
+        const float pA = exp2f(sA - m), pB = exp2f(sB - m);
+        lsum += pA + pB;
+        mbar_wait(&vfull[sl], u & 1);
+        const long ord = (long)(first + WS_PAIRS * j) * H + h;
+        const uint32_t vofs = sd.v_offsets[ord] & 15u;
+        const uint8_t *vs = vring + sl * stage_v + vofs;
+        const uint32_t cA = lds_u16(vs + 6 + 2 * lane), cB = lds_u16(vs + 6 + 2 * (lane + 32));
+        const uint32_t iA = kvc_warp_incl_scan(cA, lane);
+        const uint32_t totA = __shfl_sync(0xffffffffu, iA, 31);
+        const uint32_t iB = kvc_warp_incl_scan(cB, lane);
+        const float aA = pA * lds_f32_a2(vs + 6 + 2 * BS + 8 * lane + 4);
+        const float aB = pB * lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32) + 4);
+        wm = fmaf(pA, lds_f32_a2(vs + 6 + 2 * BS + 8 * lane), wm);
+        wm = fmaf(pB, lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32)), wm);
+        const float2 aA2 = make_float2(aA, aA), aB2 = make_float2(aB, aB);
+        const uint32_t bit0 = (vofs + V_HDR) * 8, slot = smem_u32(vring + sl * stage_v);
+        Cursor cur[2];
+        cursor_init(cur[0], slot, bit0 + iA - cA);
+        cursor_init(cur[1], slot, bit0 + totA + iB - cB);
+        const uint32_t p0A = cur[0].p, p0B = cur[1].p;
+        if (MODE == 1) {
+            Cursor2 c2c[2];
+            cursor2_init(c2c[0], slot, bit0 + iA - cA);
+            cursor2_init(c2c[1], slot, bit0 + totA + iB - cB);
+#pragma unroll
+            for (int c2 = 0; c2 < D / 2; ++c2) {
+                if (c2 % 4 == 0) {
+                    cursor2_reload(c2c[0]);
+                    cursor2_reload(c2c[1]);
+                }
+                acc[c2] = __ffma2_rn(cursor2_pair(c2c[0], lut_s), aA2, acc[c2]);
+                acc[c2] = __ffma2_rn(cursor2_pair(c2c[1], lut_s), aB2, acc[c2]);
+            }
+            cur[0].p = c2c[0].p;
+            cur[1].p = c2c[1].p;
+        } else {
+            decode_two<MODE, true>(cur, lut_s, lane_s, [&](int c2, float2 fA, float2 fB) {
+                acc[c2] = __ffma2_rn(fA, aA2, acc[c2]);
+                acc[c2] = __ffma2_rn(fB, aB2, acc[c2]);
+            });
+        }
+        bad |= (((cur[0].p - p0A) & 0xFFFFu) != cA) | (((cur[1].p - p0B) & 0xFFFFu) != cB);
+        __syncwarp();
+        if (lane == 0 && j + 2 < n) issue(true, j + 2);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) kvc_set_err(err, KVC_ERR_CODEC);
+    lsum = kvc_warp_sum(lsum);
+    wm = kvc_warp_sum(wm);
+    __syncthreads();  // K warps are done: their rings are free scratch
+    Partial *wp = reinterpret_cast<Partial *>(smem + pair * per_pair);
+#pragma unroll
+    for (int c = 0; c < D / 2; ++c) {
+        const float vx = kvc_warp_sum(acc[c].x);
+        const float vy = kvc_warp_sum(acc[c].y);
+        if (lane == ((2 * c) & 31)) {
+            wp->o[2 * c] = vx + wm;
+            wp->o[2 * c + 1] = vy + wm;
+        }
+    }
+    if (lane == 0) {
+        wp->m = m;
+        wp->l = lsum;
+    }
+    __syncthreads();
+    if (pair == 0) {
+        float M = -INFINITY;
+        for (int w = 0; w < WS_PAIRS; ++w)
+            M = fmaxf(M, reinterpret_cast<const Partial *>(smem + w * per_pair)->m);
+        float L = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int w = 0; w < WS_PAIRS; ++w) {
+            const Partial *pw = reinterpret_cast<const Partial *>(smem + w * per_pair);
+            const float sc = (pw->m == -INFINITY) ? 0.f : exp2f(pw->m - M);
+            L += pw->l * sc;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) o[k] += pw->o[lane + 32 * k] * sc;
         }
         Partial *dst = partial + ((long)sidx * H + h) * n_splits + split;
 #pragma unroll
@@ -730,6 +1127,43 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
     if (smem + lut_bytes + 256 > 227 * 1024)
         return kvc_fail(KVC_ERR_CONFIG, "block extents too large for staging");
     dim3 grid(n_splits, H, n_seqs);
+    const char *impl = getenv("KVC_FUSED_IMPL");
+    const bool use_ws = !(impl && impl[0] == 'i');
+    const size_t ws_smem = WS_PAIRS * (2 * (size_t)(stage_k + stage_v) + 1024 + 64);
+    if (use_ws && max_chunks > 0 && ws_smem + lut_bytes + 256 <= 227 * 1024) {
+        const int ws_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H);
+        const int ws_splits = (max_chunks + ws_cps - 1) / ws_cps;
+        if (sizeof(Partial) * (size_t)n_seqs * H * ws_splits > workspace_bytes)
+            return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
+        dim3 g2(ws_splits, H, n_seqs);
+        if (mode == 0) {
+            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_ws_kernel<0>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)ws_smem));
+            fused_attn_ws_kernel<0><<<g2, kThreadsWS, ws_smem, s>>>(
+                seqs_dev, H, q_dev, scores_dev, ctx_stride, part, ws_cps, ws_splits, stage_k,
+                stage_v, err_dev);
+        } else if (mode == 1) {
+            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_ws_kernel<1>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)ws_smem));
+            fused_attn_ws_kernel<1><<<g2, kThreadsWS, ws_smem, s>>>(
+                seqs_dev, H, q_dev, scores_dev, ctx_stride, part, ws_cps, ws_splits, stage_k,
+                stage_v, err_dev);
+        } else {
+            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_ws_kernel<2>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)ws_smem));
+            fused_attn_ws_kernel<2><<<g2, kThreadsWS, ws_smem, s>>>(
+                seqs_dev, H, q_dev, scores_dev, ctx_stride, part, ws_cps, ws_splits, stage_k,
+                stage_v, err_dev);
+        }
+        int st = kvc_check_launch("fused_attn_ws_kernel");
+        if (st) return st;
+        combine_kernel<<<dim3(1, H, n_seqs), 128, 0, s>>>(seqs_dev, H, bs, q_dev, part, ws_splits,
+                                                          out_dev, scores_dev, ctx_stride);
+        return kvc_check_launch("combine_kernel");
+    }
     if (max_chunks > 0) {
 #define KVC_LAUNCH_FUSED(M)                                                                   \
     do {                                                                                      \
