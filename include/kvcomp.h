@@ -154,8 +154,20 @@ int kvc_encode_append(const uint8_t *codes_dev, const float *metas_dev, int n_ch
                       kvc_arena_counters *counters_dev, void *workspace_dev, void *stream);
 size_t kvc_encode_workspace_bytes(int nb, int bs);
 
+/* Store pass A of prefill (kvcache.py:110-121): quantise the full blocks of K
+ * and V and accumulate their code histograms (hist_dev: 512 x u64, K bins
+ * then V bins).  No codes are written. */
+int kvc_store_hist(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
+                   int n_chunks, int H, int D, int bs, double rel_k, double rel_v,
+                   uint64_t *hist_dev, void *stream);
+
+/* 1 if the single-pass Store kernels cover this block shape / code length. */
+int kvc_store_supported(int bs, int D, int max_len);
+
 /* One Store event with known codebooks (kvcache.py:217-239): quantise K and
- * V from x[t, h, :] (t < n_chunks*bs) and append both arenas. */
+ * V from x[t, h, :] (t < n_chunks*bs), Huffman-encode and append both arenas
+ * in one launch; arena offsets come from a decoupled look-back scan in
+ * block_index order (deterministic, no code round trip through HBM). */
 int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
                      int n_chunks, int H_local, int H_total, int head_base, int D, int bs,
                      double rel_k, double rel_v, uint32_t chunk_base,

@@ -87,6 +87,8 @@ SIGNATURES = {
     "kvc_store_append": (I, [P, P, I, L, I, I, I, I, I, I, D_, D_, U32, P, I, P, I, P, U64, P, P,
                              P, U64, P, P, P, SZ, P]),
     "kvc_store_workspace_bytes": (SZ, [I, I, I, I]),
+    "kvc_store_hist": (I, [P, P, I, L, I, I, I, I, D_, D_, P, P]),
+    "kvc_store_supported": (I, [I, I, I]),
     "kvc_k_scores": (I, [P, I, I, I, I, P, P, L, P, P]),
     "kvc_softmax_rows": (I, [P, I, L, L, P]),
     "kvc_v_output": (I, [P, I, I, I, I, P, L, P, P, P, P]),

@@ -412,43 +412,3 @@ extern "C" int kvc_encode_append(const uint8_t *codes_dev, const float *metas_de
                                   &w.scalars[1], w.max_extent, counters_dev, w.err);
     return kvc_check_launch("commit_kernel");
 }
-
-extern "C" size_t kvc_store_workspace_bytes(int n_chunks, int H, int D, int bs) {
-    size_t nb = (size_t)n_chunks * H;
-    size_t codes = align256(nb * bs * D);
-    size_t metas = align256(nb * (size_t)(bs > D ? bs : D) * 8);
-    return codes + metas + kvc_encode_workspace_bytes((int)nb, bs);
-}
-
-extern "C" int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
-                                int n_chunks, int H_local, int H_total, int head_base, int D,
-                                int bs, double rel_k, double rel_v, uint32_t chunk_base,
-                                const kvc_codebook_dev *k_cb_dev, int k_max_len,
-                                const kvc_codebook_dev *v_cb_dev, int v_max_len,
-                                uint8_t *k_arena_dev, uint64_t k_capacity, uint32_t *k_offsets_dev,
-                                kvc_arena_counters *k_counters_dev, uint8_t *v_arena_dev,
-                                uint64_t v_capacity, uint32_t *v_offsets_dev,
-                                kvc_arena_counters *v_counters_dev, void *workspace_dev,
-                                size_t workspace_bytes, void *stream) {
-    if (n_chunks == 0) return KVC_OK;
-    if (workspace_bytes < kvc_store_workspace_bytes(n_chunks, H_local, D, bs))
-        return kvc_fail(KVC_ERR_CONFIG, "store workspace too small");
-    size_t nb = (size_t)n_chunks * H_local;
-    char *p = static_cast<char *>(workspace_dev);
-    uint8_t *codes = reinterpret_cast<uint8_t *>(p);
-    float *metas = reinterpret_cast<float *>(p + align256(nb * bs * D));
-    void *enc = p + align256(nb * bs * D) + align256(nb * (size_t)(bs > D ? bs : D) * 8);
-    int st = kvc_quantize(k_dev, x_dtype, row_stride, n_chunks, H_local, D, bs, KVC_K_BLOCK, rel_k,
-                          codes, metas, nullptr, stream);
-    if (st) return st;
-    st = kvc_encode_append(codes, metas, n_chunks, H_local, H_total, head_base, chunk_base, bs, D,
-                           D, k_max_len, k_cb_dev, k_arena_dev, k_capacity, k_offsets_dev,
-                           k_counters_dev, enc, stream);
-    if (st) return st;
-    st = kvc_quantize(v_dev, x_dtype, row_stride, n_chunks, H_local, D, bs, KVC_V_TOKEN, rel_v,
-                      codes, metas, nullptr, stream);
-    if (st) return st;
-    return kvc_encode_append(codes, metas, n_chunks, H_local, H_total, head_base, chunk_base, bs,
-                             D, bs, v_max_len, v_cb_dev, v_arena_dev, v_capacity, v_offsets_dev,
-                             v_counters_dev, enc, stream);
-}

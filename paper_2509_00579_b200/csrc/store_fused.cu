@@ -1,0 +1,540 @@
+// store_fused.cu — single-pass Store: quantise -> Huffman encode -> append,
+// with the arena offset of each block found by a decoupled look-back scan
+// (deterministic block_index order, no code round trip through HBM).
+//
+//   prefill:  pass A  store_kernel<false>  quantise + code histogram (K, V)
+//             host    2x256 histogram -> smoothed canonical codebooks
+//             pass B  store_kernel<true>   quantise + encode + look-back + write
+//   append:   pass B only (codebooks fixed after prefill, SPEC / kvcache.py:150-177)
+//
+// One CTA per (chunk, head) block; blockIdx.y selects K (0) or V (1).  The
+// block is staged in shared memory as f32 (16-byte vector loads), per-unit
+// min/max and codes are computed there, and the serialised block image
+// (codec.py:229-244) is assembled in shared memory as big-endian words:
+// a warp per slice, each lane emits its run of codewords at the offset given
+// by a warp prefix sum of code lengths.
+//
+// Quantisation is bit-exact with the reference's binary64 arithmetic
+// (quantizer.py:114-141): an f32 candidate t = (x-min)*RN(1/s) is within
+// 4.6e-5 of the binary64 quotient (3 roundings, t <= 256), so its code is final
+// unless frac(t) lies within 2^-12 of 1/2 (the only decision boundary of
+// round-half-up); those values, and any non-finite/huge intermediate, take the
+// binary64 path (reciprocal multiply, then __ddiv_rn near the boundary).
+#include <cmath>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+struct StoreTensor {
+    const void *x;              // [.., H_local, D] rows, row_stride elements apart
+    int mode;                   // KVC_K_BLOCK / KVC_V_TOKEN
+    double rel;
+    const kvc_codebook_dev *cb; // NULL in the histogram pass
+    uint8_t *arena;
+    uint64_t capacity;
+    uint32_t *offsets;
+    kvc_arena_counters *counters;
+    unsigned long long *status; // look-back words, one per block (zeroed)
+    unsigned long long *acc;    // [0] ticket, [1] done, [2] payload bits, [3] payload bytes, [4] max extent
+    unsigned long long *hist;   // 256 bins (histogram pass)
+    int max_code;               // ceil(1/rel): codes lie in [0, max_code]
+};
+
+struct StoreParams {
+    StoreTensor t[2];
+    long row_stride;
+    int n_chunks, H_local, H_total, head_base, D, bs;
+    uint32_t chunk_base;
+    int *err;
+};
+
+__device__ __forceinline__ uint8_t code_f64(float x, float lo, float scale) {
+    const double s64 = (double)scale;
+    const double d = __dsub_rn((double)x, (double)lo);
+    double t = __dmul_rn(d, __drcp_rn(s64));
+    double f = floor(t);
+    double frac = __dsub_rn(t, f);
+    if (fabs(frac - 0.5) < 1.0e-11 * (t + 1.0)) {
+        t = __ddiv_rn(d, s64);
+        f = floor(t);
+        frac = __dsub_rn(t, f);
+    }
+    if (frac >= 0.5) f += 1.0;
+    return (uint8_t)(int)f;
+}
+
+__device__ __forceinline__ uint8_t code_fast(float x, float lo, float scale, float r32) {
+    if (!(scale > 0.f)) return 0;
+    const float t = __fmul_rn(__fsub_rn(x, lo), r32);
+    if (t < 300.f) {
+        const float c = floorf(t);
+        const float f = t - c;
+        if (fabsf(f - 0.5f) > (1.0f / 4096.0f)) return (uint8_t)(int)(c + (f >= 0.5f ? 1.f : 0.f));
+    }
+    return code_f64(x, lo, scale);
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void img_or_byte(uint32_t *img, int j, uint32_t v) {
+    atomicOr(&img[j >> 2], (v & 0xFFu) << (8 * (3 - (j & 3))));
+}
+__device__ __forceinline__ void img_or_bits32(uint32_t *img, uint32_t p, uint32_t v) {
+    const uint32_t s = p & 31;
+    atomicOr(&img[p >> 5], v >> s);
+    if (s) atomicOr(&img[(p >> 5) + 1], v << (32 - s));
+}
+
+// Shared-memory layout (dynamic): stage f32 [bs*D] (reused as the block image),
+// codes u8 [bs*D], unit lo/scale/r32 f32 [n_units], slice bits u32 [bs],
+// slice offsets u32 [bs], codebook words u32[256] + lengths u8[256].
+// DT / BST: compile-time head_dim / block_size (0 = runtime, generic shapes).
+template <typename T, bool ENCODE, int DT, int BST>
+__global__ void __launch_bounds__(kThreads)
+store_kernel(StoreParams P, int stage_words) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const StoreTensor S = P.t[blockIdx.y];  // one copy into registers
+    const int D = DT ? DT : P.D, bs = BST ? BST : P.bs, nv = bs * D;
+    const bool is_v = S.mode == KVC_V_TOKEN;
+    const int n_units = is_v ? bs : D;
+    T *stage = reinterpret_cast<T *>(sm);  // staged in the input type (fp16 halves smem)
+    uint8_t *codes = sm + 4 * (size_t)stage_words;
+    const int codes_bytes = nv;
+    float *u_lo = reinterpret_cast<float *>(codes + ((codes_bytes + 15) & ~15));
+    float *u_sc = u_lo + n_units;
+    float *u_r = u_sc + n_units;
+    uint32_t *s_bits = reinterpret_cast<uint32_t *>(u_r + n_units);
+    uint32_t *s_off = s_bits + bs;
+    uint32_t *cw = s_off + bs;
+    uint8_t *cl = reinterpret_cast<uint8_t *>(cw + 256);
+    __shared__ uint32_t sh_hist[256];
+    __shared__ uint32_t sh_whist[kWarps][32];
+    __shared__ long sh_b;
+    __shared__ unsigned long long sh_excl;
+    __shared__ uint32_t sh_total_bits;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long nb = (long)P.n_chunks * P.H_local;
+
+    // logical block id in scheduling order (look-back needs predecessors running)
+    if (tid == 0) sh_b = ENCODE ? (long)atomicAdd(&S.acc[0], 1ull) : (long)blockIdx.x;
+    if (!ENCODE)
+        for (int i = tid; i < 256; i += kThreads) sh_hist[i] = 0;
+    if (ENCODE)
+        for (int i = tid; i < 256; i += kThreads) {
+            cw[i] = S.cb->words[i];
+            cl[i] = S.cb->lengths[i];
+        }
+    __syncthreads();
+    const long b = sh_b;
+    const int chunk = (int)(b / P.H_local), hl = (int)(b % P.H_local);
+    const uint64_t base = ENCODE ? S.counters->cursor : 0;
+    const T *src = static_cast<const T *>(S.x) + (long)chunk * bs * P.row_stride + (long)hl * D;
+
+    // ---- stage [bs, D] as f32 ------------------------------------------
+    constexpr int VEC = 16 / sizeof(T);
+    if (D % VEC == 0 && (P.row_stride % VEC) == 0 &&
+        (reinterpret_cast<uintptr_t>(S.x) & 15) == 0) {
+        const int vpr = D / VEC;
+        for (int i = tid; i < bs * vpr; i += kThreads) {
+            const int r = i / vpr, v = i % vpr;
+            const uint4 u = *reinterpret_cast<const uint4 *>(src + (long)r * P.row_stride + v * VEC);
+            *reinterpret_cast<uint4 *>(stage + r * D + v * VEC) = u;
+        }
+    } else {
+        for (int i = tid; i < nv; i += kThreads) {
+            const int r = i / D, c = i % D;
+            stage[i] = src[(long)r * P.row_stride + c];
+        }
+    }
+    __syncthreads();
+
+    // ---- per-unit (min, scale): K per channel column, V per token row ----
+    if (!is_v) {
+        for (int c = tid; c < D; c += kThreads) {
+            float lo = kvc_load(&stage[c]), hi = lo;
+            for (int r = 1; r < bs; ++r) {
+                const float v = kvc_load(&stage[r * D + c]);
+                lo = fminf(lo, v);
+                hi = fmaxf(hi, v);
+            }
+            const float sc = (float)__dmul_rn(S.rel, __dsub_rn((double)hi, (double)lo));
+            u_lo[c] = lo;
+            u_sc[c] = sc;
+            u_r[c] = sc > 0.f ? __frcp_rn(sc) : 0.f;
+        }
+    } else {
+        for (int r = warp; r < bs; r += kWarps) {
+            float lo = 3.4e38f, hi = -3.4e38f;
+            for (int c = lane; c < D; c += 32) {
+                const float v = kvc_load(&stage[r * D + c]);
+                lo = fminf(lo, v);
+                hi = fmaxf(hi, v);
+            }
+            lo = kvc_warp_min(lo);
+            hi = kvc_warp_max(hi);
+            if (lane == 0) {
+                const float sc = (float)__dmul_rn(S.rel, __dsub_rn((double)hi, (double)lo));
+                u_lo[r] = lo;
+                u_sc[r] = sc;
+                u_r[r] = sc > 0.f ? __frcp_rn(sc) : 0.f;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- codes (+ histogram in pass A) --------------------------------
+    // Pass A: per-warp 32-bin shared histograms (small alphabets) keep atomic
+    // contention inside a warp; wider alphabets use the shared 256-bin one.
+    const bool small_alpha = S.max_code < 32;
+    uint32_t *whist = sh_whist[warp];
+    if (!ENCODE) {
+        whist[lane] = 0;
+        __syncwarp();
+    }
+    auto count = [&](bool ok, uint32_t code) {
+        if (!ok) return;
+        if (small_alpha) atomicAdd(&whist[code], 1u);
+        else atomicAdd(&sh_hist[code], 1u);
+    };
+    if (D <= kThreads) {
+        // thread -> fixed column c (one division per thread, none per element)
+        const int rstep = kThreads / D;
+        const int c = tid % D, r0 = tid / D;
+        const bool col_ok = r0 < rstep;
+        const int iters = (bs + rstep - 1) / rstep;
+        for (int k = 0; k < iters; ++k) {
+            const int r = r0 + k * rstep;
+            const bool ok = col_ok && r < bs;
+            uint32_t code = 0;
+            if (ok) {
+                const int u = is_v ? r : c;
+                const int i = r * D + c;
+                code = code_fast(kvc_load(&stage[i]), u_lo[u], u_sc[u], u_r[u]);
+                if (ENCODE) codes[i] = (uint8_t)code;
+            }
+            if (!ENCODE) count(ok, code);
+        }
+    } else {
+        for (int i = tid; i < nv; i += kThreads) {
+            const int r = i / D, c = i - r * D;
+            const int u = is_v ? r : c;
+            const uint32_t code = code_fast(kvc_load(&stage[i]), u_lo[u], u_sc[u], u_r[u]);
+            if (ENCODE) codes[i] = (uint8_t)code;
+            else count(true, code);
+        }
+    }
+    __syncthreads();
+    if (!ENCODE) {
+        if (small_alpha) {
+            if (tid < 32) {
+                uint32_t v = 0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) v += sh_whist[w][tid];
+                if (v) atomicAdd(&S.hist[tid], (unsigned long long)v);
+            }
+        } else {
+            for (int i = tid; i < 256; i += kThreads)
+                if (sh_hist[i]) atomicAdd(&S.hist[i], (unsigned long long)sh_hist[i]);
+        }
+        return;
+    }
+
+    // ---- slice bit counts: warp per slice, lane per run of codes --------
+    const int cpl = (D + 31) / 32;
+    bool bad = false;
+    for (int r = warp; r < bs; r += kWarps) {
+        uint32_t bits = 0;
+        for (int k = 0; k < cpl; ++k) {
+            const int c = lane * cpl + k;
+            if (c < D) {
+                const uint32_t l = cl[codes[r * D + c]];
+                bad |= (l == 0);
+                bits += l;
+            }
+        }
+        bits = kvc_warp_incl_scan(bits, lane);
+        if (lane == 31) {
+            s_bits[r] = bits;
+            bad |= bits > 0xFFFFu;
+        }
+    }
+    if (bad) kvc_set_err(P.err, KVC_ERR_CODEC);
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t carry = 0;
+        for (int r0 = 0; r0 < bs; r0 += 32) {
+            const int r = r0 + lane;
+            const uint32_t v = r < bs ? s_bits[r] : 0;
+            const uint32_t inc = kvc_warp_incl_scan(v, lane);
+            if (r < bs) s_off[r] = carry + inc - v;
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) sh_total_bits = carry;
+    }
+    __syncthreads();
+    const uint32_t total_bits = sh_total_bits;
+    const int hdr = kvc_header_bytes(bs, n_units);
+    const uint32_t pbytes = (total_bits + 7) / 8;
+    const uint32_t size = (hdr + pbytes + 3) & ~3u;
+
+    // ---- block image in shared memory (reuses the staging area) --------
+    uint32_t *img = reinterpret_cast<uint32_t *>(sm);
+    for (int i = tid; i < (int)(size >> 2); i += kThreads) img[i] = 0;
+    __syncthreads();
+    const uint32_t block_index = (P.chunk_base + (uint32_t)chunk) * (uint32_t)P.H_total +
+                                 (uint32_t)(P.head_base + hl);
+    if (tid < 4) img_or_byte(img, tid, block_index >> (8 * tid));
+    if (tid < 2) img_or_byte(img, 4 + tid, (uint32_t)bs >> (8 * tid));
+    for (int r = tid; r < bs; r += kThreads) {
+        img_or_byte(img, 6 + 2 * r, s_bits[r]);
+        img_or_byte(img, 7 + 2 * r, s_bits[r] >> 8);
+    }
+    for (int i = tid; i < 2 * n_units; i += kThreads) {
+        const uint32_t w = __float_as_uint((i & 1) ? u_sc[i >> 1] : u_lo[i >> 1]);
+        const int j0 = 6 + 2 * bs + 4 * i;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) img_or_byte(img, j0 + k, w >> (8 * k));
+    }
+    for (int r = warp; r < bs; r += kWarps) {
+        // lane's run of codes starts at the warp-exclusive prefix of lengths
+        uint32_t lbits = 0;
+        for (int k = 0; k < cpl; ++k) {
+            const int c = lane * cpl + k;
+            if (c < D) lbits += cl[codes[r * D + c]];
+        }
+        const uint32_t incl = kvc_warp_incl_scan(lbits, lane);
+        uint32_t p = (uint32_t)hdr * 8 + s_off[r] + incl - lbits;
+        uint64_t accb = 0;
+        int nacc = 0;
+        for (int k = 0; k < cpl; ++k) {
+            const int c = lane * cpl + k;
+            if (c >= D) break;
+            const uint32_t s = codes[r * D + c];
+            const int l = cl[s];
+            accb |= (uint64_t)cw[s] << (64 - nacc - l);
+            nacc += l;
+            if (nacc >= 32) {
+                img_or_bits32(img, p, (uint32_t)(accb >> 32));
+                p += 32;
+                accb <<= 32;
+                nacc -= 32;
+            }
+        }
+        if (nacc) img_or_bits32(img, p, (uint32_t)(accb >> 32));
+    }
+
+    // ---- decoupled look-back over block sizes (block_index order) ------
+    // warp 0 inspects 32 predecessors per step: waits until all have
+    // published, adds aggregates back to the nearest inclusive prefix.
+    if (warp == 0) {
+        const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kMask = (1ull << 62) - 1;
+        if (lane == 0) {
+            if (b == 0) st_release(&S.status[0], kInc | size);
+            else st_release(&S.status[b], kAgg | size);
+        }
+        unsigned long long excl = 0;
+        long hi = b - 1;  // window [hi-31, hi]
+        while (hi >= 0) {
+            const long q = hi - lane;
+            unsigned long long w = 0;
+            if (q >= 0) {
+                do { w = ld_acquire(&S.status[q]); } while ((w >> 62) == 0);
+            } else {
+                w = kInc;  // before block 0: inclusive 0
+            }
+            const uint32_t inc_mask = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+            const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;  // nearest inclusive
+            unsigned long long part = (lane <= first_inc) ? (w & kMask) : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            excl += part;
+            if (inc_mask) break;
+            hi -= 32;
+        }
+        if (lane == 0) {
+            if (b != 0) st_release(&S.status[b], kInc | (excl + size));
+            sh_excl = excl;
+        }
+    }
+    __syncthreads();
+
+    // ---- coalesced write-out at cursor + exclusive offset --------------
+    const uint64_t off = base + sh_excl;
+    const bool fits = off + size <= S.capacity && off + size <= 0xFFFFFFFFull;
+    if (fits) {
+        uint32_t *dst = reinterpret_cast<uint32_t *>(S.arena + off);
+        for (int i = tid; i < (int)(size >> 2); i += kThreads) dst[i] = __byte_perm(img[i], 0, 0x0123);
+    }
+    if (tid == 0) {
+        S.offsets[S.counters->n_blocks + b] = (uint32_t)off;
+        atomicAdd(&S.acc[2], (unsigned long long)total_bits);
+        atomicAdd(&S.acc[3], (unsigned long long)pbytes);
+        atomicMax(&S.acc[4], (unsigned long long)size);
+        __threadfence();
+        if (atomicAdd(&S.acc[1], 1ull) == (unsigned long long)(nb - 1)) {
+            __threadfence();
+            const unsigned long long total = atomicAdd(&S.status[nb - 1], 0ull) & ((1ull << 62) - 1);
+            kvc_arena_counters *ct = S.counters;
+            if (*P.err) {
+                if (!ct->err) ct->err = *P.err;
+            } else if (ct->cursor + total > S.capacity || ct->cursor + total > 0xFFFFFFFFull) {
+                if (!ct->err) ct->err = KVC_ERR_ARENA_FULL;
+            } else {
+                ct->cursor += total;
+                ct->n_blocks += (uint64_t)nb;
+                ct->payload_bits += atomicAdd(&S.acc[2], 0ull);
+                ct->payload_bytes += atomicAdd(&S.acc[3], 0ull);
+                const uint32_t mx = (uint32_t)atomicAdd(&S.acc[4], 0ull);
+                if (mx > ct->max_extent) ct->max_extent = mx;
+            }
+        }
+    }
+}
+
+size_t smem_bytes(int bs, int D, int max_len, int elem = 4) {
+    const int nv0 = bs * D;
+    const int nv = nv0;
+    const int n_units = bs > D ? bs : D;
+    const size_t img = (size_t)kvc_header_bytes(bs, n_units) + ((size_t)nv * max_len + 7) / 8 + 16;
+    size_t stage = (size_t)elem * nv;
+    stage = (stage + 15) & ~size_t(15);
+    if (img > stage) stage = (img + 15) & ~size_t(15);
+    return stage + ((nv + 15) & ~15) + 12 * (size_t)n_units + 8 * (size_t)bs + 256 * 5 + 64;
+}
+
+inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+extern "C" int kvc_store_supported(int bs, int D, int max_len) {
+    return bs >= 1 && D >= 1 && bs <= 1024 && D <= 2048 && smem_bytes(bs, D, max_len) <= 200 * 1024;
+}
+
+extern "C" size_t kvc_store_workspace_bytes(int n_chunks, int H, int D, int bs) {
+    (void)D;
+    (void)bs;
+    const size_t nb = (size_t)(n_chunks > 0 ? n_chunks : 1) * H;
+    return 2 * (a256(8 * nb) + 256) + 256;
+}
+
+static int launch_store(const StoreParams &P, int x_dtype, bool encode, int max_len,
+                        cudaStream_t s) {
+    const int nb = P.n_chunks * P.H_local;
+    const int nv = P.bs * P.D;
+    size_t sm = smem_bytes(P.bs, P.D, encode ? max_len : 1, x_dtype == KVC_F16 ? 2 : 4);
+    const int cb = nv;
+    int stage_words = (int)((sm - ((cb + 15) & ~15) - 12 * (size_t)(P.bs > P.D ? P.bs : P.D) -
+                             8 * (size_t)P.bs - 256 * 5 - 64) / 4);
+    if (sm > 200 * 1024) return kvc_fail(KVC_ERR_CONFIG, "block too large for the fused store");
+    dim3 grid(nb, 2);
+#define KVC_STORE_LAUNCH2(T, E, DT, BST)                                                       \
+    do {                                                                                       \
+        KVC_CUDA_TRY(cudaFuncSetAttribute(store_kernel<T, E, DT, BST>,                         \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                                          200 * 1024));                                        \
+        store_kernel<T, E, DT, BST><<<grid, kThreads, sm, s>>>(P, stage_words);                \
+    } while (0)
+#define KVC_STORE_LAUNCH(T, E)                                                                 \
+    do {                                                                                       \
+        if (P.D == 128 && P.bs == 64) KVC_STORE_LAUNCH2(T, E, 128, 64);                        \
+        else KVC_STORE_LAUNCH2(T, E, 0, 0);                                                    \
+    } while (0)
+    if (x_dtype == KVC_F16) {
+        if (encode) KVC_STORE_LAUNCH(__half, true);
+        else KVC_STORE_LAUNCH(__half, false);
+    } else if (x_dtype == KVC_F32) {
+        if (encode) KVC_STORE_LAUNCH(float, true);
+        else KVC_STORE_LAUNCH(float, false);
+    } else {
+        return kvc_fail(KVC_ERR_TENSOR, "unsupported dtype");
+    }
+#undef KVC_STORE_LAUNCH
+#undef KVC_STORE_LAUNCH2
+    return kvc_check_launch("store_kernel");
+}
+
+// Pass A of prefill: quantise K and V, accumulate their 256-bin histograms
+// (hist_dev: 512 x u64, K then V; codebook.py:75-80 over all heads).
+extern "C" int kvc_store_hist(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
+                              int n_chunks, int H, int D, int bs, double rel_k, double rel_v,
+                              uint64_t *hist_dev, void *stream) {
+    if (n_chunks == 0) return KVC_OK;
+    if (!kvc_store_supported(bs, D, 1)) return kvc_fail(KVC_ERR_CONFIG, "shape not supported");
+    StoreParams P{};
+    P.t[0].x = k_dev;
+    P.t[0].mode = KVC_K_BLOCK;
+    P.t[0].rel = rel_k;
+    P.t[0].hist = reinterpret_cast<unsigned long long *>(hist_dev);
+    P.t[0].max_code = (int)ceil(1.0 / rel_k);
+    P.t[1].max_code = (int)ceil(1.0 / rel_v);
+    P.t[1].x = v_dev;
+    P.t[1].mode = KVC_V_TOKEN;
+    P.t[1].rel = rel_v;
+    P.t[1].hist = reinterpret_cast<unsigned long long *>(hist_dev) + 256;
+    P.row_stride = row_stride;
+    P.n_chunks = n_chunks;
+    P.H_local = H;
+    P.H_total = H;
+    P.D = D;
+    P.bs = bs;
+    return launch_store(P, x_dtype, false, 1, static_cast<cudaStream_t>(stream));
+}
+
+// Pass B (prefill) / append event: quantise + encode + append K and V blocks
+// (kvcache.py:217-239) in one launch.
+extern "C" int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
+                                int n_chunks, int H_local, int H_total, int head_base, int D,
+                                int bs, double rel_k, double rel_v, uint32_t chunk_base,
+                                const kvc_codebook_dev *k_cb_dev, int k_max_len,
+                                const kvc_codebook_dev *v_cb_dev, int v_max_len,
+                                uint8_t *k_arena_dev, uint64_t k_capacity, uint32_t *k_offsets_dev,
+                                kvc_arena_counters *k_counters_dev, uint8_t *v_arena_dev,
+                                uint64_t v_capacity, uint32_t *v_offsets_dev,
+                                kvc_arena_counters *v_counters_dev, void *workspace_dev,
+                                size_t workspace_bytes, void *stream) {
+    if (n_chunks == 0) return KVC_OK;
+    const int max_len = k_max_len > v_max_len ? k_max_len : v_max_len;
+    if (!kvc_store_supported(bs, D, max_len)) return kvc_fail(KVC_ERR_CONFIG, "shape not supported");
+    if (workspace_bytes < kvc_store_workspace_bytes(n_chunks, H_local, D, bs))
+        return kvc_fail(KVC_ERR_CONFIG, "store workspace too small");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t nb = (size_t)n_chunks * H_local;
+    char *w = static_cast<char *>(workspace_dev);
+    const size_t per = a256(8 * nb) + 256;
+    KVC_CUDA_TRY(cudaMemsetAsync(w, 0, 2 * per + 256, s));
+    StoreParams P{};
+    for (int t = 0; t < 2; ++t) {
+        StoreTensor &T = P.t[t];
+        T.x = t ? v_dev : k_dev;
+        T.mode = t ? KVC_V_TOKEN : KVC_K_BLOCK;
+        T.rel = t ? rel_v : rel_k;
+        T.cb = t ? v_cb_dev : k_cb_dev;
+        T.arena = t ? v_arena_dev : k_arena_dev;
+        T.capacity = t ? v_capacity : k_capacity;
+        T.offsets = t ? v_offsets_dev : k_offsets_dev;
+        T.counters = t ? v_counters_dev : k_counters_dev;
+        T.status = reinterpret_cast<unsigned long long *>(w + t * per);
+        T.acc = reinterpret_cast<unsigned long long *>(w + t * per + a256(8 * nb));
+    }
+    P.row_stride = row_stride;
+    P.n_chunks = n_chunks;
+    P.H_local = H_local;
+    P.H_total = H_total;
+    P.head_base = head_base;
+    P.D = D;
+    P.bs = bs;
+    P.chunk_base = chunk_base;
+    P.err = reinterpret_cast<int *>(w + 2 * per);
+    return launch_store(P, x_dtype, true, max_len, s);
+}

@@ -24,7 +24,7 @@ from . import _lib
 from .codebook import HuffmanCodebook, build_smoothed_codebook
 from .codec import DeviceArena, worst_block_bytes
 from .errors import CodecError, ConfigError
-from .quantizer import QuantConfig, QuantMode, as_device_tensor, quantize_tokens
+from .quantizer import QuantConfig, QuantMode, as_device_tensor, dtype_code, quantize_tokens
 from .tensor_io import CacheTensor
 
 MAX_SLICE_BITS = 0xFFFF
@@ -73,6 +73,9 @@ class LayerCacheState:
         self.buffered = 0
         self._desc_dev = None
         self._desc_key = None
+        self._fused_store = bool(_lib.lib().kvc_store_supported(
+            cfg_k.block_size, head_dim, max(k_codebook.max_code_length,
+                                             v_codebook.max_code_length)))
 
     # ------------------------------------------------------------------
     @classmethod
@@ -101,9 +104,21 @@ class LayerCacheState:
         n_full = n_chunks * bs
         if cfg_k.mode is QuantMode.K_CHANNEL:
             raise ConfigError("K_CHANNEL mode is not implemented on the device yet")
+        if kt.dtype != vt.dtype:
+            kt, vt = kt.to(torch.float32), vt.to(torch.float32)
+        lib = _lib.lib()
+        stream = torch.cuda.current_stream(kt.device).cuda_stream
+        fused = bool(lib.kvc_store_supported(bs, D, 32 if codebooks is None else max(
+            codebooks[0].max_code_length, codebooks[1].max_code_length)))
         hist = torch.zeros(512, dtype=torch.int64, device=kt.device)
         kcodes = kmetas = vcodes = vmetas = None
-        if n_full:
+        if n_full and codebooks is None and fused:
+            # pass A: quantise + histogram only (store_fused.cu)
+            _lib.check(lib.kvc_store_hist(kt.data_ptr(), vt.data_ptr(), dtype_code(kt), H * D,
+                                          n_chunks, H, D, bs, cfg_k.rel_quant_scale,
+                                          cfg_v.rel_quant_scale, hist.data_ptr(), stream),
+                       "kvc_store_hist")
+        elif n_full and not fused:
             kcodes, kmetas = quantize_tokens(kt, n_chunks, H, D, bs, cfg_k.mode,
                                              cfg_k.rel_quant_scale,
                                              hist[:256] if codebooks is None else None)
@@ -121,7 +136,15 @@ class LayerCacheState:
         st = cls(H, D, cfg_k, cfg_v, k_cb, v_cb, dtype=src_dtype, device=kt.device,
                  head_base=head_base, head_total=head_total, capacity=capacity)
         if n_full:
-            st._encode(kcodes, kmetas, vcodes, vmetas, n_chunks)
+            if st._fused_store:
+                st._store(kt, vt, n_chunks)
+            else:
+                if kcodes is None:
+                    kcodes, kmetas = quantize_tokens(kt, n_chunks, H, D, bs, cfg_k.mode,
+                                                     cfg_k.rel_quant_scale)
+                    vcodes, vmetas = quantize_tokens(vt, n_chunks, H, D, bs, QuantMode.V_TOKEN,
+                                                     cfg_v.rel_quant_scale)
+                st._encode(kcodes, kmetas, vcodes, vmetas, n_chunks)
         r = ctx - n_full
         if r:
             st._k_buffer[:r] = kt[n_full:].to(torch.float32)
@@ -159,10 +182,38 @@ class LayerCacheState:
             arena.note_append(nb, worst)
         self.compressed_tokens += n_chunks * bs
 
+    def _store(self, k_src: torch.Tensor, v_src: torch.Tensor, n_chunks: int) -> None:
+        """Single-launch quantise + encode + append of n_chunks*H blocks per
+        tensor from k_src/v_src rows [0, n_chunks*bs) (store_fused.cu)."""
+        bs, H, D = self.cfg_k.block_size, self.head_num, self.head_dim
+        lib = _lib.lib()
+        nb = n_chunks * H
+        kw = nb * worst_block_bytes(bs, D, D, self.k_codebook.max_code_length)
+        vw = nb * worst_block_bytes(bs, bs, D, self.v_codebook.max_code_length)
+        self.k_arena.reserve(nb, kw)
+        self.v_arena.reserve(nb, vw)
+        ws = self._workspace(lib.kvc_store_workspace_bytes(n_chunks, H, D, bs))
+        st = lib.kvc_store_append(
+            k_src.data_ptr(), v_src.data_ptr(), dtype_code(k_src), H * D, n_chunks, H,
+            self.head_total, self.head_base, D, bs, self.cfg_k.rel_quant_scale,
+            self.cfg_v.rel_quant_scale, self.compressed_tokens // bs, self._k_tab.data_ptr(),
+            self.k_codebook.max_code_length, self._v_tab.data_ptr(),
+            self.v_codebook.max_code_length, self.k_arena.buf_ptr, self.k_arena.alloc_capacity,
+            self.k_arena.offsets_ptr, self.k_arena.counters_ptr, self.v_arena.buf_ptr,
+            self.v_arena.alloc_capacity, self.v_arena.offsets_ptr, self.v_arena.counters_ptr,
+            ws.data_ptr(), ws.numel(), torch.cuda.current_stream(self.device).cuda_stream)
+        _lib.check(st, "kvc_store_append")
+        self.k_arena.note_append(nb, kw)
+        self.v_arena.note_append(nb, vw)
+        self.compressed_tokens += n_chunks * bs
+
     def _compress_buffer(self, n: int) -> None:
         """Compress buffer rows [0, n) (n a multiple of block_size)."""
         bs = self.cfg_k.block_size
         n_chunks = n // bs
+        if self._fused_store:
+            self._store(self._k_buffer, self._v_buffer, n_chunks)
+            return
         kcodes, kmetas = quantize_tokens(self._k_buffer, n_chunks, self.head_num, self.head_dim,
                                          bs, self.cfg_k.mode, self.cfg_k.rel_quant_scale)
         vcodes, vmetas = quantize_tokens(self._v_buffer, n_chunks, self.head_num, self.head_dim,

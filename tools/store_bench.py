@@ -1,0 +1,104 @@
+"""Store-path timing: prefill passes and growing-cache append events.
+
+Times, with CUDA events on the launching stream:
+  * prefill of one config-2 (seq, layer) slice (32K tokens x 40 heads x 128,
+    fp16): pass A (kvc_store_hist), the host codebook build, pass B
+    (kvc_store_append) and the whole LayerCacheState.prefill call;
+  * a config-4-style append event (128 tokens x H heads, from the f32 buffer)
+    through LayerCacheState._store, i.e. one kvc_store_append launch.
+Prints one JSON line.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2509_00579_b200 as kv  # noqa: E402
+from paper_2509_00579_b200 import _lib  # noqa: E402
+
+
+def ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+def main(ctx=32768, H=40, D=128, reps=10):
+    dev = torch.device("cuda")
+    k = kv.generate_synthetic_device(kv.SyntheticSpec(ctx, H, D, seed=0), dev)
+    v = kv.generate_synthetic_device(kv.SyntheticSpec(ctx, H, D, seed=1), dev)
+    ck, cv = kv.QuantConfig(kv.QuantMode.K_BLOCK), kv.QuantConfig(kv.QuantMode.V_TOKEN)
+    lib = _lib.lib()
+    s = torch.cuda.current_stream()
+    nb_chunks = ctx // 64
+    in_bytes = 2 * ctx * H * D * 2
+    # whole prefill (host sync for the histogram included)
+    for _ in range(2):
+        st = kv.LayerCacheState.prefill(k, v, ck, cv, check=False)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        st = kv.LayerCacheState.prefill(k, v, ck, cv, check=False)
+    torch.cuda.synchronize()
+    t_prefill = (time.perf_counter() - t0) / reps
+    # pass A alone
+    hist = torch.zeros(512, dtype=torch.int64, device=dev)
+    a, b = ev(), ev()
+    a.record(s)
+    for _ in range(reps):
+        lib.kvc_store_hist(k.data_ptr(), v.data_ptr(), 0, H * D, nb_chunks, H, D, 64, 0.05, 0.15,
+                           hist.data_ptr(), s.cuda_stream)
+    b.record(s)
+    torch.cuda.synchronize()
+    t_a = a.elapsed_time(b) / reps * 1e-3
+    # pass B alone: re-encode into fresh states with known codebooks
+    cbs = (st.k_codebook, st.v_codebook)
+    fresh = [kv.LayerCacheState(H, D, ck, cv, cbs[0], cbs[1], dtype=np.float16, device=dev)
+             for _ in range(reps)]
+    for f in fresh:  # pre-size arenas so timing excludes allocation
+        f.k_arena.reserve(nb_chunks * H, nb_chunks * H * 7400)
+        f.v_arena.reserve(nb_chunks * H, nb_chunks * H * 7000)
+        f._workspace(lib.kvc_store_workspace_bytes(nb_chunks, H, D, 64))
+    torch.cuda.synchronize()
+    a.record(s)
+    for f in fresh:
+        f._store(k, v, nb_chunks)
+    b.record(s)
+    torch.cuda.synchronize()
+    t_b = a.elapsed_time(b) / reps * 1e-3
+    ok = fresh[0].k_arena.snapshot() == st.k_arena.snapshot()
+    # append event: 128 tokens x H heads from the f32 buffers (config 4 shape H=32)
+    He = 32
+    ke = kv.generate_synthetic_device(kv.SyntheticSpec(4096, He, D, seed=2), dev)
+    ve = kv.generate_synthetic_device(kv.SyntheticSpec(4096, He, D, seed=3), dev)
+    se = kv.LayerCacheState.prefill(ke, ve, ck, cv)
+    se._k_buffer[:128] = ke[:128].float()
+    se._v_buffer[:128] = ve[:128].float()
+    n_ev = 64
+    se.k_arena.reserve(n_ev * 2 * He, n_ev * 2 * He * 7400)
+    se.v_arena.reserve(n_ev * 2 * He, n_ev * 2 * He * 7000)
+    torch.cuda.synchronize()
+    a.record(s)
+    for _ in range(n_ev):
+        se._store(se._k_buffer, se._v_buffer, 2)
+    b.record(s)
+    torch.cuda.synchronize()
+    t_ev = a.elapsed_time(b) / n_ev * 1e-3
+    ev_bytes = 2 * 128 * He * D * 4
+    se.check()
+    print(json.dumps({
+        "prefill_slice": {"shape": [ctx, H, D], "fp16_in_bytes": in_bytes,
+                          "prefill_s": t_prefill, "prefill_gbs": in_bytes / t_prefill / 1e9,
+                          "passA_s": t_a, "passA_gbs": in_bytes / t_a / 1e9,
+                          "passB_s": t_b, "passB_gbs": in_bytes / t_b / 1e9,
+                          "device_gbs": in_bytes / (t_a + t_b) / 1e9,
+                          "passB_bit_exact_vs_prefill": ok},
+        "append_event": {"tokens": 128, "heads": He, "us_per_event": t_ev * 1e6,
+                         "gbs_f32_in": ev_bytes / t_ev / 1e9},
+    }))
+
+
+if __name__ == "__main__":
+    main()
