@@ -346,6 +346,11 @@ def main():
     comp_gbs = comp_bytes_step * world_f / (ms * 1e-3) / 1e9
     e2e_val = eq_bytes_step * world_f / (e2e_ms * 1e-3) / 1e9
     store_gbs = store_bytes / float(np.median(store_times)) / 1e9
+    store_detail = None
+    if rank == 0:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import store_bench
+        store_detail = store_bench.main(ctx=T, H=hl, D=128, reps=5)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -372,10 +377,17 @@ def main():
                            "kernel, one layer, same shape"},
             "speedup_vs_dense_fp16": round(value / dense_gbs, 3),
             "store": {"compress_gbs": round(store_gbs, 3), "unit": "GB/s fp16 K+V in",
-                      "note": "LayerCacheState.prefill of one (seq, layer) incl. host codebook"},
+                      "note": "LayerCacheState.prefill of one (seq, layer) incl. histogram "
+                              "D2H + host codebook (wall clock)",
+                      "device_passA_gbs": round(store_detail["prefill_slice"]["passA_gbs"], 2),
+                      "device_passB_gbs": round(store_detail["prefill_slice"]["passB_gbs"], 2),
+                      "device_prefill_gbs": round(store_detail["prefill_slice"]["device_gbs"], 2),
+                      "append_event_us": round(store_detail["append_event"]["us_per_event"], 2),
+                      "append_event": "config 4: 128 tokens x 32 heads x 128 from the f32 "
+                                      "buffer, one kvc_store_append launch"},
             "roofline": {"bound": "hbm", "achieved": round(ach, 2), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
-                         "traffic": None, "peak_kind": peak_kind,
+                         "traffic": _ncu_traffic(), "peak_kind": peak_kind,
                          "kernel": "fused_attn_kernel (+combine), one layer launch, "
                                    "compressed bytes"},
             "e2e": {"value": round(e2e_val, 2), "unit": "GB/s (equivalent fp16 KV)",
@@ -389,6 +401,21 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _ncu_traffic():
+    """dram read+write bytes per fused-kernel launch from the committed ncu
+    --set full capture (profiles/fused_ncu_latest.json), if present."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fused_ncu_latest.json")) as fh:
+            d = json.load(fh)
+        def gb(v):
+            num, unit = v.split()[0], v.split()[1] if len(v.split()) > 1 else "byte"
+            mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            return float(num) * mul
+        return int(gb(d["dram__bytes_read.sum"]) + gb(d["dram__bytes_write.sum"]))
+    except Exception:
+        return None
 
 
 def _lib_ws(kv, B, H, max_chunks):

@@ -88,7 +88,7 @@ def main(ctx=32768, H=40, D=128, reps=10):
     t_ev = a.elapsed_time(b) / n_ev * 1e-3
     ev_bytes = 2 * 128 * He * D * 4
     se.check()
-    print(json.dumps({
+    return {
         "prefill_slice": {"shape": [ctx, H, D], "fp16_in_bytes": in_bytes,
                           "prefill_s": t_prefill, "prefill_gbs": in_bytes / t_prefill / 1e9,
                           "passA_s": t_a, "passA_gbs": in_bytes / t_a / 1e9,
@@ -97,8 +97,8 @@ def main(ctx=32768, H=40, D=128, reps=10):
                           "passB_bit_exact_vs_prefill": ok},
         "append_event": {"tokens": 128, "heads": He, "us_per_event": t_ev * 1e6,
                          "gbs_f32_in": ev_bytes / t_ev / 1e9},
-    }))
+    }
 
 
 if __name__ == "__main__":
-    main()
+    print(json.dumps(main()))
