@@ -10,6 +10,7 @@
 // (m, l, o[128]) are merged, together with the f32 buffered tokens, by
 // combine_kernel.  Also: the uncompressed fp16 decode-attention comparator.
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -496,6 +497,14 @@ __device__ __forceinline__ void cursor2_reload(Cursor2 &c) {
     c.hi = __funnelshift_l(w1, w0, c.p);
     c.lo = __funnelshift_l(w2, w1, c.p);
 }
+// single-symbol step on the lane-replicated 64-entry LUT (entry = float | len)
+__device__ __forceinline__ uint32_t cursor2_sym(Cursor2 &c, uint32_t lane_s) {
+    const uint32_t e = lds32(lane_s + ((c.hi >> 26) << 7));
+    c.hi = __funnelshift_l(c.lo, c.hi, e);
+    c.lo = __funnelshift_l(0u, c.lo, e);
+    c.p += e;
+    return e;
+}
 __device__ __forceinline__ float2 cursor2_pair(Cursor2 &c, uint32_t lut_s) {
     const uint32_t e = lds32(lut_s + ((c.hi >> 20) << 2));
     c.hi = __funnelshift_l(c.lo, c.hi, e);
@@ -574,12 +583,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int MODE>
+template <int MODE, int VMODE>
 __global__ void __launch_bounds__(kThreadsWS, 2)
 fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__restrict__ q,
                      float *__restrict__ scores, long ctx_stride, Partial *__restrict__ partial,
                      int chunks_per_split, int n_splits, int stage_k, int stage_v, int *err) {
-    __shared__ __align__(128) uint32_t s_lut[2][Dec<MODE>::kLutWords];
+    __shared__ __align__(128) uint32_t s_lutK[Dec<MODE>::kLutWords];
+    __shared__ __align__(128) uint32_t s_lutV[Dec<VMODE>::kLutWords];
     __shared__ uint64_t s_lbar[1];
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
@@ -606,20 +616,18 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
         mbar_init(&sempty[0], 32);
         mbar_init(&sempty[1], 32);
     }
-    if (MODE == 1 && threadIdx.x == 0) mbar_init(s_lbar, 1);
+    constexpr bool kTma = MODE == 1 || VMODE == 1;
+    if (kTma && threadIdx.x == 0) mbar_init(s_lbar, 1);
     fence_mbar_init();
     __syncthreads();
-    if (MODE == 1) {
-        if (threadIdx.x == 0) {
-            mbar_expect_tx(s_lbar, 2u * (4u << KVC_LUT_BITS));
-            tma_load_1d(s_lut[0], sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
-            tma_load_1d(s_lut[1], sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
-        }
-    } else {
-        build_lut<MODE>(s_lut[0], sd.k_cb);
-        build_lut<MODE>(s_lut[1], sd.v_cb);
-        __syncthreads();
+    if (kTma && threadIdx.x == 0) {
+        mbar_expect_tx(s_lbar, ((MODE == 1) + (VMODE == 1)) * (4u << KVC_LUT_BITS));
+        if (MODE == 1) tma_load_1d(s_lutK, sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+        if (VMODE == 1) tma_load_1d(s_lutV, sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
     }
+    if (MODE != 1) build_lut<MODE>(s_lutK, sd.k_cb);
+    if (VMODE != 1) build_lut<VMODE>(s_lutV, sd.v_cb);
+    if (MODE != 1 || VMODE != 1) __syncthreads();
 
     const int c_begin = split * chunks_per_split;
     const int c_end = min(sd.n_chunks, c_begin + chunks_per_split);
@@ -648,8 +656,6 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
         mbar_expect_tx(b, bytes);
         tma_load_1d(dst, (v ? sd.v_arena : sd.k_arena) + a, bytes, b);
     };
-    const uint32_t lut_s = smem_u32(s_lut[is_v ? 1 : 0]);
-    const uint32_t lane_s = lut_s + 4 * lane;
     bool bad = false;
 
     if (!is_v) {
@@ -664,7 +670,9 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
 #pragma unroll
         for (int k = 0; k < 4; ++k) qreg[k] = qh[lane + 32 * k];
         const uint32_t qf_s = smem_u32(qf);
-        if (MODE == 1) mbar_wait(s_lbar, 0);
+        const uint32_t lut_s = smem_u32(s_lutK);
+        const uint32_t lane_s = lut_s + 4 * lane;
+        if (kTma) mbar_wait(s_lbar, 0);
         for (int j = 0; j < n; ++j) {
             const int u = j >> 1, sl = j & 1;
             mbar_wait(&kfull[sl], u & 1);
@@ -691,30 +699,24 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
             const uint32_t p0A = cur[0].p, p0B = cur[1].p;
             float2 sA2 = make_float2(0.f, 0.f), sB2 = sA2;
             if (MODE == 1) {
+                // 64-bit windows, one reload per 5 pair steps (<= 60 bits at
+                // max_len 6): 12 groups of 5 + a tail of 4 pair steps.
                 Cursor2 c2c[2];
                 cursor2_init(c2c[0], slot, bit0 + iA - cA);
                 cursor2_init(c2c[1], slot, bit0 + totA + iB - cB);
-#pragma unroll 1
-                for (int g = 0; g < D / 16; ++g) {   // 8 pair steps = 16 channels per group
-                    float4 qv[4];
+                auto steps = [&](int c2base, auto np) {
+                    cursor2_reload(c2c[0]);
+                    cursor2_reload(c2c[1]);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        asm volatile(KVC_LD_SHARED ".v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(qv[k].x), "=f"(qv[k].y), "=f"(qv[k].z), "=f"(qv[k].w)
-                                     : "r"(qf_s + 64 * g + 16 * k));
-                    }
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) {
-                        if (t % 4 == 0) {
-                            cursor2_reload(c2c[0]);
-                            cursor2_reload(c2c[1]);
-                        }
-                        const float4 qq = qv[t / 2];
-                        const float2 q2 = (t & 1) ? make_float2(qq.z, qq.w) : make_float2(qq.x, qq.y);
+                    for (int t = 0; t < decltype(np)::value; ++t) {
+                        const float2 q2 = lds64f(qf_s + 8 * (c2base + t));
                         sA2 = __ffma2_rn(cursor2_pair(c2c[0], lut_s), q2, sA2);
                         sB2 = __ffma2_rn(cursor2_pair(c2c[1], lut_s), q2, sB2);
                     }
-                }
+                };
+#pragma unroll 1
+                for (int g = 0; g < 12; ++g) steps(5 * g, std::integral_constant<int, 5>());
+                steps(60, std::integral_constant<int, 4>());
                 cur[0].p = c2c[0].p;
                 cur[1].p = c2c[1].p;
             } else {
@@ -755,7 +757,9 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
     float2 acc[D / 2];
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) acc[c] = make_float2(0.f, 0.f);
-    if (MODE == 1) mbar_wait(s_lbar, 0);
+    const uint32_t lut_s = smem_u32(s_lutV);
+    const uint32_t lane_s = lut_s + 4 * lane;
+    if (kTma) mbar_wait(s_lbar, 0);
     for (int j = 0; j < n; ++j) {
         const int u = j >> 1, sl = j & 1;
         mbar_wait(&sfull[sl], u & 1);
@@ -791,23 +795,33 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
         cursor_init(cur[0], slot, bit0 + iA - cA);
         cursor_init(cur[1], slot, bit0 + totA + iB - cB);
         const uint32_t p0A = cur[0].p, p0B = cur[1].p;
-        if (MODE == 1) {
+        if (VMODE == 1 || VMODE == 0) {
+            // 64-bit windows; 5 pair steps (<= 60 bits at max_len 6) per reload
             Cursor2 c2c[2];
             cursor2_init(c2c[0], slot, bit0 + iA - cA);
             cursor2_init(c2c[1], slot, bit0 + totA + iB - cB);
 #pragma unroll
             for (int c2 = 0; c2 < D / 2; ++c2) {
-                if (c2 % 4 == 0) {
+                if (c2 % 5 == 0) {
                     cursor2_reload(c2c[0]);
                     cursor2_reload(c2c[1]);
                 }
-                acc[c2] = __ffma2_rn(cursor2_pair(c2c[0], lut_s), aA2, acc[c2]);
-                acc[c2] = __ffma2_rn(cursor2_pair(c2c[1], lut_s), aB2, acc[c2]);
+                if (VMODE == 1) {
+                    acc[c2] = __ffma2_rn(cursor2_pair(c2c[0], lut_s), aA2, acc[c2]);
+                    acc[c2] = __ffma2_rn(cursor2_pair(c2c[1], lut_s), aB2, acc[c2]);
+                } else {
+                    const uint32_t a0 = cursor2_sym(c2c[0], lane_s), b0 = cursor2_sym(c2c[1], lane_s);
+                    const uint32_t a1 = cursor2_sym(c2c[0], lane_s), b1 = cursor2_sym(c2c[1], lane_s);
+                    acc[c2] = __ffma2_rn(make_float2(__uint_as_float(a0 & ~15u), __uint_as_float(a1 & ~15u)),
+                                         aA2, acc[c2]);
+                    acc[c2] = __ffma2_rn(make_float2(__uint_as_float(b0 & ~15u), __uint_as_float(b1 & ~15u)),
+                                         aB2, acc[c2]);
+                }
             }
             cur[0].p = c2c[0].p;
             cur[1].p = c2c[1].p;
         } else {
-            decode_two<MODE, true>(cur, lut_s, lane_s, [&](int c2, float2 fA, float2 fB) {
+            decode_two<VMODE, true>(cur, lut_s, lane_s, [&](int c2, float2 fA, float2 fB) {
                 acc[c2] = __ffma2_rn(fA, aA2, acc[c2]);
                 acc[c2] = __ffma2_rn(fB, aB2, acc[c2]);
             });
@@ -1136,28 +1150,24 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         if (sizeof(Partial) * (size_t)n_seqs * H * ws_splits > workspace_bytes)
             return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
         dim3 g2(ws_splits, H, n_seqs);
-        if (mode == 0) {
-            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_ws_kernel<0>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)ws_smem));
-            fused_attn_ws_kernel<0><<<g2, kThreadsWS, ws_smem, s>>>(
-                seqs_dev, H, q_dev, scores_dev, ctx_stride, part, ws_cps, ws_splits, stage_k,
-                stage_v, err_dev);
-        } else if (mode == 1) {
-            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_ws_kernel<1>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)ws_smem));
-            fused_attn_ws_kernel<1><<<g2, kThreadsWS, ws_smem, s>>>(
-                seqs_dev, H, q_dev, scores_dev, ctx_stride, part, ws_cps, ws_splits, stage_k,
-                stage_v, err_dev);
-        } else {
-            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_ws_kernel<2>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)ws_smem));
-            fused_attn_ws_kernel<2><<<g2, kThreadsWS, ws_smem, s>>>(
-                seqs_dev, H, q_dev, scores_dev, ctx_stride, part, ws_cps, ws_splits, stage_k,
-                stage_v, err_dev);
-        }
+        // V decoder: pair LUT (measured fastest); KVC_FUSED_VMODE=0 selects the
+        // lane-replicated, bank-conflict-free single-symbol LUT6 instead.
+        const char *venv = getenv("KVC_FUSED_VMODE");
+        const int vmode = (mode == 2) ? 2 : (venv && venv[0] == '0' ? 0 : 1);
+#define KVC_LAUNCH_WS(M, VM)                                                                 \
+    do {                                                                                     \
+        KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_ws_kernel<M, VM>,                       \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                          (int)ws_smem));                                    \
+        fused_attn_ws_kernel<M, VM><<<g2, kThreadsWS, ws_smem, s>>>(                         \
+            seqs_dev, H, q_dev, scores_dev, ctx_stride, part, ws_cps, ws_splits, stage_k,    \
+            stage_v, err_dev);                                                               \
+    } while (0)
+        if (mode == 2) KVC_LAUNCH_WS(2, 2);
+        else if (mode == 0) KVC_LAUNCH_WS(0, 0);
+        else if (vmode == 0) KVC_LAUNCH_WS(1, 0);
+        else KVC_LAUNCH_WS(1, 1);
+#undef KVC_LAUNCH_WS
         int st = kvc_check_launch("fused_attn_ws_kernel");
         if (st) return st;
         combine_kernel<<<dim3(1, H, n_seqs), 128, 0, s>>>(seqs_dev, H, bs, q_dev, part, ws_splits,
