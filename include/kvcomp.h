@@ -156,10 +156,12 @@ size_t kvc_encode_workspace_bytes(int nb, int bs);
 
 /* Store pass A of prefill (kvcache.py:110-121): quantise the full blocks of K
  * and V and accumulate their code histograms (hist_dev: 512 x u64, K bins
- * then V bins).  No codes are written. */
+ * then V bins).  No codes are written.  k_mode KVC_K_BLOCK or KVC_K_CHANNEL;
+ * K_CHANNEL takes k_ranges_dev = f32 [2][H][D] whole-context (min, max) and
+ * clips codes to [0, ceil(1/rel)] (quantizer.py:191-197). */
 int kvc_store_hist(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
-                   int n_chunks, int H, int D, int bs, double rel_k, double rel_v,
-                   uint64_t *hist_dev, void *stream);
+                   int n_chunks, int H, int D, int bs, int k_mode, double rel_k, double rel_v,
+                   const float *k_ranges_dev, uint64_t *hist_dev, void *stream);
 
 /* 1 if the single-pass Store kernels cover this block shape / code length. */
 int kvc_store_supported(int bs, int D, int max_len);
@@ -170,7 +172,8 @@ int kvc_store_supported(int bs, int D, int max_len);
  * block_index order (deterministic, no code round trip through HBM). */
 int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
                      int n_chunks, int H_local, int H_total, int head_base, int D, int bs,
-                     double rel_k, double rel_v, uint32_t chunk_base,
+                     int k_mode, double rel_k, double rel_v, const float *k_ranges_dev,
+                     uint32_t chunk_base,
                      const kvc_codebook_dev *k_cb_dev, int k_max_len,
                      const kvc_codebook_dev *v_cb_dev, int v_max_len, uint8_t *k_arena_dev,
                      uint64_t k_capacity, uint32_t *k_offsets_dev,

@@ -58,9 +58,11 @@ def lib():
             "orc_encode_block": (i, [P, i, i, P, P, i, ctypes.c_uint32, P, P, P, P]),
             "orc_decode_block": (i, [P, l, i, i, P, P, P, P, P, P]),
             "orc_compress_tokens": (i, [P, i, i, i, i, i, d, ctypes.c_uint32, P, P, l, P, P, P, i]),
-            "orc_compress_tokens_shard": (i, [P, i, i, i, i, i, d, ctypes.c_uint32, i, i, P, P, l,
-                                              P, P, P, i]),
+            "orc_compress_tokens_shard": (i, [P, i, i, i, i, i, d, ctypes.c_uint32, i, i, P, P, P,
+                                              l, P, P, P, i]),
             "orc_tokens_histogram": (i, [P, i, i, i, i, i, d, P, i]),
+            "orc_tokens_histogram_r": (i, [P, i, i, i, i, i, d, P, P, i]),
+            "orc_quantize_block_ranges": (i, [P, l, i, i, d, P, P, P, P, P]),
             "orc_k_scores": (i, [P, P, l, l, i, i, i, P, P, P, i, l, P, i]),
             "orc_softmax_rows": (None, [P, l, l, P]),
             "orc_v_output": (i, [P, P, l, l, i, i, i, P, P, P, i, l, P, i]),
@@ -165,8 +167,10 @@ class OracleState:
     """CPU mirror of the reference LayerCacheState (K_BLOCK + V_TOKEN)."""
 
     def __init__(self, H, D, bs, buffer, rel_k, rel_v, k_lengths, v_lengths, itemsize=4,
-                 n_threads=1):
+                 n_threads=1, k_ranges=None):
         self.H, self.D, self.bs, self.buffer = H, D, bs, buffer
+        # K_CHANNEL: float32 [2, H, D] whole-context (min, max) (kvcache.py:104-108)
+        self.k_ranges = None if k_ranges is None else np.ascontiguousarray(k_ranges, np.float32)
         self.rel_k, self.rel_v = float(rel_k), float(rel_v)
         self.k_lengths = np.asarray(k_lengths, np.uint8).copy()
         self.v_lengths = np.asarray(v_lengths, np.uint8).copy()
@@ -188,24 +192,29 @@ class OracleState:
 
     @classmethod
     def prefill(cls, k, v, bs=64, buffer=None, rel_k=0.05, rel_v=0.15, codebooks=None,
-                n_threads=1):
+                n_threads=1, k_mode="kblock"):
         itemsize = np.asarray(k).dtype.itemsize
         k = np.ascontiguousarray(k, dtype=np.float32)
         v = np.ascontiguousarray(v, dtype=np.float32)
         buffer = 2 * bs if buffer is None else buffer
         ctx, H, D = k.shape
         n_full = (ctx // bs) * bs
+        ranges = None
+        if k_mode == "kchannel":
+            ranges = np.ascontiguousarray(np.stack([k.min(axis=0), k.max(axis=0)]), np.float32)
         if codebooks is None:
             hk = np.zeros(256, np.uint64)
             hv = np.zeros(256, np.uint64)
             if n_full:
-                lib().orc_tokens_histogram(_p(k), n_full, H, D, bs, 0, rel_k, _p(hk), n_threads)
+                lib().orc_tokens_histogram_r(_p(k), n_full, H, D, bs, 0, rel_k,
+                                             _p(ranges) if ranges is not None else None, _p(hk),
+                                             n_threads)
                 lib().orc_tokens_histogram(_p(v), n_full, H, D, bs, 1, rel_v, _p(hv), n_threads)
             kl = huffman_lengths(smooth_histogram(hk, cls.max_code(rel_k)))
             vl = huffman_lengths(smooth_histogram(hv, cls.max_code(rel_v)))
         else:
             kl, vl = codebooks
-        st = cls(H, D, bs, buffer, rel_k, rel_v, kl, vl, itemsize, n_threads)
+        st = cls(H, D, bs, buffer, rel_k, rel_v, kl, vl, itemsize, n_threads, k_ranges=ranges)
         if n_full:
             st._compress(k[:n_full], v[:n_full])
         r = ctx - n_full
@@ -227,10 +236,12 @@ class OracleState:
         offs = np.zeros(max(nb, 1), np.uint32)
         bits = np.zeros(max(nb, 1), np.uint64)
         tokens = np.ascontiguousarray(tokens, np.float32)
-        _chk(lib().orc_compress_tokens(_p(tokens), n, self.H, self.D, self.bs, mode, rel,
-                                       self.compressed_tokens // self.bs, _p(lengths), _p(buf),
-                                       -1, ctypes.byref(cursor), _p(offs), _p(bits),
-                                       self.n_threads), "compress")
+        ranges = self.k_ranges if (which == "k" and self.k_ranges is not None) else None
+        _chk(lib().orc_compress_tokens_shard(_p(tokens), n, self.H, self.D, self.bs, mode, rel,
+                                             self.compressed_tokens // self.bs, self.H, 0,
+                                             _p(ranges) if ranges is not None else None,
+                                             _p(lengths), _p(buf), -1, ctypes.byref(cursor),
+                                             _p(offs), _p(bits), self.n_threads), "compress")
         self.arena[which] = bytearray(buf[: cursor.value].tobytes())
         self.offsets[which] += [int(o) for o in offs[:nb]]
         self.payload_bits[which] += int(bits[:nb].sum())
@@ -338,7 +349,7 @@ def compress_shard(tokens, bs, mode, rel, lengths, H_total, head_base, chunk_bas
     bits = np.zeros(max(nb, 1), np.uint64)
     lengths = np.ascontiguousarray(lengths, np.uint8)
     _chk(lib().orc_compress_tokens_shard(_p(tokens), n, H, D, bs, m, float(rel), chunk_base,
-                                         H_total, head_base, _p(lengths), _p(buf), -1,
+                                         H_total, head_base, None, _p(lengths), _p(buf), -1,
                                          ctypes.byref(cursor), _p(offs), _p(bits), n_threads),
          "compress_shard")
     return buf[: cursor.value].tobytes(), offs[:nb].copy()

@@ -63,15 +63,23 @@ static void parallel_for(long n, int n_threads, range_fn fn, void *ctx)
 /* Quantisation (quantizer.py:107-141, :162-209)                        */
 /* ------------------------------------------------------------------ */
 
-/* Quantise n values x[i*stride] sharing one (min, scale) unit. */
-static void quant_unit(const float *x, long stride, int n, double rel, uint8_t *codes,
-                       long cstride, float *vmin_out, float *scale_out)
+/* Quantise n values x[i*stride] sharing one (min, scale) unit.  With
+ * fixed_range (K_CHANNEL, quantizer.py:191-197) the unit range is given and
+ * codes are clipped to [0, clamp_max]. */
+static void quant_unit_r(const float *x, long stride, int n, double rel, uint8_t *codes,
+                         long cstride, float *vmin_out, float *scale_out, const float *fixed_range,
+                         int clamp_max)
 {
     float lo = x[0], hi = x[0];
-    for (int i = 1; i < n; ++i) {
-        float v = x[(long)i * stride];
-        if (v < lo) lo = v;
-        if (v > hi) hi = v;
+    if (fixed_range) {
+        lo = fixed_range[0];
+        hi = fixed_range[1];
+    } else {
+        for (int i = 1; i < n; ++i) {
+            float v = x[(long)i * stride];
+            if (v < lo) lo = v;
+            if (v > hi) hi = v;
+        }
     }
     /* min/max of f32 values are exact; scale = f32(rel64 * (max64 - min64)) */
     float scale = (float)(rel * ((double)hi - (double)lo));
@@ -82,6 +90,10 @@ static void quant_unit(const float *x, long stride, int n, double rel, uint8_t *
             double t = ((double)x[(long)i * stride] - (double)lo) / s64;
             double f = floor(t);
             if (t - f >= 0.5) f += 1.0;
+            if (fixed_range) {
+                if (f < 0) f = 0;
+                if (f > clamp_max) f = clamp_max;
+            }
             c = (uint8_t)f;
         }
         codes[(long)i * cstride] = c;
@@ -90,11 +102,30 @@ static void quant_unit(const float *x, long stride, int n, double rel, uint8_t *
     *scale_out = scale;
 }
 
+static void quant_unit(const float *x, long stride, int n, double rel, uint8_t *codes,
+                       long cstride, float *vmin_out, float *scale_out)
+{
+    quant_unit_r(x, stride, n, rel, codes, cstride, vmin_out, scale_out, NULL, 0);
+}
+
 /*
  * Quantise one (bs, D) block.  mode 0 = K_BLOCK (one unit per column),
  * mode 1 = V_TOKEN (one unit per row).  x rows are `row_stride` floats apart
  * (so a [ctx, H, D] tensor can be addressed in place).
  */
+/* K_CHANNEL (mode 2): ranges = [D] mins then [D] maxs for this head. */
+int orc_quantize_block_ranges(const float *x, long row_stride, int bs, int D, double rel,
+                              const float *rmin, const float *rmax, uint8_t *codes, float *mins,
+                              float *scales)
+{
+    int clamp_max = (int)ceil(1.0 / rel);
+    for (int c = 0; c < D; ++c) {
+        float r[2] = {rmin[c], rmax[c]};
+        quant_unit_r(x + c, row_stride, bs, rel, codes + c, D, &mins[c], &scales[c], r, clamp_max);
+    }
+    return ORC_OK;
+}
+
 int orc_quantize_block(const float *x, long row_stride, int bs, int D, int mode, double rel,
                        uint8_t *codes, float *mins, float *scales)
 {
@@ -387,6 +418,7 @@ int orc_decode_block(const uint8_t *ext, long len, int n_units, int D, const uin
 typedef struct {
     const float *tokens; int H, D, bs, mode, n_units; double rel; uint32_t chunk_base;
     int H_total, head_base;
+    const float *ranges;  /* K_CHANNEL: [2][H][D] (mins, maxs) of this shard, or NULL */
     const uint8_t *lengths; const uint32_t *words; uint8_t *tmp; long max_block;
     long *sizes; uint64_t *pbits; int err;
 } compress_ctx;
@@ -400,7 +432,13 @@ static void compress_range(long lo, long hi, int tid, void *p)
     for (long b = lo; b < hi; ++b) {
         int chunk = (int)(b / c->H), head = (int)(b % c->H);
         const float *x = c->tokens + ((long)chunk * c->bs * c->H + head) * c->D;
-        orc_quantize_block(x, (long)c->H * c->D, c->bs, c->D, c->mode, c->rel, codes, mins, scales);
+        if (c->ranges)
+            orc_quantize_block_ranges(x, (long)c->H * c->D, c->bs, c->D, c->rel,
+                                      c->ranges + (long)head * c->D,
+                                      c->ranges + ((long)c->H + head) * c->D, codes, mins, scales);
+        else
+            orc_quantize_block(x, (long)c->H * c->D, c->bs, c->D, c->mode, c->rel, codes, mins,
+                               scales);
         long len = 0;
         uint8_t *dst = c->tmp + b * c->max_block;
         int s = orc_encode_block(codes, c->bs, c->D, mins, scales, c->n_units,
@@ -421,15 +459,16 @@ static void compress_range(long lo, long hi, int tid, void *p)
  * block_index = (chunk_base + chunk) * H_total + head_base + h. */
 int orc_compress_tokens_shard(const float *tokens, int n_tok, int H, int D, int bs, int mode,
                               double rel, uint32_t chunk_base, int H_total, int head_base,
-                              const uint8_t *lengths, uint8_t *arena, long capacity, long *cursor,
-                              uint32_t *offsets_out, uint64_t *payload_bits_out, int n_threads)
+                              const float *ranges, const uint8_t *lengths, uint8_t *arena,
+                              long capacity, long *cursor, uint32_t *offsets_out,
+                              uint64_t *payload_bits_out, int n_threads)
 {
     uint32_t words[256];
     int st = orc_canonical_words(lengths, words);
     if (st) return st;
     long nb = (long)(n_tok / bs) * H;
     compress_ctx c = {tokens, H, D, bs, mode, mode == 1 ? bs : D, rel, chunk_base, H_total,
-                      head_base, lengths, words, NULL, 0, NULL, NULL, ORC_OK};
+                      head_base, ranges, lengths, words, NULL, 0, NULL, NULL, ORC_OK};
     c.max_block = block_header_bytes(bs, c.n_units) + (long)bs * D * 4 + 4;
     c.tmp = (uint8_t *)malloc((size_t)(nb ? nb : 1) * (size_t)c.max_block);
     c.sizes = (long *)calloc((size_t)(nb ? nb : 1), sizeof(long));
@@ -460,13 +499,14 @@ int orc_compress_tokens(const float *tokens, int n_tok, int H, int D, int bs, in
                         uint8_t *arena, long capacity, long *cursor, uint32_t *offsets_out,
                         uint64_t *payload_bits_out, int n_threads)
 {
-    return orc_compress_tokens_shard(tokens, n_tok, H, D, bs, mode, rel, chunk_base, H, 0,
+    return orc_compress_tokens_shard(tokens, n_tok, H, D, bs, mode, rel, chunk_base, H, 0, NULL,
                                      lengths, arena, capacity, cursor, offsets_out,
                                      payload_bits_out, n_threads);
 }
 
 typedef struct {
     const float *tokens; int H, D, bs, mode, n_units; double rel; uint64_t (*local)[256];
+    const float *ranges;
 } hist_ctx;
 
 static void hist_range(long lo, long hi, int tid, void *p)
@@ -478,20 +518,35 @@ static void hist_range(long lo, long hi, int tid, void *p)
     for (long b = lo; b < hi; ++b) {
         int chunk = (int)(b / c->H), head = (int)(b % c->H);
         const float *x = c->tokens + ((long)chunk * c->bs * c->H + head) * c->D;
-        orc_quantize_block(x, (long)c->H * c->D, c->bs, c->D, c->mode, c->rel, codes, mins, scales);
+        if (c->ranges)
+            orc_quantize_block_ranges(x, (long)c->H * c->D, c->bs, c->D, c->rel,
+                                      c->ranges + (long)head * c->D,
+                                      c->ranges + ((long)c->H + head) * c->D, codes, mins, scales);
+        else
+            orc_quantize_block(x, (long)c->H * c->D, c->bs, c->D, c->mode, c->rel, codes, mins,
+                               scales);
         orc_histogram(codes, (long)c->bs * c->D, c->local[tid]);
     }
     free(codes); free(mins); free(scales);
 }
 
 /* Prefill histogram over the full blocks of a [n_full, H, D] tensor (kvcache.py:116-121). */
+int orc_tokens_histogram_r(const float *tokens, int n_tok, int H, int D, int bs, int mode,
+                           double rel, const float *ranges, uint64_t *hist, int n_threads);
+
 int orc_tokens_histogram(const float *tokens, int n_tok, int H, int D, int bs, int mode,
                          double rel, uint64_t *hist, int n_threads)
+{
+    return orc_tokens_histogram_r(tokens, n_tok, H, D, bs, mode, rel, NULL, hist, n_threads);
+}
+
+int orc_tokens_histogram_r(const float *tokens, int n_tok, int H, int D, int bs, int mode,
+                           double rel, const float *ranges, uint64_t *hist, int n_threads)
 {
     if (n_threads < 1) n_threads = 1;
     if (n_threads > 256) n_threads = 256;
     long nb = (long)(n_tok / bs) * H;
-    hist_ctx c = {tokens, H, D, bs, mode, mode == 1 ? bs : D, rel, NULL};
+    hist_ctx c = {tokens, H, D, bs, mode, mode == 1 ? bs : D, rel, NULL, ranges};
     c.local = (uint64_t (*)[256])calloc((size_t)n_threads, sizeof(uint64_t[256]));
     parallel_for(nb, n_threads, hist_range, &c);
     memset(hist, 0, 256 * sizeof(uint64_t));

@@ -13,6 +13,7 @@ from .codebook import (HuffmanCodebook, build_codebook, build_histogram, build_s
                        codebook_from_lengths, deserialize_codebook, histogram_entropy,
                        serialize_codebook, smooth_histogram)
 from .codec import DataMovement, DeviceArena
+from .container import load_state, read_header, save_state
 from .errors import (ArenaFullError, CodebookError, CodecError, ConfigError,
                      ContainerFormatError, KvpackError, TensorFormatError)
 from .kvcache import LayerCacheState

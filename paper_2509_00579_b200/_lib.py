@@ -84,10 +84,10 @@ SIGNATURES = {
     "kvc_quantize": (I, [P, I, L, I, I, I, I, I, D_, P, P, P, P]),
     "kvc_encode_append": (I, [P, P, I, I, I, I, U32, I, I, I, I, P, P, U64, P, P, P, P]),
     "kvc_encode_workspace_bytes": (SZ, [I, I]),
-    "kvc_store_append": (I, [P, P, I, L, I, I, I, I, I, I, D_, D_, U32, P, I, P, I, P, U64, P, P,
-                             P, U64, P, P, P, SZ, P]),
+    "kvc_store_append": (I, [P, P, I, L, I, I, I, I, I, I, I, D_, D_, P, U32, P, I, P, I, P, U64,
+                             P, P, P, U64, P, P, P, SZ, P]),
     "kvc_store_workspace_bytes": (SZ, [I, I, I, I]),
-    "kvc_store_hist": (I, [P, P, I, L, I, I, I, I, D_, D_, P, P]),
+    "kvc_store_hist": (I, [P, P, I, L, I, I, I, I, I, D_, D_, P, P, P]),
     "kvc_store_supported": (I, [I, I, I]),
     "kvc_k_scores": (I, [P, I, I, I, I, P, P, L, P, P]),
     "kvc_softmax_rows": (I, [P, I, L, L, P]),

@@ -85,6 +85,24 @@ class DeviceArena:
             new[:cur] = self._buf[:cur]
             self._buf = new
 
+    def load(self, data: bytes, offsets: np.ndarray, counters: bytes, headroom: int = 1 << 16):
+        """Replace the contents with serialised blocks (container restore)."""
+        n = len(data)
+        cap = n + headroom if self.capacity is None else self.capacity
+        if self.capacity is not None and n > self.capacity:
+            raise ArenaFullError("restored arena exceeds capacity")
+        buf = torch.zeros(cap + TMA_SLACK, dtype=torch.uint8)
+        buf[:n] = torch.frombuffer(bytearray(data), dtype=torch.uint8) if n else buf[:0]
+        self._buf = buf.to(self.device)
+        nb = len(offsets)
+        offs = torch.zeros(max(nb, 1), dtype=torch.int32)
+        if nb:
+            offs[:nb] = torch.from_numpy(np.asarray(offsets, np.uint32).view(np.int32).copy())
+        self._offsets = offs.to(self.device)
+        self._counters = torch.frombuffer(bytearray(counters), dtype=torch.uint8).to(self.device)
+        self.n_blocks = nb
+        self._bound = n
+
     def note_append(self, n_blocks: int, worst_bytes: int) -> None:
         self.n_blocks += n_blocks
         self._bound += worst_bytes

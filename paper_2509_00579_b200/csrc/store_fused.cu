@@ -42,6 +42,7 @@ struct StoreTensor {
     unsigned long long *acc;    // [0] ticket, [1] done, [2] payload bits, [3] payload bytes, [4] max extent
     unsigned long long *hist;   // 256 bins (histogram pass)
     int max_code;               // ceil(1/rel): codes lie in [0, max_code]
+    const float *ranges;        // K_CHANNEL: [2][H_local][D] whole-context (min, max)
 };
 
 struct StoreParams {
@@ -76,6 +77,28 @@ __device__ __forceinline__ uint8_t code_fast(float x, float lo, float scale, flo
         if (fabsf(f - 0.5f) > (1.0f / 4096.0f)) return (uint8_t)(int)(c + (f >= 0.5f ? 1.f : 0.f));
     }
     return code_f64(x, lo, scale);
+}
+
+// K_CHANNEL: fixed whole-context ranges, so t may fall outside [0, max_code];
+// round half up then clip (quantizer.py:137-140).
+__device__ __forceinline__ uint8_t code_clamped(float x, float lo, float scale, float r32,
+                                                int clamp_max) {
+    if (!(scale > 0.f)) return 0;
+    const float t = __fmul_rn(__fsub_rn(x, lo), r32);
+    float code;
+    if (fabsf(t) < 300.f && fabsf(t - floorf(t) - 0.5f) > (1.0f / 4096.0f)) {
+        const float c = floorf(t);
+        code = c + ((t - c) >= 0.5f ? 1.f : 0.f);
+    } else {
+        const double s64 = (double)scale;
+        const double d = __dsub_rn((double)x, (double)lo);
+        double tt = __ddiv_rn(d, s64);
+        double f = floor(tt);
+        if (__dsub_rn(tt, f) >= 0.5) f += 1.0;
+        code = (float)fmin(fmax(f, -1.0), 1024.0);
+    }
+    code = fminf(fmaxf(code, 0.f), (float)clamp_max);
+    return (uint8_t)(int)code;
 }
 
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
@@ -160,7 +183,17 @@ store_kernel(StoreParams P, int stage_words) {
     __syncthreads();
 
     // ---- per-unit (min, scale): K per channel column, V per token row ----
-    if (!is_v) {
+    const bool is_kc = S.mode == KVC_K_CHANNEL;
+    if (is_kc) {
+        for (int c = tid; c < D; c += kThreads) {
+            const float lo = S.ranges[(long)hl * D + c];
+            const float hi = S.ranges[((long)P.H_local + hl) * D + c];
+            const float sc = (float)__dmul_rn(S.rel, __dsub_rn((double)hi, (double)lo));
+            u_lo[c] = lo;
+            u_sc[c] = sc;
+            u_r[c] = sc > 0.f ? __frcp_rn(sc) : 0.f;
+        }
+    } else if (!is_v) {
         for (int c = tid; c < D; c += kThreads) {
             float lo = kvc_load(&stage[c]), hi = lo;
             for (int r = 1; r < bs; ++r) {
@@ -220,7 +253,8 @@ store_kernel(StoreParams P, int stage_words) {
             if (ok) {
                 const int u = is_v ? r : c;
                 const int i = r * D + c;
-                code = code_fast(kvc_load(&stage[i]), u_lo[u], u_sc[u], u_r[u]);
+                code = is_kc ? code_clamped(kvc_load(&stage[i]), u_lo[u], u_sc[u], u_r[u], S.max_code)
+                             : code_fast(kvc_load(&stage[i]), u_lo[u], u_sc[u], u_r[u]);
                 if (ENCODE) codes[i] = (uint8_t)code;
             }
             if (!ENCODE) count(ok, code);
@@ -229,7 +263,9 @@ store_kernel(StoreParams P, int stage_words) {
         for (int i = tid; i < nv; i += kThreads) {
             const int r = i / D, c = i - r * D;
             const int u = is_v ? r : c;
-            const uint32_t code = code_fast(kvc_load(&stage[i]), u_lo[u], u_sc[u], u_r[u]);
+            const uint32_t code =
+                is_kc ? code_clamped(kvc_load(&stage[i]), u_lo[u], u_sc[u], u_r[u], S.max_code)
+                      : code_fast(kvc_load(&stage[i]), u_lo[u], u_sc[u], u_r[u]);
             if (ENCODE) codes[i] = (uint8_t)code;
             else count(true, code);
         }
@@ -467,13 +503,18 @@ static int launch_store(const StoreParams &P, int x_dtype, bool encode, int max_
 // Pass A of prefill: quantise K and V, accumulate their 256-bin histograms
 // (hist_dev: 512 x u64, K then V; codebook.py:75-80 over all heads).
 extern "C" int kvc_store_hist(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
-                              int n_chunks, int H, int D, int bs, double rel_k, double rel_v,
-                              uint64_t *hist_dev, void *stream) {
+                              int n_chunks, int H, int D, int bs, int k_mode, double rel_k,
+                              double rel_v, const float *k_ranges_dev, uint64_t *hist_dev,
+                              void *stream) {
+    if (k_mode != KVC_K_BLOCK && k_mode != KVC_K_CHANNEL) return kvc_fail(KVC_ERR_CONFIG, "bad K mode");
+    if (k_mode == KVC_K_CHANNEL && !k_ranges_dev)
+        return kvc_fail(KVC_ERR_CONFIG, "K_CHANNEL quantization requires whole-context channel_ranges");
     if (n_chunks == 0) return KVC_OK;
     if (!kvc_store_supported(bs, D, 1)) return kvc_fail(KVC_ERR_CONFIG, "shape not supported");
     StoreParams P{};
     P.t[0].x = k_dev;
-    P.t[0].mode = KVC_K_BLOCK;
+    P.t[0].mode = k_mode;
+    P.t[0].ranges = k_ranges_dev;
     P.t[0].rel = rel_k;
     P.t[0].hist = reinterpret_cast<unsigned long long *>(hist_dev);
     P.t[0].max_code = (int)ceil(1.0 / rel_k);
@@ -495,7 +536,8 @@ extern "C" int kvc_store_hist(const void *k_dev, const void *v_dev, int x_dtype,
 // (kvcache.py:217-239) in one launch.
 extern "C" int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
                                 int n_chunks, int H_local, int H_total, int head_base, int D,
-                                int bs, double rel_k, double rel_v, uint32_t chunk_base,
+                                int bs, int k_mode, double rel_k, double rel_v,
+                                const float *k_ranges_dev, uint32_t chunk_base,
                                 const kvc_codebook_dev *k_cb_dev, int k_max_len,
                                 const kvc_codebook_dev *v_cb_dev, int v_max_len,
                                 uint8_t *k_arena_dev, uint64_t k_capacity, uint32_t *k_offsets_dev,
@@ -504,6 +546,9 @@ extern "C" int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtyp
                                 kvc_arena_counters *v_counters_dev, void *workspace_dev,
                                 size_t workspace_bytes, void *stream) {
     if (n_chunks == 0) return KVC_OK;
+    if (k_mode != KVC_K_BLOCK && k_mode != KVC_K_CHANNEL) return kvc_fail(KVC_ERR_CONFIG, "bad K mode");
+    if (k_mode == KVC_K_CHANNEL && !k_ranges_dev)
+        return kvc_fail(KVC_ERR_CONFIG, "K_CHANNEL quantization requires whole-context channel_ranges");
     const int max_len = k_max_len > v_max_len ? k_max_len : v_max_len;
     if (!kvc_store_supported(bs, D, max_len)) return kvc_fail(KVC_ERR_CONFIG, "shape not supported");
     if (workspace_bytes < kvc_store_workspace_bytes(n_chunks, H_local, D, bs))
@@ -517,8 +562,10 @@ extern "C" int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtyp
     for (int t = 0; t < 2; ++t) {
         StoreTensor &T = P.t[t];
         T.x = t ? v_dev : k_dev;
-        T.mode = t ? KVC_V_TOKEN : KVC_K_BLOCK;
+        T.mode = t ? KVC_V_TOKEN : k_mode;
         T.rel = t ? rel_v : rel_k;
+        T.max_code = (int)ceil(1.0 / T.rel);
+        T.ranges = t ? nullptr : k_ranges_dev;
         T.cb = t ? v_cb_dev : k_cb_dev;
         T.arena = t ? v_arena_dev : k_arena_dev;
         T.capacity = t ? v_capacity : k_capacity;

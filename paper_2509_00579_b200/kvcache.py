@@ -45,8 +45,8 @@ class LayerCacheState:
             raise ConfigError("K and V must share block_size and buffer_size")
         if head_dim * 32 > MAX_SLICE_BITS:
             raise ConfigError("head_dim too large for 16-bit slice counters")
-        if cfg_k.mode is QuantMode.K_CHANNEL:
-            raise ConfigError("K_CHANNEL mode is not implemented on the device yet")
+        if cfg_k.mode is QuantMode.K_CHANNEL and k_channel_ranges is None:
+            raise ConfigError("K_CHANNEL mode requires whole-context channel ranges")
         self.head_num = head_num
         self.head_dim = head_dim
         self.cfg_k = cfg_k
@@ -54,9 +54,17 @@ class LayerCacheState:
         self.k_codebook = k_codebook
         self.v_codebook = v_codebook
         self.dtype = np.dtype(dtype)
-        self.k_channel_ranges = k_channel_ranges
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
+        # K_CHANNEL whole-context ranges: f32 [2, H, D] on the device (kvcache.py:104-108)
+        self._k_ranges = None
+        self.k_channel_ranges = None
+        if k_channel_ranges is not None:
+            mins, maxs = k_channel_ranges
+            t = torch.stack([torch.as_tensor(np.asarray(m, np.float32)) if not isinstance(
+                m, torch.Tensor) else m.to(torch.float32).cpu() for m in (mins, maxs)])
+            self._k_ranges = t.to(self.device).contiguous()
+            self.k_channel_ranges = (t[0].numpy(), t[1].numpy())
         self.head_base = head_base
         self.head_total = head_total if head_total is not None else head_num
         self.k_arena = DeviceArena(self.device, capacity)
@@ -102,8 +110,14 @@ class LayerCacheState:
         bs = cfg_k.block_size
         n_chunks = ctx // bs
         n_full = n_chunks * bs
-        if cfg_k.mode is QuantMode.K_CHANNEL:
-            raise ConfigError("K_CHANNEL mode is not implemented on the device yet")
+        k_is_ch = cfg_k.mode is QuantMode.K_CHANNEL
+        if k_is_ch and k_channel_ranges is None:
+            kf = kt.to(torch.float32)
+            k_channel_ranges = (kf.amin(dim=0), kf.amax(dim=0))
+        ranges_dev = None
+        if k_is_ch:
+            ranges_dev = torch.stack([torch.as_tensor(r, dtype=torch.float32).to(kt.device)
+                                      for r in k_channel_ranges]).contiguous()
         if kt.dtype != vt.dtype:
             kt, vt = kt.to(torch.float32), vt.to(torch.float32)
         lib = _lib.lib()
@@ -115,10 +129,14 @@ class LayerCacheState:
         if n_full and codebooks is None and fused:
             # pass A: quantise + histogram only (store_fused.cu)
             _lib.check(lib.kvc_store_hist(kt.data_ptr(), vt.data_ptr(), dtype_code(kt), H * D,
-                                          n_chunks, H, D, bs, cfg_k.rel_quant_scale,
-                                          cfg_v.rel_quant_scale, hist.data_ptr(), stream),
+                                          n_chunks, H, D, bs, cfg_k.mode.abi,
+                                          cfg_k.rel_quant_scale, cfg_v.rel_quant_scale,
+                                          ranges_dev.data_ptr() if ranges_dev is not None
+                                          else None, hist.data_ptr(), stream),
                        "kvc_store_hist")
         elif n_full and not fused:
+            if k_is_ch:
+                raise ConfigError("K_CHANNEL needs the single-pass store kernels (shape too big)")
             kcodes, kmetas = quantize_tokens(kt, n_chunks, H, D, bs, cfg_k.mode,
                                              cfg_k.rel_quant_scale,
                                              hist[:256] if codebooks is None else None)
@@ -134,7 +152,8 @@ class LayerCacheState:
         else:
             k_cb, v_cb = codebooks
         st = cls(H, D, cfg_k, cfg_v, k_cb, v_cb, dtype=src_dtype, device=kt.device,
-                 head_base=head_base, head_total=head_total, capacity=capacity)
+                 head_base=head_base, head_total=head_total, capacity=capacity,
+                 k_channel_ranges=k_channel_ranges)
         if n_full:
             if st._fused_store:
                 st._store(kt, vt, n_chunks)
@@ -195,8 +214,10 @@ class LayerCacheState:
         ws = self._workspace(lib.kvc_store_workspace_bytes(n_chunks, H, D, bs))
         st = lib.kvc_store_append(
             k_src.data_ptr(), v_src.data_ptr(), dtype_code(k_src), H * D, n_chunks, H,
-            self.head_total, self.head_base, D, bs, self.cfg_k.rel_quant_scale,
-            self.cfg_v.rel_quant_scale, self.compressed_tokens // bs, self._k_tab.data_ptr(),
+            self.head_total, self.head_base, D, bs, self.cfg_k.mode.abi,
+            self.cfg_k.rel_quant_scale, self.cfg_v.rel_quant_scale,
+            self._k_ranges.data_ptr() if self._k_ranges is not None else None,
+            self.compressed_tokens // bs, self._k_tab.data_ptr(),
             self.k_codebook.max_code_length, self._v_tab.data_ptr(),
             self.v_codebook.max_code_length, self.k_arena.buf_ptr, self.k_arena.alloc_capacity,
             self.k_arena.offsets_ptr, self.k_arena.counters_ptr, self.v_arena.buf_ptr,

@@ -78,7 +78,7 @@ def _state_record(prefix, st):
     return rec
 
 
-def _prefill_hist(k_work, v_work, cfg_k, cfg_v, H):
+def _prefill_hist(k_work, v_work, cfg_k, cfg_v, H, ranges=None):
     """Raw (unsmoothed) prefill histograms, via the reference's own functions."""
     n_full = (k_work.shape[0] // cfg_k.block_size) * cfg_k.block_size
     hk = np.zeros(256, dtype=np.uint64)
@@ -87,7 +87,7 @@ def _prefill_hist(k_work, v_work, cfg_k, cfg_v, H):
     if n_full:
         from kvpack.kvcache import _quantize_tokens
 
-        kq = _quantize_tokens(k_work[:n_full], cfg_k, 0, H, None)
+        kq = _quantize_tokens(k_work[:n_full], cfg_k, 0, H, ranges)
         vq = _quantize_tokens(v_work[:n_full], cfg_v, 0, H, None)
         hk += kv.build_histogram(np.concatenate([b.codes.ravel() for b in kq]))
         hv += kv.build_histogram(np.concatenate([b.codes.ravel() for b in vq]))
@@ -95,8 +95,9 @@ def _prefill_hist(k_work, v_work, cfg_k, cfg_v, H):
 
 
 def make_case(name, *, ctx, H, D, bs, buffer=None, rel_k=0.05, rel_v=0.15, dtype=np.float16,
-              seed=0, appended=0, inject=None, constant=None, synthetic=True, n_q=2):
-    cfg_k = kv.QuantConfig(kv.QuantMode.K_BLOCK, block_size=bs, rel_quant_scale=rel_k,
+              seed=0, appended=0, inject=None, constant=None, synthetic=True, n_q=2,
+              k_mode="kblock"):
+    cfg_k = kv.QuantConfig(kv.QuantMode(k_mode), block_size=bs, rel_quant_scale=rel_k,
                            buffer_size=buffer)
     cfg_v = kv.QuantConfig(kv.QuantMode.V_TOKEN, block_size=bs, rel_quant_scale=rel_v,
                            buffer_size=buffer)
@@ -120,7 +121,8 @@ def make_case(name, *, ctx, H, D, bs, buffer=None, rel_k=0.05, rel_v=0.15, dtype
             bytes(np.asarray(x, dtype=np.uint8).tobytes())) for x in inject)
     rec = {
         "cfg": np.array([ctx, H, D, bs, cfg_k.buffer_size, appended], dtype=np.int64),
-        "rel": np.array([rel_k, rel_v], dtype=np.float64),
+        "rel": np.array([cfg_k.rel_quant_scale, rel_v], dtype=np.float64),
+        "k_mode": np.array(k_mode),
         "k_in": k_in, "v_in": v_in,
         "k_app": kfull[ctx:].astype(np.float32), "v_app": vfull[ctx:].astype(np.float32),
     }
@@ -128,7 +130,12 @@ def make_case(name, *, ctx, H, D, bs, buffer=None, rel_k=0.05, rel_v=0.15, dtype
         rec["inject_k"] = np.asarray(inject[0], dtype=np.uint8)
         rec["inject_v"] = np.asarray(inject[1], dtype=np.uint8)
     k_ct, v_ct = kv.CacheTensor(k_in), kv.CacheTensor(v_in)
-    hk, hv, kq, vq = _prefill_hist(k_ct.as_float32(), v_ct.as_float32(), cfg_k, cfg_v, H)
+    ranges = None
+    if k_mode == "kchannel":
+        kw = k_ct.as_float32()
+        ranges = (kw.min(axis=0).astype(np.float32), kw.max(axis=0).astype(np.float32))
+        rec["k_ranges"] = np.stack(ranges)
+    hk, hv, kq, vq = _prefill_hist(k_ct.as_float32(), v_ct.as_float32(), cfg_k, cfg_v, H, ranges)
     rec["k_hist"] = hk
     rec["v_hist"] = hv
     if kq:
@@ -161,6 +168,9 @@ def make_case(name, *, ctx, H, D, bs, buffer=None, rel_k=0.05, rel_v=0.15, dtype
     kd, vd = st.fetch_dequantized()
     rec["deq_k"] = kd.values
     rec["deq_v"] = vd.values
+    tmpf = os.path.join(tempfile.mkdtemp(), "s.kvcz")
+    kv.save_state(st, tmpf)
+    rec["kvcz"] = np.frombuffer(open(tmpf, "rb").read(), np.uint8).copy()
     path = os.path.join(HERE, f"{name}.npz")
     np.savez_compressed(path, **rec)
     print(f"{name}: ctx={ctx}+{appended} H={H} D={D} bs={bs} k_maxlen={int(st.k_codebook.max_code_length)} "
@@ -325,6 +335,10 @@ def main():
               appended=12, inject=(np.eye(256, dtype=np.uint8)[0], np.eye(256, dtype=np.uint8)[0]))
     make_case("c_prefill_short", ctx=5, H=2, D=16, bs=8, dtype=np.float32, synthetic=False,
               seed=10, appended=20)
+    make_case("c_kchannel", ctx=64 * 3 + 11, H=2, D=64, bs=64, seed=12, appended=90,
+              rel_k=None, k_mode="kchannel")
+    make_case("c_kchannel_f32_bs8", ctx=8 * 3 + 2, H=2, D=4, bs=8, buffer=16, dtype=np.float32,
+              synthetic=False, seed=30, appended=20, rel_k=0.05, k_mode="kchannel")
     if args.big or args.cfg2:
         big_digests(args.cfg2)
 

@@ -56,7 +56,10 @@ def _replay(g, n_threads=1):
     ctx, H, D, bs, buffer, appended, rel_k, rel_v = unpack_cfg(g)
     cbs = (g["inject_k"], g["inject_v"]) if "inject_k" in g else None
     st = oracle.OracleState.prefill(g["k_in"], g["v_in"], bs=bs, buffer=buffer, rel_k=rel_k,
-                                    rel_v=rel_v, codebooks=cbs, n_threads=n_threads)
+                                    rel_v=rel_v, codebooks=cbs, n_threads=n_threads,
+                                    k_mode=str(g.get("k_mode", "kblock")))
+    if "k_ranges" in g:
+        assert np.array_equal(st.k_ranges, g["k_ranges"])
     return st
 
 
@@ -78,7 +81,7 @@ def _check_state(st, g, prefix):
 def test_golden_store(case, n_threads):
     g = load(case)
     ctx, H, D, bs, buffer, appended, rel_k, rel_v = unpack_cfg(g)
-    if "k_codes" in g:
+    if "k_codes" in g and str(g.get("k_mode", "kblock")) == "kblock":
         for b in range(g["k_codes"].shape[0]):
             chunk, head = divmod(b, H)
             xk = g["k_in"][chunk * bs:(chunk + 1) * bs, head].astype(np.float32)

@@ -48,8 +48,8 @@ def main(ctx=32768, H=40, D=128, reps=10):
     a, b = ev(), ev()
     a.record(s)
     for _ in range(reps):
-        lib.kvc_store_hist(k.data_ptr(), v.data_ptr(), 0, H * D, nb_chunks, H, D, 64, 0.05, 0.15,
-                           hist.data_ptr(), s.cuda_stream)
+        lib.kvc_store_hist(k.data_ptr(), v.data_ptr(), 0, H * D, nb_chunks, H, D, 64, 0, 0.05, 0.15,
+                           None, hist.data_ptr(), s.cuda_stream)
     b.record(s)
     torch.cuda.synchronize()
     t_a = a.elapsed_time(b) / reps * 1e-3
