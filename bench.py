@@ -45,6 +45,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fused decomp+attn GB/s & compress GB/s vs HBM roofline; compression ratio"
+PRESETS = {
+    2: dict(layers=40, batch=8, ctx=32768, heads=40, group=1,
+            workload="cfg2: Llama-2-13B KV, fused fetch-attention decode step"),
+    3: dict(layers=32, batch=4, ctx=131072, heads=8, group=4,
+            workload="cfg3: Llama-3-8B GQA KV (8 KV heads x group 4), fused fetch decode step"),
+    5: dict(layers=32, batch=64, ctx=8192, heads=32, group=1,
+            workload="cfg5: Llama-2-7B KV batch 64, fused fetch decode step + quant sweep"),
+}
+SWEEP = [(1 / 255, 1 / 255), (0.01, 0.02), (0.02, 0.05), (0.05, 0.15), (0.06, 0.2),
+         (0.1, 0.25), (0.25, 0.5), (0.5, 1.0)]
 
 
 def _peaks():
@@ -209,14 +219,20 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--layers", type=int, default=40)
-    ap.add_argument("--batch", type=int, default=8)
-    ap.add_argument("--ctx", type=int, default=32768)
-    ap.add_argument("--heads", type=int, default=40)
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5],
+                    help="BASELINE config: 2 (default headline), 3 (GQA), 5 (batch-64 + sweep)")
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--ctx", type=int, default=None)
+    ap.add_argument("--heads", type=int, default=None)
+    ap.add_argument("--group", type=int, default=None)
     ap.add_argument("--cpu-ctx", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    for k, v in PRESETS[args.config].items():
+        if getattr(args, k, None) is None:
+            setattr(args, k, v)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -238,7 +254,7 @@ def main():
         raise SystemExit("heads must divide across ranks")
     hl = args.heads // world
     hb = rank * hl
-    L, B, T, H = args.layers, args.batch, args.ctx, args.heads
+    L, B, T, H, G = args.layers, args.batch, args.ctx, args.heads, args.group
 
     states, store_times, store_bytes = build_cache(kv, torch, L, B, T, H, hb, hl, device,
                                                    group=dist.group.WORLD if world > 1 else None)
@@ -250,18 +266,25 @@ def main():
     comp_bytes_step = sum(comp_bytes_layer) + L * B * hl * 128 * 8   # + q + out
     ratio = float(np.mean([kv.collect_stats(s).compression_ratio for s in states[0]]))
 
-    q = torch.randn((L, B, hl, 128), device=device, dtype=torch.float32)
-    outs = torch.empty((L, B, hl, 128), device=device, dtype=torch.float32)
+    q = torch.randn((L, B, hl * G, 128), device=device, dtype=torch.float32)
+    outs = torch.empty((L, B, hl * G, 128), device=device, dtype=torch.float32)
     caches = [kv.attention._BatchDesc() for _ in range(L)]
     wss = [None] * L
     need = _lib_ws(kv, B, hl, max(s.n_chunks for s in states[0]))
     ws = torch.empty(need, dtype=torch.uint8, device=device)
-    gathered = torch.empty((world, L, B, hl, 128), device=device) if world > 1 else None
+    gathered = torch.empty((world, L, B, hl * G, 128), device=device) if world > 1 else None
+
+    def layer_call(layer):
+        if G == 1:
+            kv.attention_batched(states[layer], q[layer], desc_cache=caches[layer], workspace=ws,
+                                 out=outs[layer])
+        else:
+            outs[layer] = kv.attention_gqa(states[layer], q[layer], G, desc_cache=caches[layer],
+                                           workspace=ws)
 
     def step():
         for layer in range(L):
-            kv.attention_batched(states[layer], q[layer], desc_cache=caches[layer], workspace=ws,
-                                 out=outs[layer])
+            layer_call(layer)
         if world > 1:
             dist.all_gather_into_tensor(gathered, outs)
 
@@ -290,8 +313,7 @@ def main():
     for layer in range(min(L, 8)):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        kv.attention_batched(states[layer], q[layer], desc_cache=caches[layer], workspace=ws,
-                             out=outs[layer])
+        layer_call(layer)
         b.record(stream)
         torch.cuda.synchronize()
         lay_ms.append(a.elapsed_time(b))
@@ -300,9 +322,9 @@ def main():
     ach = comp_bytes_layer[0] / (lay_ms * 1e-3) / 1e9
 
     # e2e through the public API with host buffers
-    qh = torch.empty((L, B, hl, 128), dtype=torch.float32).pin_memory()
+    qh = torch.empty((L, B, hl * G, 128), dtype=torch.float32).pin_memory()
     qh.copy_(q.cpu())
-    oh = torch.empty((L, B, hl, 128), dtype=torch.float32).pin_memory()
+    oh = torch.empty((L, B, hl * G, 128), dtype=torch.float32).pin_memory()
 
     def e2e_step():
         q.copy_(qh, non_blocking=True)
@@ -327,14 +349,13 @@ def main():
     dk = torch.randn((B, hl, T, 128), device=device, dtype=torch.float16)
     dv = torch.randn_like(dk)
     dq = q[0].contiguous()
-    dout = torch.empty((B, hl, 128), device=device)
-    dws = None
+    dout = torch.empty((B, hl * G, 128), device=device)
     for _ in range(3):
-        kv.dense_attention_f16(dk, dv, dq, out=dout)
+        kv.dense_attention_f16(dk, dv, dq, out=dout, group=G)
     torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(10):
-        kv.dense_attention_f16(dk, dv, dq, out=dout)
+        kv.dense_attention_f16(dk, dv, dq, out=dout, group=G)
     e1.record(stream)
     torch.cuda.synchronize()
     dense_ms = e0.elapsed_time(e1) / 10
@@ -365,8 +386,9 @@ def main():
             "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u8 Huffman codes -> f32 accumulate",
             "data": "synthetic (reference generator distribution, device RNG), random q",
-            "config": {"workload": "cfg2: Llama-2-13B KV, fused fetch-attention decode step",
-                       "layers": L, "batch": B, "ctx": T, "kv_heads": H, "head_dim": 128,
+            "config": {"workload": PRESETS[args.config]["workload"],
+                       "layers": L, "batch": B, "ctx": T, "kv_heads": H, "group": G,
+                       "head_dim": 128,
                        "block_size": 64, "rel_k": 0.05, "rel_v": 0.15,
                        "parallelism": f"kv-head shard x{world}",
                        "l2": "inputs (compressed cache) >> L2; no flush needed"},
@@ -391,16 +413,56 @@ def main():
                          "kernel": "fused_attn_kernel (+combine), one layer launch, "
                                    "compressed bytes"},
             "e2e": {"value": round(e2e_val, 2), "unit": "GB/s (equivalent fp16 KV)",
-                    "h2d_bytes_per_step": int(L * B * hl * 128 * 4),
-                    "d2h_bytes_per_step": int(L * B * hl * 128 * 4)},
-            "gpu_launches": int(args.steps * L * 2),
+                    "h2d_bytes_per_step": int(L * B * hl * G * 128 * 4),
+                    "d2h_bytes_per_step": int(L * B * hl * G * 128 * 4)},
+            "gpu_launches": int(args.steps * L * 2 * G),
             "clocks": clk.summary(),
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        if args.config == 5:
+            line["quant_sweep"] = quant_sweep(kv, torch, device, T, H, B)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def quant_sweep(kv, torch, device, T, H, B):
+    """Config 5 sweep: compression ratio (reference formula) and fused fetch
+    throughput (batch B, one layer) per (relK, relV) setting."""
+    rows = []
+    for rk, rv in SWEEP:
+        ck = kv.QuantConfig(kv.QuantMode.K_BLOCK, rel_quant_scale=rk)
+        cv = kv.QuantConfig(kv.QuantMode.V_TOKEN, rel_quant_scale=rv)
+        states = []
+        for b in range(B):
+            k = kv.generate_synthetic_device(kv.SyntheticSpec(T, H, 128, seed=b), device)
+            v = kv.generate_synthetic_device(kv.SyntheticSpec(T, H, 128, seed=b ^ 0x9E3779B9),
+                                             device)
+            st = kv.LayerCacheState.prefill(k, v, ck, cv, check=False)
+            st.compact()
+            states.append(st)
+        stats = kv.collect_stats(states[0])
+        q = torch.randn((B, H, 128), device=device)
+        cache = kv.attention._BatchDesc()
+        for _ in range(2):
+            kv.attention_batched(states, q, desc_cache=cache)
+        torch.cuda.synchronize()
+        a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            kv.attention_batched(states, q, desc_cache=cache)
+        b2.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b2) / 5
+        rows.append({"rel_k": round(rk, 6), "rel_v": round(rv, 6),
+                     "ratio": round(stats.compression_ratio, 4),
+                     "k_max_len": int(states[0].k_codebook.max_code_length),
+                     "v_max_len": int(states[0].v_codebook.max_code_length),
+                     "fetch_eq_gbs": round(2 * B * T * H * 128 * 2 / (ms * 1e-3) / 1e9, 1),
+                     "fetch_ms": round(ms, 4)})
+        del states
+    return rows
 
 
 def _ncu_traffic():

@@ -6,7 +6,8 @@ hand-written sm_100a kernels in ``libkvcomp.so`` (C ABI: include/kvcomp.h).
 Tensors live on the CUDA device; results are torch tensors.
 """
 
-from .attention import (AttentionOutput, attention_batched, attention_step, dense_attention_f16,
+from .attention import (AttentionOutput, attention_batched, attention_gqa, attention_step,
+                        dense_attention_f16,
                         fused_k_scores, fused_v_output, multistage_attention, reference_output,
                         reference_scores, softmax_rows)
 from .codebook import (HuffmanCodebook, build_codebook, build_histogram, build_smoothed_codebook,

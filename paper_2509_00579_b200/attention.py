@@ -246,20 +246,41 @@ def multistage_attention(state: LayerCacheState, q,
     return AttentionOutput(out=out, scores=scores)
 
 
+def attention_gqa(states: Sequence[LayerCacheState], q: torch.Tensor, group: int,
+                  desc_cache: Optional["_BatchDesc"] = None,
+                  workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Grouped-query decode attention: q [B, H_kv*group, D], query head
+    h*group+j reads KV head h (Llama-3 layout).  The reference has no GQA
+    (SPEC non-goal); its oracle runs one attention_step per group member, and
+    so does this entry point (one fused launch per member)."""
+    B, HQ, D = q.shape
+    H = HQ // group
+    out = torch.empty((B, HQ, D), dtype=torch.float32, device=q.device)
+    qv = q.view(B, H, group, D)
+    ov = out.view(B, H, group, D)
+    cache = desc_cache if desc_cache is not None else _BatchDesc()
+    for j in range(group):
+        o, _, err = attention_batched(states, qv[:, :, j].contiguous(), desc_cache=cache,
+                                      workspace=workspace)
+        ov[:, :, j] = o
+    return out
+
+
 def dense_attention_f16(k: torch.Tensor, v: torch.Tensor, q: torch.Tensor,
                         out: Optional[torch.Tensor] = None,
-                        workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+                        workspace: Optional[torch.Tensor] = None, group: int = 1) -> torch.Tensor:
     """Uncompressed fp16 decode attention (north-star comparator kernel).
-    k, v: [S, H, ctx, D] f16 contiguous on the device; q: [S, H, D] f32."""
+    k, v: [S, H, ctx, D] f16 contiguous on the device; q: [S, H*group, D] f32
+    (GQA: K/V rows are read once for all `group` query heads)."""
     S, H, ctx, D = k.shape
     lib = _lib.lib()
-    need = lib.kvc_dense_workspace_bytes(S, H, 1, D, ctx)
+    need = lib.kvc_dense_workspace_bytes(S, H, group, D, ctx)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=k.device)
     if out is None:
-        out = torch.empty((S, H, D), dtype=torch.float32, device=k.device)
-    st = lib.kvc_dense_attention_f16(k.data_ptr(), v.data_ptr(), S, H, D, 1, ctx, q.data_ptr(),
-                                     out.data_ptr(), workspace.data_ptr(), workspace.numel(),
-                                     _stream(k.device))
+        out = torch.empty((S, H * group, D), dtype=torch.float32, device=k.device)
+    st = lib.kvc_dense_attention_f16(k.data_ptr(), v.data_ptr(), S, H, D, group, ctx,
+                                     q.data_ptr(), out.data_ptr(), workspace.data_ptr(),
+                                     workspace.numel(), _stream(k.device))
     _lib.check(st, "kvc_dense_attention_f16")
     return out

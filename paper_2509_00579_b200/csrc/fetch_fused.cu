@@ -942,6 +942,8 @@ combine_kernel(const kvc_seq_desc *__restrict__ seqs, int H, int bs, const float
 // warp per iteration; online softmax; split-K partials -> combine.
 // ---------------------------------------------------------------------------
 constexpr int kDenseNW = 4;
+// G query heads share each KV head (GQA); K/V rows are read once for all G.
+template <int G>
 __global__ void __launch_bounds__(kDenseNW * 32)
 dense_attn_kernel(const __half *__restrict__ K, const __half *__restrict__ V, int H, long ctx,
                   const float *__restrict__ q, Partial *__restrict__ partial, long tok_per_split,
@@ -951,17 +953,25 @@ dense_attn_kernel(const __half *__restrict__ K, const __half *__restrict__ V, in
     const int g = lane & 15, half = lane >> 4;
     const long base = ((long)sidx * H + h) * ctx * D;
     const __half *Kh = K + base, *Vh = V + base;
-    const float *qh = q + ((long)sidx * H + h) * D;
     const float sm_scale = kLog2e / sqrtf((float)D);
-    float qv[8];
+    float qv[G][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) qv[i] = qh[g * 8 + i] * sm_scale;
+    for (int j = 0; j < G; ++j) {
+        const float *qh = q + ((long)sidx * H * G + (long)h * G + j) * D;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) qv[j][i] = qh[g * 8 + i] * sm_scale;
+    }
     const long t_begin = (long)split * tok_per_split;
     const long t_end = min(ctx, t_begin + tok_per_split);
-    float m = -INFINITY, l = 0.f, o[8];
+    float m[G], l[G], o[G][8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] = 0.f;
-    constexpr int R = 8;  // rows per half-warp per iteration
+    for (int j = 0; j < G; ++j) {
+        m[j] = -INFINITY;
+        l[j] = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[j][i] = 0.f;
+    }
+    constexpr int R = G > 2 ? 4 : 8;  // rows per half-warp per iteration
     for (long t0 = t_begin + (long)warp * 2 * R; t0 < t_end; t0 += (long)kDenseNW * 2 * R) {
         uint4 kr[R], vr[R];
 #pragma unroll
@@ -975,73 +985,81 @@ dense_attn_kernel(const __half *__restrict__ K, const __half *__restrict__ V, in
                 vr[r] = make_uint4(0, 0, 0, 0);
             }
         }
-        float s[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const __half2 *k2 = reinterpret_cast<const __half2 *>(&kr[r]);
-            float a = 0.f;
+        for (int j = 0; j < G; ++j) {
+            float s[R];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                float2 f = __half22float2(k2[i]);
-                a = fmaf(f.x, qv[2 * i], a);
-                a = fmaf(f.y, qv[2 * i + 1], a);
+            for (int r = 0; r < R; ++r) {
+                const __half2 *k2 = reinterpret_cast<const __half2 *>(&kr[r]);
+                float a = 0.f;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    float2 f = __half22float2(k2[i]);
+                    a = fmaf(f.x, qv[j][2 * i], a);
+                    a = fmaf(f.y, qv[j][2 * i + 1], a);
+                }
+#pragma unroll
+                for (int o2 = 8; o2 > 0; o2 >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o2);
+                s[r] = (t0 + 2 * r + half < t_end) ? a : -INFINITY;
+            }
+            float bm = -INFINITY;
+#pragma unroll
+            for (int r = 0; r < R; ++r) bm = fmaxf(bm, s[r]);
+            bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
+            if (bm > m[j]) {
+                float alpha = exp2f(m[j] - bm);
+                l[j] *= alpha;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[j][i] *= alpha;
+                m[j] = bm;
             }
 #pragma unroll
-            for (int o2 = 8; o2 > 0; o2 >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o2);
-            s[r] = (t0 + 2 * r + half < t_end) ? a : -INFINITY;
-        }
-        float bm = -INFINITY;
+            for (int r = 0; r < R; ++r) {
+                float pr = exp2f(s[r] - m[j]);
+                l[j] += pr;
+                const __half2 *v2 = reinterpret_cast<const __half2 *>(&vr[r]);
 #pragma unroll
-        for (int r = 0; r < R; ++r) bm = fmaxf(bm, s[r]);
-        bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
-        if (bm > m) {
-            float alpha = exp2f(m - bm);
-            l *= alpha;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) o[i] *= alpha;
-            m = bm;
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            float p = exp2f(s[r] - m);
-            l += p;
-            const __half2 *v2 = reinterpret_cast<const __half2 *>(&vr[r]);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                float2 f = __half22float2(v2[i]);
-                o[2 * i] = fmaf(p, f.x, o[2 * i]);
-                o[2 * i + 1] = fmaf(p, f.y, o[2 * i + 1]);
+                for (int i = 0; i < 4; ++i) {
+                    float2 f = __half22float2(v2[i]);
+                    o[j][2 * i] = fmaf(pr, f.x, o[j][2 * i]);
+                    o[j][2 * i + 1] = fmaf(pr, f.y, o[j][2 * i + 1]);
+                }
             }
         }
     }
     // merge the two half-warps (same m), then warps via smem
-    l += __shfl_xor_sync(0xffffffffu, l, 16);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] += __shfl_xor_sync(0xffffffffu, o[i], 16);
     __shared__ float sh_o[kDenseNW][D], sh_m[kDenseNW], sh_l[kDenseNW];
-    if (half == 0) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) sh_o[warp][g * 8 + i] = o[i];
-    }
-    if (lane == 0) {
-        sh_m[warp] = m;
-        sh_l[warp] = l;
-    }
-    __syncthreads();
-    if (threadIdx.x < D) {
-        float M = -INFINITY;
-        for (int w = 0; w < kDenseNW; ++w) M = fmaxf(M, sh_m[w]);
-        float L = 0.f, O = 0.f;
-        for (int w = 0; w < kDenseNW; ++w) {
-            float sc = sh_m[w] == -INFINITY ? 0.f : exp2f(sh_m[w] - M);
-            L += sh_l[w] * sc;
-            O += sh_o[w][threadIdx.x] * sc;
+    for (int j = 0; j < G; ++j) {
+        float lj = l[j] + __shfl_xor_sync(0xffffffffu, l[j], 16);
+        float oj[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) oj[i] = o[j][i] + __shfl_xor_sync(0xffffffffu, o[j][i], 16);
+        __syncthreads();
+        if (half == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) sh_o[warp][g * 8 + i] = oj[i];
         }
-        Partial *dst = partial + ((long)sidx * H + h) * n_splits + split;
-        dst->o[threadIdx.x] = O;
-        if (threadIdx.x == 0) {
-            dst->m = M;
-            dst->l = L;
+        if (lane == 0) {
+            sh_m[warp] = m[j];
+            sh_l[warp] = lj;
+        }
+        __syncthreads();
+        if (threadIdx.x < D) {
+            float M = -INFINITY;
+            for (int w = 0; w < kDenseNW; ++w) M = fmaxf(M, sh_m[w]);
+            float L = 0.f, O = 0.f;
+            for (int w = 0; w < kDenseNW; ++w) {
+                float sc = sh_m[w] == -INFINITY ? 0.f : exp2f(sh_m[w] - M);
+                L += sh_l[w] * sc;
+                O += sh_o[w][threadIdx.x] * sc;
+            }
+            Partial *dst = partial + ((long)sidx * H * G + (long)h * G + j) * n_splits + split;
+            dst->o[threadIdx.x] = O;
+            if (threadIdx.x == 0) {
+                dst->m = M;
+                dst->l = L;
+            }
         }
     }
 }
@@ -1198,17 +1216,18 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
 }
 
 extern "C" size_t kvc_dense_workspace_bytes(int n_seqs, int H, int group, int D_, long ctx) {
-    (void)group;
     (void)D_;
     long splits = (ctx + 255) / 256;
-    return sizeof(Partial) * (size_t)n_seqs * H * (size_t)splits;
+    return sizeof(Partial) * (size_t)n_seqs * H * (size_t)(group > 0 ? group : 1) * (size_t)splits;
 }
 
 extern "C" int kvc_dense_attention_f16(const void *k_dev, const void *v_dev, int n_seqs, int H,
                                        int D_, int group, long ctx, const float *q_dev,
                                        float *out_dev, void *workspace_dev, size_t workspace_bytes,
                                        void *stream) {
-    if (D_ != D || group != 1) return kvc_fail(KVC_ERR_CONFIG, "dense kernel: head_dim 128, group 1");
+    if (D_ != D) return kvc_fail(KVC_ERR_CONFIG, "dense kernel: head_dim 128");
+    if (group != 1 && group != 2 && group != 4 && group != 8)
+        return kvc_fail(KVC_ERR_CONFIG, "dense kernel: group must be 1, 2, 4 or 8");
     if (ctx < 1) return kvc_fail(KVC_ERR_CONFIG, "empty context");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     long nh = (long)n_seqs * H;
@@ -1218,14 +1237,19 @@ extern "C" int kvc_dense_attention_f16(const void *k_dev, const void *v_dev, int
     if (tps < 256) tps = 256;
     tps = (tps + 63) / 64 * 64;
     splits = (ctx + tps - 1) / tps;
-    if (sizeof(Partial) * (size_t)nh * splits > workspace_bytes)
+    if (sizeof(Partial) * (size_t)nh * group * splits > workspace_bytes)
         return kvc_fail(KVC_ERR_CONFIG, "dense workspace too small");
     Partial *part = static_cast<Partial *>(workspace_dev);
-    dense_attn_kernel<<<dim3((unsigned)splits, H, n_seqs), kDenseNW * 32, 0, s>>>(
-        static_cast<const __half *>(k_dev), static_cast<const __half *>(v_dev), H, ctx, q_dev, part,
-        tps, (int)splits);
+    dim3 grid((unsigned)splits, H, n_seqs);
+    const __half *k = static_cast<const __half *>(k_dev), *v = static_cast<const __half *>(v_dev);
+    switch (group) {
+        case 1: dense_attn_kernel<1><<<grid, kDenseNW * 32, 0, s>>>(k, v, H, ctx, q_dev, part, tps, (int)splits); break;
+        case 2: dense_attn_kernel<2><<<grid, kDenseNW * 32, 0, s>>>(k, v, H, ctx, q_dev, part, tps, (int)splits); break;
+        case 4: dense_attn_kernel<4><<<grid, kDenseNW * 32, 0, s>>>(k, v, H, ctx, q_dev, part, tps, (int)splits); break;
+        default: dense_attn_kernel<8><<<grid, kDenseNW * 32, 0, s>>>(k, v, H, ctx, q_dev, part, tps, (int)splits); break;
+    }
     int st = kvc_check_launch("dense_attn_kernel");
     if (st) return st;
-    dense_combine_kernel<<<dim3(1, H, n_seqs), 128, 0, s>>>(H, part, (int)splits, out_dev);
+    dense_combine_kernel<<<dim3(1, H * group, n_seqs), 128, 0, s>>>(H * group, part, (int)splits, out_dev);
     return kvc_check_launch("dense_combine_kernel");
 }

@@ -325,3 +325,34 @@ def test_container_bytes_match_reference(kv, case, tmp_path):
     p2 = tmp_path / "again.kvcz"
     kv.save_state(back, p2)
     assert p2.read_bytes() == g["kvcz"].tobytes()
+
+
+@pytest.mark.parametrize("group", [2, 4])
+def test_dense_fp16_gqa(kv, group):
+    torch.manual_seed(1)
+    S, H, T, D = 2, 2, 3000, 128
+    k = torch.randn(S, H, T, D, device="cuda").half()
+    v = torch.randn(S, H, T, D, device="cuda").half()
+    q = torch.randn(S, H * group, D, device="cuda")
+    out = kv.dense_attention_f16(k, v, q, group=group)
+    kk = k.float().repeat_interleave(group, dim=1)
+    vv = v.float().repeat_interleave(group, dim=1)
+    s = torch.einsum("shtd,shd->sht", kk, q) / math.sqrt(D)
+    ref = torch.einsum("sht,shtd->shd", torch.softmax(s, -1), vv)
+    assert max_relative_error(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-5
+
+
+def test_fused_gqa_matches_per_member_steps(kv):
+    """Config-3 style: 2 KV heads x group 4; each query head attends its KV head."""
+    group, H = 4, 2
+    k = kv.generate_synthetic(kv.SyntheticSpec(2000, H, 128, seed=40)).values.astype(np.float16)
+    v = kv.generate_synthetic(kv.SyntheticSpec(2000, H, 128, seed=41)).values.astype(np.float16)
+    st = kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v),
+                                    kv.QuantConfig(kv.QuantMode.K_BLOCK),
+                                    kv.QuantConfig(kv.QuantMode.V_TOKEN))
+    q = np.random.default_rng(4).standard_normal((1, H * group, 128), dtype=np.float32)
+    out = kv.attention_gqa([st], torch.from_numpy(q).cuda(), group)
+    for j in range(group):
+        r = kv.attention_step(st, q[0].reshape(H, group, 128)[:, j])
+        assert max_relative_error(out[0].view(H, group, 128)[:, j].cpu().numpy(),
+                                  r.out.cpu().numpy()) <= 1e-6
