@@ -251,14 +251,33 @@ def attention_gqa(states: Sequence[LayerCacheState], q: torch.Tensor, group: int
                   workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
     """Grouped-query decode attention: q [B, H_kv*group, D], query head
     h*group+j reads KV head h (Llama-3 layout).  The reference has no GQA
-    (SPEC non-goal); its oracle runs one attention_step per group member, and
-    so does this entry point (one fused launch per member)."""
+    (SPEC non-goal; its oracle runs one attention_step per group member).
+    Groups of 2 or 4 with codes <= 6 bits run the decode-once GQA kernel
+    (each K/V block decoded once for all members); otherwise one fused
+    launch per member."""
     B, HQ, D = q.shape
     H = HQ // group
-    out = torch.empty((B, HQ, D), dtype=torch.float32, device=q.device)
+    dev = q.device
+    out = torch.empty((B, HQ, D), dtype=torch.float32, device=dev)
+    cache = desc_cache if desc_cache is not None else _BatchDesc()
+    if group in (2, 4) and _fused_supported(states) and all(
+            max(s.k_codebook.max_code_length, s.v_codebook.max_code_length) <= 6 for s in states):
+        lib = _lib.lib()
+        ddev, dhost = cache.get(states)
+        max_chunks = max(s.n_chunks for s in states)
+        need = lib.kvc_attention_workspace_bytes(B, H, group, D, max_chunks)
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        qc = q.contiguous()
+        st = lib.kvc_attention(ddev.data_ptr(), ctypes_addr(dhost), B, H, D,
+                               states[0].cfg_k.block_size, group, qc.data_ptr(), out.data_ptr(),
+                               None, 0, workspace.data_ptr(), workspace.numel(), err.data_ptr(),
+                               _stream(dev))
+        if st == _lib.KVC_OK:
+            return out
     qv = q.view(B, H, group, D)
     ov = out.view(B, H, group, D)
-    cache = desc_cache if desc_cache is not None else _BatchDesc()
     for j in range(group):
         o, _, err = attention_batched(states, qv[:, :, j].contiguous(), desc_cache=cache,
                                       workspace=workspace)

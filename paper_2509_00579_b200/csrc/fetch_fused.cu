@@ -871,18 +871,351 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
     }
 }
 
+// G consecutive f32 from shared memory in one vector load (G = 2 or 4)
+template <int G>
+__device__ __forceinline__ void lds_vec(uint32_t addr, float *v) {
+    if (G == 4) {
+        asm volatile(KVC_LD_SHARED ".v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(addr));
+    } else {
+        asm volatile(KVC_LD_SHARED ".v2.f32 {%0, %1}, [%2];" : "=f"(v[0]), "=f"(v[1]) : "r"(addr));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Decode-once GQA fused fetch: G query heads share each KV head (Llama-3
+// layout: query head h*G+g reads KV head h).  K warps decode each K slice
+// once and accumulate G dot products per token (q' for every group member
+// in shared memory); V warps decode each V slice once into a bank-swizzled
+// u8 code tile (row stride 132 B, one STS.U16 per decoded pair) and then run a
+// per-channel GEMV over the 64 tokens for all G weight vectors, lanes owning
+// 4 channels each.  Same TMA rings / score ring / split partials as the G=1
+// kernel; partial index = (seq * H*G + h*G + g) * n_splits + split.
+// ---------------------------------------------------------------------------
+constexpr int kTileRow = 132;  // bytes per token row of the V code tile
+constexpr int kTileRow0 = kTileRow;
+__host__ __device__ constexpr int gqa_per_pair(int stage_k, int stage_v, int G) {
+    return 2 * (stage_k + stage_v) + 4 * (G * D + 2 * G * BS + G * BS) + BS * kTileRow0 + 64;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kThreadsWS, 1)
+fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__restrict__ q,
+                      Partial *__restrict__ partial, int chunks_per_split, int n_splits,
+                      int stage_k, int stage_v, int *err) {
+    __shared__ __align__(128) uint32_t s_lutK[1 << KVC_LUT_BITS];
+    __shared__ __align__(128) uint32_t s_lutV[1 << KVC_LUT_BITS];
+    __shared__ uint64_t s_lbar[1];
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const bool is_v = warp >= WS_PAIRS;
+    const int pair = warp & (WS_PAIRS - 1);
+    const int per_pair = gqa_per_pair(stage_k, stage_v, G);
+    uint8_t *pb = smem + pair * per_pair;
+    uint8_t *kring = pb, *vring = pb + 2 * stage_k;
+    float *qf = reinterpret_cast<float *>(pb + 2 * (stage_k + stage_v));  // [128][G]
+    float *sring = qf + G * D;                                            // [2][G][64]
+    float *sa = sring + 2 * G * BS;                                       // [64][G]
+    uint8_t *tile = reinterpret_cast<uint8_t *>(sa + G * BS);            // [64][132]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(tile + BS * kTileRow);
+    uint64_t *kfull = bar, *vfull = bar + 2, *sfull = bar + 4, *sempty = bar + 6;
+
+    const int split = blockIdx.x, h = blockIdx.y, sidx = blockIdx.z;
+    const kvc_seq_desc sd = seqs[sidx];
+    if (!is_v && lane == 0) {
+        mbar_init(&kfull[0], 1);
+        mbar_init(&kfull[1], 1);
+        mbar_init(&vfull[0], 1);
+        mbar_init(&vfull[1], 1);
+        mbar_init(&sfull[0], 32);
+        mbar_init(&sfull[1], 32);
+        mbar_init(&sempty[0], 32);
+        mbar_init(&sempty[1], 32);
+    }
+    if (threadIdx.x == 0) mbar_init(s_lbar, 1);
+    fence_mbar_init();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(s_lbar, 2u * (4u << KVC_LUT_BITS));
+        tma_load_1d(s_lutK, sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+        tma_load_1d(s_lutV, sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+    }
+    const int c_begin = split * chunks_per_split;
+    const int c_end = min(sd.n_chunks, c_begin + chunks_per_split);
+    const int first = c_begin + pair;
+    const int n = first < c_end ? (c_end - first + WS_PAIRS - 1) / WS_PAIRS : 0;
+    const float sm_scale = kLog2e / sqrtf((float)D);
+    auto issue = [&](bool v, int j) {
+        const long ord = (long)(first + WS_PAIRS * j) * H + h;
+        const uint32_t *offs = v ? sd.v_offsets : sd.k_offsets;
+        const kvc_arena_counters *ct = v ? sd.v_counters : sd.k_counters;
+        const long nb = (long)ct->n_blocks;
+        const uint64_t s0 = offs[ord];
+        const uint64_t e0 = (ord + 1 < nb) ? (uint64_t)offs[ord + 1] : ct->cursor;
+        const uint64_t a = s0 & ~15ull;
+        uint32_t bytes = (uint32_t)(((e0 + 15) & ~15ull) - a);
+        if (bytes > (uint32_t)(v ? stage_v : stage_k)) {
+            kvc_set_err(err, KVC_ERR_CODEC);
+            bytes = 16;
+        }
+        uint64_t *b = v ? &vfull[j & 1] : &kfull[j & 1];
+        uint8_t *dst = v ? vring + (j & 1) * stage_v : kring + (j & 1) * stage_k;
+        mbar_expect_tx(b, bytes);
+        tma_load_1d(dst, (v ? sd.v_arena : sd.k_arena) + a, bytes, b);
+    };
+    bool bad = false;
+
+    if (!is_v) {
+        // ============ K warp: G scores per decoded token ============
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegK));
+        if (lane == 0) {
+            if (n > 0) issue(false, 0);
+            if (n > 1) issue(false, 1);
+        }
+        float qreg[G][4];
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                qreg[g][k] = q[((long)sidx * H * G + (long)h * G + g) * D + lane + 32 * k];
+        const uint32_t qf_s = smem_u32(qf), lut_s = smem_u32(s_lutK);
+        mbar_wait(s_lbar, 0);
+        for (int j = 0; j < n; ++j) {
+            const int u = j >> 1, sl = j & 1;
+            mbar_wait(&kfull[sl], u & 1);
+            const long ord = (long)(first + WS_PAIRS * j) * H + h;
+            const uint32_t kofs = sd.k_offsets[ord] & 15u;
+            const uint8_t *ks = kring + sl * stage_k + kofs;
+            const uint32_t cA = lds_u16(ks + 6 + 2 * lane), cB = lds_u16(ks + 6 + 2 * (lane + 32));
+            const uint32_t iA = kvc_warp_incl_scan(cA, lane);
+            const uint32_t totA = __shfl_sync(0xffffffffu, iA, 31);
+            const uint32_t iB = kvc_warp_incl_scan(cB, lane);
+            float base[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) base[g] = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int c = lane + 32 * k;
+                const float sc = lds_f32_a2(ks + 6 + 2 * BS + 8 * c + 4);
+                const float mn = lds_f32_a2(ks + 6 + 2 * BS + 8 * c);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    qf[c * G + g] = sc * qreg[g][k];
+                    base[g] = fmaf(mn, qreg[g][k], base[g]);
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) base[g] = kvc_warp_sum(base[g]);
+            __syncwarp();
+            const uint32_t bit0 = (kofs + K_HDR) * 8, slot = smem_u32(kring + sl * stage_k);
+            Cursor2 cc[2];
+            cursor2_init(cc[0], slot, bit0 + iA - cA);
+            cursor2_init(cc[1], slot, bit0 + totA + iB - cB);
+            const uint32_t p0A = cc[0].p, p0B = cc[1].p;
+            float2 sA2[G], sB2[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) sA2[g] = sB2[g] = make_float2(0.f, 0.f);
+#pragma unroll 1
+            for (int c5 = 0; c5 < 65; c5 += 5) {
+                cursor2_reload(cc[0]);
+                cursor2_reload(cc[1]);
+#pragma unroll
+                for (int t = 0; t < 5; ++t) {
+                    const int c2 = c5 + t;
+                    if (c2 < D / 2) {
+                        const float2 fA = cursor2_pair(cc[0], lut_s), fB = cursor2_pair(cc[1], lut_s);
+                        // q' of channels 2*c2 and 2*c2+1 for all G members (broadcast loads)
+                        float qa[G], qb[G];
+                        lds_vec<G>(qf_s + 4 * G * (2 * c2), qa);
+                        lds_vec<G>(qf_s + 4 * G * (2 * c2 + 1), qb);
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            const float2 q2 = make_float2(qa[g], qb[g]);
+                            sA2[g] = __ffma2_rn(fA, q2, sA2[g]);
+                            sB2[g] = __ffma2_rn(fB, q2, sB2[g]);
+                        }
+                    }
+                }
+            }
+            bad |= (((cc[0].p - p0A) & 0xFFFFu) != cA) | (((cc[1].p - p0B) & 0xFFFFu) != cB);
+            mbar_wait(&sempty[sl], (u & 1) ^ 1);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                sring[(sl * G + g) * BS + lane] = (sA2[g].x + sA2[g].y + base[g]) * sm_scale;
+                sring[(sl * G + g) * BS + lane + 32] = (sB2[g].x + sB2[g].y + base[g]) * sm_scale;
+            }
+            mbar_arrive(&sfull[sl]);
+            __syncwarp();
+            if (lane == 0 && j + 2 < n) issue(false, j + 2);
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) kvc_set_err(err, KVC_ERR_CODEC);
+        __syncthreads();
+        __syncthreads();
+        return;
+    }
+
+    // ============ V warp: decode once into the tile, GEMV for G heads ============
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegV));
+    if (lane == 0) {
+        if (n > 0) issue(true, 0);
+        if (n > 1) issue(true, 1);
+    }
+    float m[G], lsum[G], wm[G], acc[G][4];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        m[g] = -INFINITY;
+        lsum[g] = wm[g] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[g][k] = 0.f;
+    }
+    const uint32_t lut_s = smem_u32(s_lutV), tile_s = smem_u32(tile), sa_s = smem_u32(sa);
+    mbar_wait(s_lbar, 0);
+    for (int j = 0; j < n; ++j) {
+        const int u = j >> 1, sl = j & 1;
+        mbar_wait(&sfull[sl], u & 1);
+        float pA[G], pB[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            pA[g] = sring[(sl * G + g) * BS + lane];
+            pB[g] = sring[(sl * G + g) * BS + lane + 32];
+        }
+        mbar_arrive(&sempty[sl]);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const float bm = kvc_warp_max(fmaxf(pA[g], pB[g]));
+            if (bm > m[g]) {
+                const float alpha = exp2f(m[g] - bm);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) acc[g][k] *= alpha;
+                lsum[g] *= alpha;
+                wm[g] *= alpha;
+                m[g] = bm;
+            }
+            pA[g] = exp2f(pA[g] - m[g]);
+            pB[g] = exp2f(pB[g] - m[g]);
+            lsum[g] += pA[g] + pB[g];
+        }
+        mbar_wait(&vfull[sl], u & 1);
+        const long ord = (long)(first + WS_PAIRS * j) * H + h;
+        const uint32_t vofs = sd.v_offsets[ord] & 15u;
+        const uint8_t *vs = vring + sl * stage_v + vofs;
+        const uint32_t cA = lds_u16(vs + 6 + 2 * lane), cB = lds_u16(vs + 6 + 2 * (lane + 32));
+        const uint32_t iA = kvc_warp_incl_scan(cA, lane);
+        const uint32_t totA = __shfl_sync(0xffffffffu, iA, 31);
+        const uint32_t iB = kvc_warp_incl_scan(cB, lane);
+        const float scA = lds_f32_a2(vs + 6 + 2 * BS + 8 * lane + 4);
+        const float scB = lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32) + 4);
+        const float mnA = lds_f32_a2(vs + 6 + 2 * BS + 8 * lane);
+        const float mnB = lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32));
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            sa[lane * G + g] = pA[g] * scA;
+            sa[(lane + 32) * G + g] = pB[g] * scB;
+            wm[g] = fmaf(pA[g], mnA, fmaf(pB[g], mnB, wm[g]));
+        }
+        // decode V slices A (token lane) and B (token lane+32) into the tile
+        const uint32_t bit0 = (vofs + V_HDR) * 8, slot = smem_u32(vring + sl * stage_v);
+        Cursor2 cc[2];
+        cursor2_init(cc[0], slot, bit0 + iA - cA);
+        cursor2_init(cc[1], slot, bit0 + totA + iB - cB);
+        const uint32_t p0A = cc[0].p, p0B = cc[1].p;
+        const uint32_t rowA = tile_s + lane * kTileRow, rowB = tile_s + (lane + 32) * kTileRow;
+#pragma unroll 1
+        for (int c5 = 0; c5 < 65; c5 += 5) {
+            cursor2_reload(cc[0]);
+            cursor2_reload(cc[1]);
+#pragma unroll
+            for (int t = 0; t < 5; ++t) {
+                const int c2 = c5 + t;
+                if (c2 < D / 2) {
+                    const uint32_t eA = lds32(lut_s + ((cc[0].hi >> 20) << 2));
+                    cc[0].hi = __funnelshift_l(cc[0].lo, cc[0].hi, eA);
+                    cc[0].lo = __funnelshift_l(0u, cc[0].lo, eA);
+                    cc[0].p += eA;
+                    const uint32_t eB = lds32(lut_s + ((cc[1].hi >> 20) << 2));
+                    cc[1].hi = __funnelshift_l(cc[1].lo, cc[1].hi, eB);
+                    cc[1].lo = __funnelshift_l(0u, cc[1].lo, eB);
+                    cc[1].p += eB;
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(rowA + 2 * c2), "h"((unsigned short)(eA >> 16)));
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(rowB + 2 * c2), "h"((unsigned short)(eB >> 16)));
+                }
+            }
+        }
+        bad |= (((cc[0].p - p0A) & 0xFFFFu) != cA) | (((cc[1].p - p0B) & 0xFFFFu) != cB);
+        __syncwarp();
+        // GEMV: lane owns channels 4*lane .. 4*lane+3 over the chunk's 64 tokens
+        const float2 magic = make_float2(-8388608.f, -8388608.f);
+#pragma unroll 4
+        for (int t = 0; t < BS; ++t) {
+            const uint32_t w = lds32(tile_s + t * kTileRow + 4 * lane);
+            const float2 f01 = __fadd2_rn(make_float2(sym_hi_byte(w, 0x7650), sym_hi_byte(w, 0x7651)), magic);
+            const float2 f23 = __fadd2_rn(make_float2(sym_hi_byte(w, 0x7652), sym_hi_byte(w, 0x7653)), magic);
+            float av[G];
+            lds_vec<G>(sa_s + 4 * G * t, av);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float a = av[g];
+                acc[g][0] = fmaf(a, f01.x, acc[g][0]);
+                acc[g][1] = fmaf(a, f01.y, acc[g][1]);
+                acc[g][2] = fmaf(a, f23.x, acc[g][2]);
+                acc[g][3] = fmaf(a, f23.y, acc[g][3]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0 && j + 2 < n) issue(true, j + 2);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) kvc_set_err(err, KVC_ERR_CODEC);
+    __syncthreads();  // K warps done: their region is scratch
+    Partial *wp = reinterpret_cast<Partial *>(smem + pair * per_pair);  // G partials per pair
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const float l = kvc_warp_sum(lsum[g]), w2 = kvc_warp_sum(wm[g]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) wp[g].o[4 * lane + k] = acc[g][k] + w2;
+        if (lane == 0) {
+            wp[g].m = m[g];
+            wp[g].l = l;
+        }
+    }
+    __syncthreads();
+    if (pair == 0) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float M = -INFINITY;
+            for (int w = 0; w < WS_PAIRS; ++w)
+                M = fmaxf(M, reinterpret_cast<const Partial *>(smem + w * per_pair)[g].m);
+            float L = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int w = 0; w < WS_PAIRS; ++w) {
+                const Partial *pw = reinterpret_cast<const Partial *>(smem + w * per_pair) + g;
+                const float sc = (pw->m == -INFINITY) ? 0.f : exp2f(pw->m - M);
+                L += pw->l * sc;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) o[k] += pw->o[lane + 32 * k] * sc;
+            }
+            Partial *dst = partial + ((long)sidx * H * G + (long)h * G + g) * n_splits + split;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst->o[lane + 32 * k] = o[k];
+            if (lane == 0) {
+                dst->m = M;
+                dst->l = L;
+            }
+        }
+    }
+}
+
 // Merge split partials + the f32 buffered tokens (attention.py:103-107,
 // :160-164) into out = O / L; also writes buffered scores when requested.
 __global__ void __launch_bounds__(128)
 combine_kernel(const kvc_seq_desc *__restrict__ seqs, int H, int bs, const float *__restrict__ q,
                const Partial *__restrict__ partial, int n_splits, float *__restrict__ out,
-               float *__restrict__ scores, long ctx_stride) {
+               float *__restrict__ scores, long ctx_stride, int group = 1) {
     __shared__ float sh_p[1024];
     __shared__ float sh_red[8];
     __shared__ float sh_m, sh_l;
-    const int h = blockIdx.y, sidx = blockIdx.z;
+    const int hq = blockIdx.y, sidx = blockIdx.z, h = hq / group, HQ = H * group;
     const kvc_seq_desc sd = seqs[sidx];
-    const float *qh = q + ((long)sidx * H + h) * D;
+    const float *qh = q + ((long)sidx * HQ + hq) * D;
     const float sm_scale = kLog2e / sqrtf((float)D), inv_sqrt = 1.0f / sqrtf((float)D);
     const int nbuf = sd.buffered;
     const long t0 = (long)sd.n_chunks * bs;
@@ -892,7 +1225,7 @@ combine_kernel(const kvc_seq_desc *__restrict__ seqs, int H, int bs, const float
         const float *kv = sd.k_buffer + ((long)t * H + h) * D;
         float a = 0.f;
         for (int c = 0; c < D; ++c) a = fmaf(kv[c], qh[c], a);
-        if (scores) scores[((long)sidx * H + h) * ctx_stride + t0 + t] = a * inv_sqrt;
+        if (scores) scores[((long)sidx * HQ + hq) * ctx_stride + t0 + t] = a * inv_sqrt;
         sh_p[t] = a * sm_scale;
         bmax = fmaxf(bmax, a * sm_scale);
     }
@@ -902,7 +1235,7 @@ combine_kernel(const kvc_seq_desc *__restrict__ seqs, int H, int bs, const float
     if (threadIdx.x == 0) {
         float M = -INFINITY;
         for (int w = 0; w < 4; ++w) M = fmaxf(M, sh_red[w]);
-        const Partial *p = partial + ((long)sidx * H + h) * n_splits;
+        const Partial *p = partial + ((long)sidx * HQ + hq) * n_splits;
         for (int s = 0; s < n_splits; ++s) M = fmaxf(M, p[s].m);
         sh_m = M;
     }
@@ -920,19 +1253,19 @@ combine_kernel(const kvc_seq_desc *__restrict__ seqs, int H, int bs, const float
     __syncthreads();
     if (threadIdx.x == 0) {
         float L = sh_red[0] + sh_red[1] + sh_red[2] + sh_red[3];
-        const Partial *p = partial + ((long)sidx * H + h) * n_splits;
+        const Partial *p = partial + ((long)sidx * HQ + hq) * n_splits;
         for (int s = 0; s < n_splits; ++s)
             if (p[s].m != -INFINITY) L += p[s].l * exp2f(p[s].m - M);
         sh_l = L;
     }
     __syncthreads();
-    const Partial *p = partial + ((long)sidx * H + h) * n_splits;
+    const Partial *p = partial + ((long)sidx * HQ + hq) * n_splits;
     for (int c = threadIdx.x; c < D; c += blockDim.x) {
         float o = 0.f;
         for (int s = 0; s < n_splits; ++s)
             if (p[s].m != -INFINITY) o += p[s].o[c] * exp2f(p[s].m - M);
         for (int t = 0; t < nbuf; ++t) o = fmaf(sh_p[t], sd.v_buffer[((long)t * H + h) * D + c], o);
-        out[((long)sidx * H + h) * D + c] = o / sh_l;
+        out[((long)sidx * HQ + hq) * D + c] = o / sh_l;
     }
 }
 
@@ -1126,7 +1459,8 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
                              void *stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (n_seqs < 1 || H < 1) return kvc_fail(KVC_ERR_CONFIG, "bad shape");
-    if (group != 1) return kvc_fail(KVC_ERR_CONFIG, "kvc_attention: use kvc_attention_gqa for group > 1");
+    if (group != 1 && group != 2 && group != 4)
+        return kvc_fail(KVC_ERR_CONFIG, "fused GQA supports group 2 or 4");
     int max_chunks = 0, max_len = 0, stage_k = 0, stage_v = 0;
     for (int i = 0; i < n_seqs; ++i) {
         max_chunks = seqs_host[i].n_chunks > max_chunks ? seqs_host[i].n_chunks : max_chunks;
@@ -1159,6 +1493,36 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
     if (smem + lut_bytes + 256 > 227 * 1024)
         return kvc_fail(KVC_ERR_CONFIG, "block extents too large for staging");
     dim3 grid(n_splits, H, n_seqs);
+    if (group > 1) {
+        // decode-once GQA kernel (pair LUT: every code <= 6 bits)
+        if (mode != 1 || max_chunks == 0)
+            return kvc_fail(KVC_ERR_CONFIG, "fused GQA needs codes <= 6 bits and a compressed region");
+        const int g_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H);
+        const int g_splits = (max_chunks + g_cps - 1) / g_cps;
+        if (sizeof(Partial) * (size_t)n_seqs * H * group * g_splits > workspace_bytes)
+            return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
+        const size_t g_smem = WS_PAIRS * (size_t)gqa_per_pair(stage_k, stage_v, group);
+        if (g_smem + 2 * 16384 + 256 > 227 * 1024)
+            return kvc_fail(KVC_ERR_CONFIG, "block extents too large for GQA staging");
+        dim3 g3(g_splits, H, n_seqs);
+        if (group == 2) {
+            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_gqa_kernel<2>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
+            fused_attn_gqa_kernel<2><<<g3, kThreadsWS, g_smem, s>>>(
+                seqs_dev, H, q_dev, part, g_cps, g_splits, stage_k, stage_v, err_dev);
+        } else {
+            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_gqa_kernel<4>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
+            fused_attn_gqa_kernel<4><<<g3, kThreadsWS, g_smem, s>>>(
+                seqs_dev, H, q_dev, part, g_cps, g_splits, stage_k, stage_v, err_dev);
+        }
+        int st = kvc_check_launch("fused_attn_gqa_kernel");
+        if (st) return st;
+        combine_kernel<<<dim3(1, H * group, n_seqs), 128, 0, s>>>(seqs_dev, H, bs, q_dev, part,
+                                                                  g_splits, out_dev, nullptr, 0,
+                                                                  group);
+        return kvc_check_launch("combine_kernel");
+    }
     const char *impl = getenv("KVC_FUSED_IMPL");
     const bool use_ws = !(impl && impl[0] == 'i');
     const size_t ws_smem = WS_PAIRS * (2 * (size_t)(stage_k + stage_v) + 1024 + 64);

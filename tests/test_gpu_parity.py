@@ -342,17 +342,24 @@ def test_dense_fp16_gqa(kv, group):
     assert max_relative_error(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-5
 
 
-def test_fused_gqa_matches_per_member_steps(kv):
-    """Config-3 style: 2 KV heads x group 4; each query head attends its KV head."""
-    group, H = 4, 2
+@pytest.mark.parametrize("group", [2, 4, 3])
+def test_fused_gqa_matches_per_member_steps(kv, group):
+    """Config-3 style: 2 KV heads x group G; each query head attends its KV head
+    (G = 2, 4: decode-once GQA kernel; G = 3: per-member launches)."""
+    H = 2
     k = kv.generate_synthetic(kv.SyntheticSpec(2000, H, 128, seed=40)).values.astype(np.float16)
     v = kv.generate_synthetic(kv.SyntheticSpec(2000, H, 128, seed=41)).values.astype(np.float16)
     st = kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v),
                                     kv.QuantConfig(kv.QuantMode.K_BLOCK),
                                     kv.QuantConfig(kv.QuantMode.V_TOKEN))
-    q = np.random.default_rng(4).standard_normal((1, H * group, 128), dtype=np.float32)
-    out = kv.attention_gqa([st], torch.from_numpy(q).cuda(), group)
-    for j in range(group):
-        r = kv.attention_step(st, q[0].reshape(H, group, 128)[:, j])
-        assert max_relative_error(out[0].view(H, group, 128)[:, j].cpu().numpy(),
-                                  r.out.cpu().numpy()) <= 1e-6
+    for extra in (0, 37):  # with and without buffered tokens
+        if extra:
+            for t in range(extra):
+                st.append_token(np.ones((H, 128), np.float32) * 0.01 * t,
+                                np.ones((H, 128), np.float32) * 0.02 * t)
+        q = np.random.default_rng(4).standard_normal((1, H * group, 128), dtype=np.float32)
+        out = kv.attention_gqa([st], torch.from_numpy(q).cuda(), group)
+        for j in range(group):
+            r = kv.attention_step(st, q[0].reshape(H, group, 128)[:, j])
+            assert max_relative_error(out[0].view(H, group, 128)[:, j].cpu().numpy(),
+                                      r.out.cpu().numpy()) <= 1e-5
