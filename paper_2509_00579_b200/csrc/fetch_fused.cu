@@ -1425,14 +1425,27 @@ int num_sms() {
     return g_num_sms;
 }
 
-int pick_chunks_per_split(int max_chunks, long n_heads_total) {
-    // aim for >= ~4 waves of 2 CTAs/SM, each warp owning >= 4 chunks
-    long target_ctas = (long)num_sms() * 2 * 4;
-    long splits = (target_ctas + n_heads_total - 1) / n_heads_total;
-    long cps = (max_chunks + splits - 1) / (splits > 0 ? splits : 1);
-    if (cps < 4 * NW) cps = 4 * NW;
-    cps = (cps + NW - 1) / NW * NW;
-    return (int)cps;
+// Chunks per CTA split.  Candidates are multiples of 4 (one per K/V pair);
+// the model charges each CTA a pipeline fill of ~1 chunk per pair and counts
+// the idle part of the last wave (resident CTAs = ctas_per_sm x SMs), and picks
+// the split with the lowest estimated time.
+int pick_chunks_per_split(int max_chunks, long n_heads_total, int ctas_per_sm = 2) {
+    const long slots = (long)num_sms() * ctas_per_sm;
+    long best_cps = 4 * NW;
+    double best = 1e30;
+    for (long cps = 4 * NW; cps <= 4096; cps += NW) {
+        const long splits = (max_chunks + cps - 1) / cps;
+        const long ctas = splits * n_heads_total;
+        const double per_cta = (double)cps / NW + 1.0;          // chunk-times per pair
+        const double waves = ceil((double)ctas / (double)slots);
+        const double t = waves * per_cta;
+        if (t < best - 1e-9) {
+            best = t;
+            best_cps = cps;
+        }
+        if (splits == 1) break;
+    }
+    return (int)best_cps;
 }
 
 }  // namespace
@@ -1497,7 +1510,7 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         // decode-once GQA kernel (pair LUT: every code <= 6 bits)
         if (mode != 1 || max_chunks == 0)
             return kvc_fail(KVC_ERR_CONFIG, "fused GQA needs codes <= 6 bits and a compressed region");
-        const int g_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H);
+        const int g_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H, 1);
         const int g_splits = (max_chunks + g_cps - 1) / g_cps;
         if (sizeof(Partial) * (size_t)n_seqs * H * group * g_splits > workspace_bytes)
             return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
