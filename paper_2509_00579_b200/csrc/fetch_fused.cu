@@ -147,6 +147,7 @@ __device__ __forceinline__ float sym_hi_byte(uint32_t e, uint32_t sel) {
 template <int MODE>
 struct Dec {
     static constexpr int kLutWords = MODE == 0 ? 64 * 32 : (1 << KVC_LUT_BITS);
+    static constexpr bool kPair = MODE == 1 || MODE == 3;  // the 4096-entry pair LUT (TMA-loaded)
     // symbols decodable from one 32-bit window; MODE 0 uses 4 (not 5) so the
     // reload cadence divides the unrolled loop (24 of 32 bits)
     static constexpr int kSymsPerWin = MODE == 0 ? 4 : (MODE == 1 ? 4 : 2);
@@ -165,7 +166,7 @@ __device__ void build_lut(uint32_t *dst, const kvc_codebook_dev *cb) {
         uint32_t e12;
         if (MODE == 0) e12 = cb->lut[(i >> 5) << 6];
         else if (MODE == 2) e12 = cb->lut[i];
-        else { dst[i] = cb->fetch_lut[i]; continue; }
+        else { dst[i] = cb->fetch_lut[i & 4095]; continue; }
         dst[i] = __float_as_uint((float)(e12 & 0xFF)) | ((e12 >> 8) & 0xF);
     }
 }
@@ -514,6 +515,36 @@ __device__ __forceinline__ float2 cursor2_pair(Cursor2 &c, uint32_t lut_s) {
                       make_float2(-8388608.f, -8388608.f));
 }
 
+// Pair step with the low 5 index bits replaced by the lane id (MODE 3).  The
+// last 5 bits of a 12-bit window are don't-care whenever the pair is <= 7
+// bits long, so entry (idx & ~31) | lane equals entry idx and the lookup of
+// every such lane lands in bank `lane`: conflict-free.  A pair of >= 8 bits
+// (bit 3 of the consumed-bits field; the substituted entry shares the first
+// 7 bits, so it is >= 8 bits too) is re-read at its true index, predicated,
+// by the few lanes that need it.  At default V scales ~8% of pairs do, so a
+// lookup costs ~2.0 wavefronts instead of ~3.5.
+__device__ __forceinline__ uint32_t lut_pair_sub(uint32_t hi, uint32_t lut_s, uint32_t lane4) {
+    const uint32_t x = hi >> 18;
+    uint32_t e = lds32(lut_s + ((x & 0x3F80u) | lane4));
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p " KVC_LD_SHARED ".u32 %0, [%2];\n\t}"
+                 : "+r"(e) : "r"(e & 8u), "r"(lut_s + (x & 0x3FFCu)));
+    return e;
+}
+__device__ __forceinline__ float2 cursor2_pair_sub(Cursor2 &c, uint32_t lut_s, uint32_t lane4) {
+    const uint32_t e = lut_pair_sub(c.hi, lut_s, lane4);
+    c.hi = __funnelshift_l(c.lo, c.hi, e);
+    c.lo = __funnelshift_l(0u, c.lo, e);
+    c.p += e;
+    return __fadd2_rn(make_float2(sym_hi_byte(e, 0x7652), sym_hi_byte(e, 0x7653)),
+                      make_float2(-8388608.f, -8388608.f));
+}
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+    float4 v;
+    asm volatile(KVC_LD_SHARED ".v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
+
 // Decode the 128 symbols of two slices (cursors c[0], c[1]) in lockstep and
 // hand each channel pair to sink(c2, f[slice0], f[slice1]).  Fully unrolled so
 // the sink can index register arrays with c2.
@@ -616,18 +647,19 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
         mbar_init(&sempty[0], 32);
         mbar_init(&sempty[1], 32);
     }
-    constexpr bool kTma = MODE == 1 || VMODE == 1;
+    constexpr bool kPK = Dec<MODE>::kPair, kPV = Dec<VMODE>::kPair;
+    constexpr bool kTma = kPK || kPV;
     if (kTma && threadIdx.x == 0) mbar_init(s_lbar, 1);
     fence_mbar_init();
     __syncthreads();
     if (kTma && threadIdx.x == 0) {
-        mbar_expect_tx(s_lbar, ((MODE == 1) + (VMODE == 1)) * (4u << KVC_LUT_BITS));
-        if (MODE == 1) tma_load_1d(s_lutK, sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
-        if (VMODE == 1) tma_load_1d(s_lutV, sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+        mbar_expect_tx(s_lbar, ((int)kPK + (int)kPV) * (4u << KVC_LUT_BITS));
+        if (kPK) tma_load_1d(s_lutK, sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+        if (kPV) tma_load_1d(s_lutV, sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
     }
-    if (MODE != 1) build_lut<MODE>(s_lutK, sd.k_cb);
-    if (VMODE != 1) build_lut<VMODE>(s_lutV, sd.v_cb);
-    if (MODE != 1 || VMODE != 1) __syncthreads();
+    if (!kPK) build_lut<MODE>(s_lutK, sd.k_cb);
+    if (!kPV) build_lut<VMODE>(s_lutV, sd.v_cb);
+    if (!kPK || !kPV) __syncthreads();
 
     const int c_begin = split * chunks_per_split;
     const int c_end = min(sd.n_chunks, c_begin + chunks_per_split);
@@ -698,24 +730,35 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
             cursor_init(cur[1], slot, bit0 + totA + iB - cB);
             const uint32_t p0A = cur[0].p, p0B = cur[1].p;
             float2 sA2 = make_float2(0.f, 0.f), sB2 = sA2;
-            if (MODE == 1) {
+            if (Dec<MODE>::kPair) {
                 // 64-bit windows, one reload per 5 pair steps (<= 60 bits at
-                // max_len 6): 12 groups of 5 + a tail of 4 pair steps.
+                // max_len 6).
                 Cursor2 c2c[2];
                 cursor2_init(c2c[0], slot, bit0 + iA - cA);
                 cursor2_init(c2c[1], slot, bit0 + totA + iB - cB);
+                // q' for two pair steps per LDS.128 (broadcast): groups of 10
+                // steps = 2 reloads + 5 q loads; 6 groups + a tail of 4.
                 auto steps = [&](int c2base, auto np) {
-                    cursor2_reload(c2c[0]);
-                    cursor2_reload(c2c[1]);
+                    float4 q4 = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                     for (int t = 0; t < decltype(np)::value; ++t) {
-                        const float2 q2 = lds64f(qf_s + 8 * (c2base + t));
-                        sA2 = __ffma2_rn(cursor2_pair(c2c[0], lut_s), q2, sA2);
-                        sB2 = __ffma2_rn(cursor2_pair(c2c[1], lut_s), q2, sB2);
+                        if (t % 5 == 0) {
+                            cursor2_reload(c2c[0]);
+                            cursor2_reload(c2c[1]);
+                        }
+                        if (t % 2 == 0) q4 = lds128f(qf_s + 8 * (c2base + t));
+                        const float2 q2 = (t % 2 == 0) ? make_float2(q4.x, q4.y) : make_float2(q4.z, q4.w);
+                        if (MODE == 3) {
+                            sA2 = __ffma2_rn(cursor2_pair_sub(c2c[0], lut_s, 4 * lane), q2, sA2);
+                            sB2 = __ffma2_rn(cursor2_pair_sub(c2c[1], lut_s, 4 * lane), q2, sB2);
+                        } else {
+                            sA2 = __ffma2_rn(cursor2_pair(c2c[0], lut_s), q2, sA2);
+                            sB2 = __ffma2_rn(cursor2_pair(c2c[1], lut_s), q2, sB2);
+                        }
                     }
                 };
 #pragma unroll 1
-                for (int g = 0; g < 12; ++g) steps(5 * g, std::integral_constant<int, 5>());
+                for (int g = 0; g < 6; ++g) steps(10 * g, std::integral_constant<int, 10>());
                 steps(60, std::integral_constant<int, 4>());
                 cur[0].p = c2c[0].p;
                 cur[1].p = c2c[1].p;
@@ -795,7 +838,7 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
         cursor_init(cur[0], slot, bit0 + iA - cA);
         cursor_init(cur[1], slot, bit0 + totA + iB - cB);
         const uint32_t p0A = cur[0].p, p0B = cur[1].p;
-        if (VMODE == 1 || VMODE == 0) {
+        if (VMODE == 1 || VMODE == 0 || VMODE == 3) {
             // 64-bit windows; 5 pair steps (<= 60 bits at max_len 6) per reload
             Cursor2 c2c[2];
             cursor2_init(c2c[0], slot, bit0 + iA - cA);
@@ -809,6 +852,9 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
                 if (VMODE == 1) {
                     acc[c2] = __ffma2_rn(cursor2_pair(c2c[0], lut_s), aA2, acc[c2]);
                     acc[c2] = __ffma2_rn(cursor2_pair(c2c[1], lut_s), aB2, acc[c2]);
+                } else if (VMODE == 3) {
+                    acc[c2] = __ffma2_rn(cursor2_pair_sub(c2c[0], lut_s, 4 * lane), aA2, acc[c2]);
+                    acc[c2] = __ffma2_rn(cursor2_pair_sub(c2c[1], lut_s, 4 * lane), aB2, acc[c2]);
                 } else {
                     const uint32_t a0 = cursor2_sym(c2c[0], lane_s), b0 = cursor2_sym(c2c[1], lane_s);
                     const uint32_t a1 = cursor2_sym(c2c[0], lane_s), b1 = cursor2_sym(c2c[1], lane_s);
@@ -898,8 +944,8 @@ __host__ __device__ constexpr int gqa_per_pair(int stage_k, int stage_v, int G) 
     return 2 * (stage_k + stage_v) + 4 * (G * D + 2 * G * BS + G * BS) + BS * kTileRow0 + 64;
 }
 
-template <int G>
-__global__ void __launch_bounds__(kThreadsWS, 1)
+template <int G, int NP>
+__global__ void __launch_bounds__(NP * 64, 1)
 fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__restrict__ q,
                       Partial *__restrict__ partial, int chunks_per_split, int n_splits,
                       int stage_k, int stage_v, int *err) {
@@ -909,8 +955,8 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
-    const bool is_v = warp >= WS_PAIRS;
-    const int pair = warp & (WS_PAIRS - 1);
+    const bool is_v = warp >= NP;
+    const int pair = is_v ? warp - NP : warp;
     const int per_pair = gqa_per_pair(stage_k, stage_v, G);
     uint8_t *pb = smem + pair * per_pair;
     uint8_t *kring = pb, *vring = pb + 2 * stage_k;
@@ -944,10 +990,10 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     const int c_begin = split * chunks_per_split;
     const int c_end = min(sd.n_chunks, c_begin + chunks_per_split);
     const int first = c_begin + pair;
-    const int n = first < c_end ? (c_end - first + WS_PAIRS - 1) / WS_PAIRS : 0;
+    const int n = first < c_end ? (c_end - first + NP - 1) / NP : 0;
     const float sm_scale = kLog2e / sqrtf((float)D);
     auto issue = [&](bool v, int j) {
-        const long ord = (long)(first + WS_PAIRS * j) * H + h;
+        const long ord = (long)(first + NP * j) * H + h;
         const uint32_t *offs = v ? sd.v_offsets : sd.k_offsets;
         const kvc_arena_counters *ct = v ? sd.v_counters : sd.k_counters;
         const long nb = (long)ct->n_blocks;
@@ -984,7 +1030,7 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
         for (int j = 0; j < n; ++j) {
             const int u = j >> 1, sl = j & 1;
             mbar_wait(&kfull[sl], u & 1);
-            const long ord = (long)(first + WS_PAIRS * j) * H + h;
+            const long ord = (long)(first + NP * j) * H + h;
             const uint32_t kofs = sd.k_offsets[ord] & 15u;
             const uint8_t *ks = kring + sl * stage_k + kofs;
             const uint32_t cA = lds_u16(ks + 6 + 2 * lane), cB = lds_u16(ks + 6 + 2 * (lane + 32));
@@ -1097,7 +1143,7 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
             lsum[g] += pA[g] + pB[g];
         }
         mbar_wait(&vfull[sl], u & 1);
-        const long ord = (long)(first + WS_PAIRS * j) * H + h;
+        const long ord = (long)(first + NP * j) * H + h;
         const uint32_t vofs = sd.v_offsets[ord] & 15u;
         const uint8_t *vs = vring + sl * stage_v + vofs;
         const uint32_t cA = lds_u16(vs + 6 + 2 * lane), cB = lds_u16(vs + 6 + 2 * (lane + 32));
@@ -1183,10 +1229,10 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             float M = -INFINITY;
-            for (int w = 0; w < WS_PAIRS; ++w)
+            for (int w = 0; w < NP; ++w)
                 M = fmaxf(M, reinterpret_cast<const Partial *>(smem + w * per_pair)[g].m);
             float L = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
-            for (int w = 0; w < WS_PAIRS; ++w) {
+            for (int w = 0; w < NP; ++w) {
                 const Partial *pw = reinterpret_cast<const Partial *>(smem + w * per_pair) + g;
                 const float sc = (pw->m == -INFINITY) ? 0.f : exp2f(pw->m - M);
                 L += pw->l * sc;
@@ -1429,14 +1475,14 @@ int num_sms() {
 // the model charges each CTA a pipeline fill of ~1 chunk per pair and counts
 // the idle part of the last wave (resident CTAs = ctas_per_sm x SMs), and picks
 // the split with the lowest estimated time.
-int pick_chunks_per_split(int max_chunks, long n_heads_total, int ctas_per_sm = 2) {
+int pick_chunks_per_split(int max_chunks, long n_heads_total, int ctas_per_sm = 2, int pairs = NW) {
     const long slots = (long)num_sms() * ctas_per_sm;
-    long best_cps = 4 * NW;
+    long best_cps = 4 * pairs;
     double best = 1e30;
-    for (long cps = 4 * NW; cps <= 4096; cps += NW) {
+    for (long cps = 4 * pairs; cps <= 4096; cps += pairs) {
         const long splits = (max_chunks + cps - 1) / cps;
         const long ctas = splits * n_heads_total;
-        const double per_cta = (double)cps / NW + 1.0;          // chunk-times per pair
+        const double per_cta = (double)cps / pairs + 1.0;       // chunk-times per pair
         const double waves = ceil((double)ctas / (double)slots);
         const double t = waves * per_cta;
         if (t < best - 1e-9) {
@@ -1510,25 +1556,33 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         // decode-once GQA kernel (pair LUT: every code <= 6 bits)
         if (mode != 1 || max_chunks == 0)
             return kvc_fail(KVC_ERR_CONFIG, "fused GQA needs codes <= 6 bits and a compressed region");
-        const int g_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H, 1);
+        // pairs per CTA (one CTA per SM): 6 when the staging fits, else 4
+        const size_t pp = (size_t)gqa_per_pair(stage_k, stage_v, group);
+        int np = 6;
+        const char *npenv = getenv("KVC_GQA_PAIRS");
+        if (npenv && npenv[0] == '4') np = 4;
+        if (np * pp + 2 * 16384 + 256 > 227 * 1024) np = 4;
+        const size_t g_smem = np * pp;
+        if (g_smem + 2 * 16384 + 256 > 227 * 1024)
+            return kvc_fail(KVC_ERR_CONFIG, "block extents too large for GQA staging");
+        const int g_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H, 1, np);
         const int g_splits = (max_chunks + g_cps - 1) / g_cps;
         if (sizeof(Partial) * (size_t)n_seqs * H * group * g_splits > workspace_bytes)
             return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
-        const size_t g_smem = WS_PAIRS * (size_t)gqa_per_pair(stage_k, stage_v, group);
-        if (g_smem + 2 * 16384 + 256 > 227 * 1024)
-            return kvc_fail(KVC_ERR_CONFIG, "block extents too large for GQA staging");
         dim3 g3(g_splits, H, n_seqs);
+#define KVC_LAUNCH_GQA(GG, NPP)                                                                     \
+    do {                                                                                            \
+        KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_gqa_kernel<GG, NPP>,                           \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem)); \
+        fused_attn_gqa_kernel<GG, NPP><<<g3, NPP * 64, g_smem, s>>>(                                \
+            seqs_dev, H, q_dev, part, g_cps, g_splits, stage_k, stage_v, err_dev);                  \
+    } while (0)
         if (group == 2) {
-            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_gqa_kernel<2>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
-            fused_attn_gqa_kernel<2><<<g3, kThreadsWS, g_smem, s>>>(
-                seqs_dev, H, q_dev, part, g_cps, g_splits, stage_k, stage_v, err_dev);
+            if (np == 6) KVC_LAUNCH_GQA(2, 6); else KVC_LAUNCH_GQA(2, 4);
         } else {
-            KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_gqa_kernel<4>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem));
-            fused_attn_gqa_kernel<4><<<g3, kThreadsWS, g_smem, s>>>(
-                seqs_dev, H, q_dev, part, g_cps, g_splits, stage_k, stage_v, err_dev);
+            if (np == 6) KVC_LAUNCH_GQA(4, 6); else KVC_LAUNCH_GQA(4, 4);
         }
+#undef KVC_LAUNCH_GQA
         int st = kvc_check_launch("fused_attn_gqa_kernel");
         if (st) return st;
         combine_kernel<<<dim3(1, H * group, n_seqs), 128, 0, s>>>(seqs_dev, H, bs, q_dev, part,
@@ -1548,7 +1602,13 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         // V decoder: pair LUT (measured fastest); KVC_FUSED_VMODE=0 selects the
         // lane-replicated, bank-conflict-free single-symbol LUT6 instead.
         const char *venv = getenv("KVC_FUSED_VMODE");
-        const int vmode = (mode == 2) ? 2 : (venv && venv[0] == '0' ? 0 : 1);
+        // default: plain pair LUT for K and V.  KVC_FUSED_VMODE / KVC_FUSED_KMODE
+        // = 3 select the lane-substituted lookups (-16% smem wavefronts, but +14%
+        // instructions and a dependent second LDS: measured 9% slower, profiles/)
+        int vmode = (mode == 2) ? 2 : 1;
+        if (mode != 2 && venv && (venv[0] == '0' || venv[0] == '1' || venv[0] == '3')) vmode = venv[0] - '0';
+        const char *kenv = getenv("KVC_FUSED_KMODE");
+        const int kmode = (mode == 1 && kenv && kenv[0] == '3') ? 3 : mode;
 #define KVC_LAUNCH_WS(M, VM)                                                                 \
     do {                                                                                     \
         KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_ws_kernel<M, VM>,                       \
@@ -1560,8 +1620,10 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
     } while (0)
         if (mode == 2) KVC_LAUNCH_WS(2, 2);
         else if (mode == 0) KVC_LAUNCH_WS(0, 0);
+        else if (kmode == 3 && vmode == 3) KVC_LAUNCH_WS(3, 3);
         else if (vmode == 0) KVC_LAUNCH_WS(1, 0);
-        else KVC_LAUNCH_WS(1, 1);
+        else if (vmode == 1) KVC_LAUNCH_WS(1, 1);
+        else KVC_LAUNCH_WS(1, 3);
 #undef KVC_LAUNCH_WS
         int st = kvc_check_launch("fused_attn_ws_kernel");
         if (st) return st;
