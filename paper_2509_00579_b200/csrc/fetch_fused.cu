@@ -938,13 +938,14 @@ __device__ __forceinline__ void lds_vec(uint32_t addr, float *v) {
 // 4 channels each.  Same TMA rings / score ring / split partials as the G=1
 // kernel; partial index = (seq * H*G + h*G + g) * n_splits + split.
 // ---------------------------------------------------------------------------
-constexpr int kTileRow = 132;  // bytes per token row of the V code tile
-constexpr int kTileRow0 = kTileRow;
-__host__ __device__ constexpr int gqa_per_pair(int stage_k, int stage_v, int G) {
-    return 2 * (stage_k + stage_v) + 4 * (G * D + 2 * G * BS + G * BS) + BS * kTileRow0 + 64;
+// V code half-tile: 64 tokens x 64 channels, row stride 68 B (17 words, odd,
+// so the 32 lanes' row stores land in 32 distinct banks)
+constexpr int kTileRow = 68;
+__host__ __device__ constexpr int gqa_per_pair(int stage_k, int stage_v, int G, int vslots) {
+    return 2 * stage_k + vslots * stage_v + 4 * (G * D + 2 * G * BS + G * BS) + BS * kTileRow + 64;
 }
 
-template <int G, int NP>
+template <int G, int NP, int VS>
 __global__ void __launch_bounds__(NP * 64, 1)
 fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__restrict__ q,
                       Partial *__restrict__ partial, int chunks_per_split, int n_splits,
@@ -957,13 +958,13 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     const uint32_t lane = threadIdx.x & 31;
     const bool is_v = warp >= NP;
     const int pair = is_v ? warp - NP : warp;
-    const int per_pair = gqa_per_pair(stage_k, stage_v, G);
+    const int per_pair = gqa_per_pair(stage_k, stage_v, G, VS);
     uint8_t *pb = smem + pair * per_pair;
     uint8_t *kring = pb, *vring = pb + 2 * stage_k;
-    float *qf = reinterpret_cast<float *>(pb + 2 * (stage_k + stage_v));  // [128][G]
+    float *qf = reinterpret_cast<float *>(pb + 2 * stage_k + VS * stage_v);  // [128][G]
     float *sring = qf + G * D;                                            // [2][G][64]
     float *sa = sring + 2 * G * BS;                                       // [64][G]
-    uint8_t *tile = reinterpret_cast<uint8_t *>(sa + G * BS);            // [64][132]
+    uint8_t *tile = reinterpret_cast<uint8_t *>(sa + G * BS);            // [64][68]
     uint64_t *bar = reinterpret_cast<uint64_t *>(tile + BS * kTileRow);
     uint64_t *kfull = bar, *vfull = bar + 2, *sfull = bar + 4, *sempty = bar + 6;
 
@@ -1005,8 +1006,9 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
             kvc_set_err(err, KVC_ERR_CODEC);
             bytes = 16;
         }
-        uint64_t *b = v ? &vfull[j & 1] : &kfull[j & 1];
-        uint8_t *dst = v ? vring + (j & 1) * stage_v : kring + (j & 1) * stage_k;
+        const int vsl = VS == 2 ? (j & 1) : 0;
+        uint64_t *b = v ? &vfull[vsl] : &kfull[j & 1];
+        uint8_t *dst = v ? vring + vsl * stage_v : kring + (j & 1) * stage_k;
         mbar_expect_tx(b, bytes);
         tma_load_1d(dst, (v ? sd.v_arena : sd.k_arena) + a, bytes, b);
     };
@@ -1105,9 +1107,9 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegV));
     if (lane == 0) {
         if (n > 0) issue(true, 0);
-        if (n > 1) issue(true, 1);
+        if (VS == 2 && n > 1) issue(true, 1);
     }
-    float m[G], lsum[G], wm[G], acc[G][4];
+    float m[G], lsum[G], wm[G], acc[G][4];  // lane owns channels 2l, 2l+1, 64+2l, 65+2l
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         m[g] = -INFINITY;
@@ -1142,10 +1144,11 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
             pB[g] = exp2f(pB[g] - m[g]);
             lsum[g] += pA[g] + pB[g];
         }
-        mbar_wait(&vfull[sl], u & 1);
+        const int vsl = VS == 2 ? sl : 0;
+        mbar_wait(&vfull[vsl], VS == 2 ? (u & 1) : (j & 1));
         const long ord = (long)(first + NP * j) * H + h;
         const uint32_t vofs = sd.v_offsets[ord] & 15u;
-        const uint8_t *vs = vring + sl * stage_v + vofs;
+        const uint8_t *vs = vring + vsl * stage_v + vofs;
         const uint32_t cA = lds_u16(vs + 6 + 2 * lane), cB = lds_u16(vs + 6 + 2 * (lane + 32));
         const uint32_t iA = kvc_warp_incl_scan(cA, lane);
         const uint32_t totA = __shfl_sync(0xffffffffu, iA, 31);
@@ -1160,56 +1163,58 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
             sa[(lane + 32) * G + g] = pB[g] * scB;
             wm[g] = fmaf(pA[g], mnA, fmaf(pB[g], mnB, wm[g]));
         }
-        // decode V slices A (token lane) and B (token lane+32) into the tile
-        const uint32_t bit0 = (vofs + V_HDR) * 8, slot = smem_u32(vring + sl * stage_v);
+        // decode V slices A (token lane) and B (token lane+32) half by half:
+        // channels 0..63 into the half-tile, GEMV, channels 64..127, GEMV
+        const uint32_t bit0 = (vofs + V_HDR) * 8, slot = smem_u32(vring + vsl * stage_v);
         Cursor2 cc[2];
         cursor2_init(cc[0], slot, bit0 + iA - cA);
         cursor2_init(cc[1], slot, bit0 + totA + iB - cB);
         const uint32_t p0A = cc[0].p, p0B = cc[1].p;
         const uint32_t rowA = tile_s + lane * kTileRow, rowB = tile_s + (lane + 32) * kTileRow;
-#pragma unroll 1
-        for (int c5 = 0; c5 < 65; c5 += 5) {
-            cursor2_reload(cc[0]);
-            cursor2_reload(cc[1]);
+        const float2 magic = make_float2(-8388608.f, -8388608.f);
 #pragma unroll
-            for (int t = 0; t < 5; ++t) {
-                const int c2 = c5 + t;
-                if (c2 < D / 2) {
-                    const uint32_t eA = lds32(lut_s + ((cc[0].hi >> 20) << 2));
-                    cc[0].hi = __funnelshift_l(cc[0].lo, cc[0].hi, eA);
-                    cc[0].lo = __funnelshift_l(0u, cc[0].lo, eA);
-                    cc[0].p += eA;
-                    const uint32_t eB = lds32(lut_s + ((cc[1].hi >> 20) << 2));
-                    cc[1].hi = __funnelshift_l(cc[1].lo, cc[1].hi, eB);
-                    cc[1].lo = __funnelshift_l(0u, cc[1].lo, eB);
-                    cc[1].p += eB;
-                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(rowA + 2 * c2), "h"((unsigned short)(eA >> 16)));
-                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(rowB + 2 * c2), "h"((unsigned short)(eB >> 16)));
+        for (int half = 0; half < 2; ++half) {
+            // 32 pair steps; reload every 5 (the cadence restarts at each half)
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+                if (t % 5 == 0) {
+                    cursor2_reload(cc[0]);
+                    cursor2_reload(cc[1]);
+                }
+                const uint32_t eA = lds32(lut_s + ((cc[0].hi >> 20) << 2));
+                cc[0].hi = __funnelshift_l(cc[0].lo, cc[0].hi, eA);
+                cc[0].lo = __funnelshift_l(0u, cc[0].lo, eA);
+                cc[0].p += eA;
+                const uint32_t eB = lds32(lut_s + ((cc[1].hi >> 20) << 2));
+                cc[1].hi = __funnelshift_l(cc[1].lo, cc[1].hi, eB);
+                cc[1].lo = __funnelshift_l(0u, cc[1].lo, eB);
+                cc[1].p += eB;
+                asm volatile("st.shared.u16 [%0], %1;" ::"r"(rowA + 2 * t), "h"((unsigned short)(eA >> 16)));
+                asm volatile("st.shared.u16 [%0], %1;" ::"r"(rowB + 2 * t), "h"((unsigned short)(eB >> 16)));
+            }
+            __syncwarp();
+            if (VS == 1 && half == 1 && lane == 0 && j + 1 < n) issue(true, j + 1);  // slot consumed
+            // GEMV over the 64 tokens: lane owns channels 64*half + 2*lane, +1
+#pragma unroll 4
+            for (int t = 0; t < BS; ++t) {
+                uint32_t w;
+                asm volatile(KVC_LD_SHARED ".u16 %0, [%1];" : "=r"(w) : "r"(tile_s + t * kTileRow + 2 * lane));
+                const float2 f01 = __fadd2_rn(make_float2(sym_hi_byte(w, 0x7650), sym_hi_byte(w, 0x7651)), magic);
+                float av[G];
+                lds_vec<G>(sa_s + 4 * G * t, av);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float2 a2 = make_float2(av[g], av[g]);
+                    float2 ac = make_float2(acc[g][2 * half], acc[g][2 * half + 1]);
+                    ac = __ffma2_rn(f01, a2, ac);
+                    acc[g][2 * half] = ac.x;
+                    acc[g][2 * half + 1] = ac.y;
                 }
             }
+            __syncwarp();
         }
         bad |= (((cc[0].p - p0A) & 0xFFFFu) != cA) | (((cc[1].p - p0B) & 0xFFFFu) != cB);
-        __syncwarp();
-        // GEMV: lane owns channels 4*lane .. 4*lane+3 over the chunk's 64 tokens
-        const float2 magic = make_float2(-8388608.f, -8388608.f);
-#pragma unroll 4
-        for (int t = 0; t < BS; ++t) {
-            const uint32_t w = lds32(tile_s + t * kTileRow + 4 * lane);
-            const float2 f01 = __fadd2_rn(make_float2(sym_hi_byte(w, 0x7650), sym_hi_byte(w, 0x7651)), magic);
-            const float2 f23 = __fadd2_rn(make_float2(sym_hi_byte(w, 0x7652), sym_hi_byte(w, 0x7653)), magic);
-            float av[G];
-            lds_vec<G>(sa_s + 4 * G * t, av);
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float a = av[g];
-                acc[g][0] = fmaf(a, f01.x, acc[g][0]);
-                acc[g][1] = fmaf(a, f01.y, acc[g][1]);
-                acc[g][2] = fmaf(a, f23.x, acc[g][2]);
-                acc[g][3] = fmaf(a, f23.y, acc[g][3]);
-            }
-        }
-        __syncwarp();
-        if (lane == 0 && j + 2 < n) issue(true, j + 2);
+        if (VS == 2 && lane == 0 && j + 2 < n) issue(true, j + 2);
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) kvc_set_err(err, KVC_ERR_CODEC);
     __syncthreads();  // K warps done: their region is scratch
@@ -1218,7 +1223,10 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     for (int g = 0; g < G; ++g) {
         const float l = kvc_warp_sum(lsum[g]), w2 = kvc_warp_sum(wm[g]);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) wp[g].o[4 * lane + k] = acc[g][k] + w2;
+        wp[g].o[2 * lane] = acc[g][0] + w2;
+        wp[g].o[2 * lane + 1] = acc[g][1] + w2;
+        wp[g].o[64 + 2 * lane] = acc[g][2] + w2;
+        wp[g].o[65 + 2 * lane] = acc[g][3] + w2;
         if (lane == 0) {
             wp[g].m = m[g];
             wp[g].l = l;
@@ -1556,13 +1564,16 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         // decode-once GQA kernel (pair LUT: every code <= 6 bits)
         if (mode != 1 || max_chunks == 0)
             return kvc_fail(KVC_ERR_CONFIG, "fused GQA needs codes <= 6 bits and a compressed region");
-        // pairs per CTA (one CTA per SM): 6 when the staging fits, else 4
-        const size_t pp = (size_t)gqa_per_pair(stage_k, stage_v, group);
-        int np = 6;
+        // pairs per CTA (one CTA per SM): 8 with a 1-slot V ring when the staging
+        // fits, else 6 or 4 with 2-slot V rings (KVC_GQA_PAIRS=4|6 caps it)
+        const size_t lim = 227 * 1024 - 2 * 16384 - 256;
+        int np = 8;
         const char *npenv = getenv("KVC_GQA_PAIRS");
-        if (npenv && npenv[0] == '4') np = 4;
-        if (np * pp + 2 * 16384 + 256 > 227 * 1024) np = 4;
-        const size_t g_smem = np * pp;
+        if (npenv && (npenv[0] == '4' || npenv[0] == '6')) np = npenv[0] - '0';
+        if (np == 8 && 8 * (size_t)gqa_per_pair(stage_k, stage_v, group, 1) > lim) np = 6;
+        if (np == 6 && 6 * (size_t)gqa_per_pair(stage_k, stage_v, group, 2) > lim) np = 4;
+        const int vsl = np == 8 ? 1 : 2;
+        const size_t g_smem = np * (size_t)gqa_per_pair(stage_k, stage_v, group, vsl);
         if (g_smem + 2 * 16384 + 256 > 227 * 1024)
             return kvc_fail(KVC_ERR_CONFIG, "block extents too large for GQA staging");
         const int g_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H, 1, np);
@@ -1570,17 +1581,17 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         if (sizeof(Partial) * (size_t)n_seqs * H * group * g_splits > workspace_bytes)
             return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
         dim3 g3(g_splits, H, n_seqs);
-#define KVC_LAUNCH_GQA(GG, NPP)                                                                     \
+#define KVC_LAUNCH_GQA(GG, NPP, VSS)                                                                   \
     do {                                                                                            \
-        KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_gqa_kernel<GG, NPP>,                           \
+        KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_gqa_kernel<GG, NPP, VSS>,                         \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem)); \
-        fused_attn_gqa_kernel<GG, NPP><<<g3, NPP * 64, g_smem, s>>>(                                \
+        fused_attn_gqa_kernel<GG, NPP, VSS><<<g3, NPP * 64, g_smem, s>>>(                                \
             seqs_dev, H, q_dev, part, g_cps, g_splits, stage_k, stage_v, err_dev);                  \
     } while (0)
         if (group == 2) {
-            if (np == 6) KVC_LAUNCH_GQA(2, 6); else KVC_LAUNCH_GQA(2, 4);
+            if (np == 8) KVC_LAUNCH_GQA(2, 8, 1); else if (np == 6) KVC_LAUNCH_GQA(2, 6, 2); else KVC_LAUNCH_GQA(2, 4, 2);
         } else {
-            if (np == 6) KVC_LAUNCH_GQA(4, 6); else KVC_LAUNCH_GQA(4, 4);
+            if (np == 8) KVC_LAUNCH_GQA(4, 8, 1); else if (np == 6) KVC_LAUNCH_GQA(4, 6, 2); else KVC_LAUNCH_GQA(4, 4, 2);
         }
 #undef KVC_LAUNCH_GQA
         int st = kvc_check_launch("fused_attn_gqa_kernel");
