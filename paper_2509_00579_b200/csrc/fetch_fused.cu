@@ -1222,7 +1222,6 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const float l = kvc_warp_sum(lsum[g]), w2 = kvc_warp_sum(wm[g]);
-#pragma unroll
         wp[g].o[2 * lane] = acc[g][0] + w2;
         wp[g].o[2 * lane + 1] = acc[g][1] + w2;
         wp[g].o[64 + 2 * lane] = acc[g][2] + w2;
