@@ -280,7 +280,7 @@ def main():
                                  out=outs[layer])
         else:
             outs[layer] = kv.attention_gqa(states[layer], q[layer], G, desc_cache=caches[layer],
-                                           workspace=ws)
+                                           workspace=ws, check=False)
 
     def step():
         for layer in range(L):
@@ -409,13 +409,13 @@ def main():
                                       "buffer, one kvc_store_append launch"},
             "roofline": {"bound": "hbm", "achieved": round(ach, 2), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
-                         "traffic": _ncu_traffic(), "peak_kind": peak_kind,
-                         "kernel": "fused_attn_kernel (+combine), one layer launch, "
-                                   "compressed bytes"},
+                         "traffic": _ncu_traffic(args.config), "peak_kind": peak_kind,
+                         "kernel": ("fused_attn_ws_kernel" if G == 1 else "fused_attn_gqa_kernel")
+                                   + " (+combine), one layer launch, compressed bytes"},
             "e2e": {"value": round(e2e_val, 2), "unit": "GB/s (equivalent fp16 KV)",
                     "h2d_bytes_per_step": int(L * B * hl * G * 128 * 4),
                     "d2h_bytes_per_step": int(L * B * hl * G * 128 * 4)},
-            "gpu_launches": int(args.steps * L * 2 * G),
+            "gpu_launches": int(args.steps * L * 2),  # fused kernel + combine per layer
             "clocks": clk.summary(),
         }
         if cpu:
@@ -465,11 +465,12 @@ def quant_sweep(kv, torch, device, T, H, B):
     return rows
 
 
-def _ncu_traffic():
-    """dram read+write bytes per fused-kernel launch from the committed ncu
-    --set full capture (profiles/fused_ncu_latest.json), if present."""
+def _ncu_traffic(config):
+    """dram read+write bytes per fused-kernel launch (one layer of this config)
+    from the committed ncu --set full capture profiles/fused_ncu_cfg<N>.json
+    (made by tools/fetch_variants.py --iters 1 under ncu), if present."""
     try:
-        with open(os.path.join(ROOT, "profiles", "fused_ncu_latest.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", f"fused_ncu_cfg{config}.json")) as fh:
             d = json.load(fh)
         def gb(v):
             num, unit = v.split()[0], v.split()[1] if len(v.split()) > 1 else "byte"

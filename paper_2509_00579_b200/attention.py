@@ -248,13 +248,15 @@ def multistage_attention(state: LayerCacheState, q,
 
 def attention_gqa(states: Sequence[LayerCacheState], q: torch.Tensor, group: int,
                   desc_cache: Optional["_BatchDesc"] = None,
-                  workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+                  workspace: Optional[torch.Tensor] = None, check: bool = True) -> torch.Tensor:
     """Grouped-query decode attention: q [B, H_kv*group, D], query head
     h*group+j reads KV head h (Llama-3 layout).  The reference has no GQA
     (SPEC non-goal; its oracle runs one attention_step per group member).
     Groups of 2 or 4 with codes <= 6 bits run the decode-once GQA kernel
     (each K/V block decoded once for all members); otherwise one fused
-    launch per member."""
+    launch per member.  check=True synchronises and raises the device error
+    word (CodecError on a corrupt stream); check=False leaves the launch
+    asynchronous (the bench's decode loop)."""
     B, HQ, D = q.shape
     H = HQ // group
     dev = q.device
@@ -275,12 +277,16 @@ def attention_gqa(states: Sequence[LayerCacheState], q: torch.Tensor, group: int
                                None, 0, workspace.data_ptr(), workspace.numel(), err.data_ptr(),
                                _stream(dev))
         if st == _lib.KVC_OK:
+            if check:
+                _lib.raise_device_error(int(err.item()), "attention_gqa")
             return out
     qv = q.view(B, H, group, D)
     ov = out.view(B, H, group, D)
     for j in range(group):
         o, _, err = attention_batched(states, qv[:, :, j].contiguous(), desc_cache=cache,
                                       workspace=workspace)
+        if check:
+            _lib.raise_device_error(int(err.item()), "attention_gqa")
         ov[:, :, j] = o
     return out
 

@@ -363,3 +363,42 @@ def test_fused_gqa_matches_per_member_steps(kv, group):
             r = kv.attention_step(st, q[0].reshape(H, group, 128)[:, j])
             assert max_relative_error(out[0].view(H, group, 128)[:, j].cpu().numpy(),
                                       r.out.cpu().numpy()) <= 1e-5
+
+
+def test_fused_gqa_ragged_batch_multi_split(kv):
+    """Two sequences of different lengths (one with buffered tokens) in one
+    decode-once GQA launch, long enough for several context splits per head."""
+    H, G = 2, 4
+    states, qs = [], []
+    for b, (ctx, extra) in enumerate(((9000, 0), (20000, 45))):
+        k = kv.generate_synthetic(kv.SyntheticSpec(ctx + extra, H, 128, seed=50 + b)).values
+        v = kv.generate_synthetic(kv.SyntheticSpec(ctx + extra, H, 128, seed=60 + b)).values
+        st = kv.LayerCacheState.prefill(kv.CacheTensor(k[:ctx].astype(np.float16)),
+                                        kv.CacheTensor(v[:ctx].astype(np.float16)),
+                                        kv.QuantConfig(kv.QuantMode.K_BLOCK),
+                                        kv.QuantConfig(kv.QuantMode.V_TOKEN))
+        for t in range(ctx, ctx + extra):
+            st.append_token(k[t], v[t])
+        states.append(st)
+    q = np.random.default_rng(7).standard_normal((2, H * G, 128), dtype=np.float32)
+    out = kv.attention_gqa(states, torch.from_numpy(q).cuda(), G)
+    for b, st in enumerate(states):
+        for j in range(G):
+            r = kv.attention_step(st, q[b].reshape(H, G, 128)[:, j])
+            assert max_relative_error(out[b].view(H, G, 128)[:, j].cpu().numpy(),
+                                      r.out.cpu().numpy()) <= 1e-5
+
+
+def test_fused_gqa_corrupt_stream_raises(kv):
+    H, G = 2, 4
+    k = kv.generate_synthetic(kv.SyntheticSpec(1024, H, 128, seed=70)).values.astype(np.float16)
+    v = kv.generate_synthetic(kv.SyntheticSpec(1024, H, 128, seed=71)).values.astype(np.float16)
+    st = kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v),
+                                    kv.QuantConfig(kv.QuantMode.K_BLOCK),
+                                    kv.QuantConfig(kv.QuantMode.V_TOKEN))
+    raw = st.v_arena.raw_tensor()
+    raw[6] ^= 1  # slice 0 bit count of V block 0
+    st._desc_key = None
+    q = torch.randn((1, H * G, 128), device="cuda")
+    with pytest.raises(kv.CodecError):
+        kv.attention_gqa([st], q, G)
