@@ -53,7 +53,9 @@ struct StoreParams {
     int *err;
 };
 
-__device__ __forceinline__ uint8_t code_f64(float x, float lo, float scale) {
+// out of line: the exact path must not be inlined at every unrolled call site
+// (ptxas then keeps the hot loop small: pass B 1.31 -> 1.17 ms on a config-2 slice)
+__device__ __noinline__ uint8_t code_f64(float x, float lo, float scale) {
     const double s64 = (double)scale;
     const double d = __dsub_rn((double)x, (double)lo);
     double t = __dmul_rn(d, __drcp_rn(s64));
@@ -79,6 +81,15 @@ __device__ __forceinline__ uint8_t code_fast(float x, float lo, float scale, flo
     return code_f64(x, lo, scale);
 }
 
+__device__ __noinline__ float code_clamped_f64(float x, float lo, float scale) {
+    const double s64 = (double)scale;
+    const double d = __dsub_rn((double)x, (double)lo);
+    double tt = __ddiv_rn(d, s64);
+    double f = floor(tt);
+    if (__dsub_rn(tt, f) >= 0.5) f += 1.0;
+    return (float)fmin(fmax(f, -1.0), 1024.0);
+}
+
 // K_CHANNEL: fixed whole-context ranges, so t may fall outside [0, max_code];
 // round half up then clip (quantizer.py:137-140).
 __device__ __forceinline__ uint8_t code_clamped(float x, float lo, float scale, float r32,
@@ -90,12 +101,7 @@ __device__ __forceinline__ uint8_t code_clamped(float x, float lo, float scale, 
         const float c = floorf(t);
         code = c + ((t - c) >= 0.5f ? 1.f : 0.f);
     } else {
-        const double s64 = (double)scale;
-        const double d = __dsub_rn((double)x, (double)lo);
-        double tt = __ddiv_rn(d, s64);
-        double f = floor(tt);
-        if (__dsub_rn(tt, f) >= 0.5) f += 1.0;
-        code = (float)fmin(fmax(f, -1.0), 1024.0);
+        code = code_clamped_f64(x, lo, scale);
     }
     code = fminf(fmaxf(code, 0.f), (float)clamp_max);
     return (uint8_t)(int)code;
