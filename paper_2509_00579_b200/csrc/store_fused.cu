@@ -107,6 +107,71 @@ __device__ __forceinline__ uint8_t code_clamped(float x, float lo, float scale, 
     return (uint8_t)(int)code;
 }
 
+// code_fast with the scale read only on the (rare) exact path
+__device__ __forceinline__ uint32_t code_fast_p(float x, float lo, float r32, const float *scale_p) {
+    const float t = __fmul_rn(__fsub_rn(x, lo), r32);
+    if (t < 300.f) {
+        const float c = floorf(t);
+        const float f = t - c;
+        if (fabsf(f - 0.5f) > (1.0f / 4096.0f)) return (uint32_t)(int)(c + (f >= 0.5f ? 1.f : 0.f));
+    }
+    const float sc = *scale_p;
+    return sc > 0.f ? code_f64(x, lo, sc) : 0u;
+}
+
+// Hot shape (head_dim 128, block 64): thread -> column pair (2j, 2j+1), rows
+// q, q+4, ..., mode specialised so the unit parameters are hoisted (K: per
+// column, loaded once) or broadcast (V: per row, one warp shares the row).
+// Pass B stores the code pair with one 16-bit store; pass A counts them.
+template <typename T, bool ENCODE, int MODE>
+__device__ __forceinline__ void quantize_hot(const T *stage, uint8_t *codes, const float *u_lo,
+                                             const float *u_sc, const float *u_r, int max_code,
+                                             bool small_alpha, uint32_t *whist, uint32_t *sh_hist,
+                                             int tid) {
+    constexpr int D = 128, BS = 64;
+    const int j = tid & 63, q = tid >> 6;  // column pair, row phase (0..3)
+    const int c0 = 2 * j;
+    float klo0 = 0.f, klo1 = 0.f, kr0 = 0.f, kr1 = 0.f;
+    if (MODE != KVC_V_TOKEN) {
+        klo0 = u_lo[c0]; klo1 = u_lo[c0 + 1];
+        kr0 = u_r[c0]; kr1 = u_r[c0 + 1];
+    }
+#pragma unroll 4
+    for (int k = 0; k < BS / 4; ++k) {
+        const int r = q + 4 * k;
+        float x0, x1;
+        if constexpr (sizeof(T) == 2) {
+            const __half2 h = *reinterpret_cast<const __half2 *>(stage + r * D + c0);
+            const float2 f = __half22float2(h);
+            x0 = f.x; x1 = f.y;
+        } else {
+            const float2 f = *reinterpret_cast<const float2 *>(stage + r * D + c0);
+            x0 = f.x; x1 = f.y;
+        }
+        uint32_t a, b;
+        if (MODE == KVC_V_TOKEN) {
+            const float lo = u_lo[r], rr = u_r[r];
+            a = code_fast_p(x0, lo, rr, &u_sc[r]);
+            b = code_fast_p(x1, lo, rr, &u_sc[r]);
+        } else if (MODE == KVC_K_CHANNEL) {
+            a = code_clamped(x0, klo0, u_sc[c0], kr0, max_code);
+            b = code_clamped(x1, klo1, u_sc[c0 + 1], kr1, max_code);
+        } else {
+            a = code_fast_p(x0, klo0, kr0, &u_sc[c0]);
+            b = code_fast_p(x1, klo1, kr1, &u_sc[c0 + 1]);
+        }
+        if (ENCODE) {
+            *reinterpret_cast<uint16_t *>(codes + r * D + c0) = (uint16_t)(a | (b << 8));
+        } else if (small_alpha) {
+            atomicAdd(&whist[a], 1u);
+            atomicAdd(&whist[b], 1u);
+        } else {
+            atomicAdd(&sh_hist[a], 1u);
+            atomicAdd(&sh_hist[b], 1u);
+        }
+    }
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -246,7 +311,17 @@ store_kernel(StoreParams P, int stage_words) {
         if (small_alpha) atomicAdd(&whist[code], 1u);
         else atomicAdd(&sh_hist[code], 1u);
     };
-    if (D <= kThreads) {
+    if constexpr (DT == 128 && BST == 64) {
+        if (is_kc)
+            quantize_hot<T, ENCODE, KVC_K_CHANNEL>(stage, codes, u_lo, u_sc, u_r, S.max_code,
+                                                   small_alpha, whist, sh_hist, tid);
+        else if (is_v)
+            quantize_hot<T, ENCODE, KVC_V_TOKEN>(stage, codes, u_lo, u_sc, u_r, S.max_code,
+                                                 small_alpha, whist, sh_hist, tid);
+        else
+            quantize_hot<T, ENCODE, KVC_K_BLOCK>(stage, codes, u_lo, u_sc, u_r, S.max_code,
+                                                 small_alpha, whist, sh_hist, tid);
+    } else if (D <= kThreads) {
         // thread -> fixed column c (one division per thread, none per element)
         const int rstep = kThreads / D;
         const int c = tid % D, r0 = tid / D;
