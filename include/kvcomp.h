@@ -183,6 +183,33 @@ int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtype, long row
                      size_t workspace_bytes, void *stream);
 size_t kvc_store_workspace_bytes(int n_chunks, int H, int D, int bs);
 
+/* Prefill without the look-back (kvcache.py:110-145; byte-identical arenas
+ * to kvc_store_hist + kvc_store_append).  For alphabets < 32 codes
+ * (kvc_store_prefill_supported):
+ *   kvc_store_hist_blocks  pass A, also writing per-block code histograms
+ *                          blk_hist_dev [2][n_chunks*H][32] u16 (K then V);
+ *   kvc_store_prefill      block sizes from those histograms and the code
+ *                          lengths, one exclusive scan -> arena offsets in
+ *                          block_index order, then pass B writes every block
+ *                          at its offset.  workspace >= 64 bytes. */
+int kvc_store_prefill_supported(int bs, int D, double rel_k, double rel_v);
+size_t kvc_store_blk_hist_bytes(int n_chunks, int H);
+int kvc_store_hist_blocks(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
+                          int n_chunks, int H, int D, int bs, int k_mode, double rel_k,
+                          double rel_v, const float *k_ranges_dev, uint64_t *hist_dev,
+                          uint16_t *blk_hist_dev, void *stream);
+int kvc_store_prefill(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
+                      int n_chunks, int H_local, int H_total, int head_base, int D, int bs,
+                      int k_mode, double rel_k, double rel_v, const float *k_ranges_dev,
+                      uint32_t chunk_base,
+                      const kvc_codebook_dev *k_cb_dev, int k_max_len,
+                      const kvc_codebook_dev *v_cb_dev, int v_max_len, uint8_t *k_arena_dev,
+                      uint64_t k_capacity, uint32_t *k_offsets_dev,
+                      kvc_arena_counters *k_counters_dev, uint8_t *v_arena_dev,
+                      uint64_t v_capacity, uint32_t *v_offsets_dev,
+                      kvc_arena_counters *v_counters_dev, const uint16_t *blk_hist_dev,
+                      void *workspace_dev, size_t workspace_bytes, void *stream);
+
 /* ---------------------------------------------------------------- */
 /* Fetch — replaces attention.py:59-188 and kvcache.py:182-212        */
 /* ---------------------------------------------------------------- */

@@ -51,6 +51,12 @@ struct StoreParams {
     int n_chunks, H_local, H_total, head_base, D, bs;
     uint32_t chunk_base;
     int *err;
+    // prefill fast path (null otherwise): pass A also writes per-block code
+    // histograms blk_hist [2][nb][32] u16; pass B with nb0 != null takes block b
+    // = blockIdx.x and its arena offset from offsets[nb0[t] + b] (written by
+    // store_offsets_kernel): no tickets, no look-back, no counter updates.
+    uint16_t *blk_hist;
+    const unsigned long long *nb0;
 };
 
 // out of line: the exact path must not be inlined at every unrolled call site
@@ -221,7 +227,8 @@ store_kernel(StoreParams P, int stage_words) {
     const long nb = (long)P.n_chunks * P.H_local;
 
     // logical block id in scheduling order (look-back needs predecessors running)
-    if (tid == 0) sh_b = ENCODE ? (long)atomicAdd(&S.acc[0], 1ull) : (long)blockIdx.x;
+    const bool prescanned = ENCODE && P.nb0 != nullptr;
+    if (tid == 0) sh_b = (ENCODE && !prescanned) ? (long)atomicAdd(&S.acc[0], 1ull) : (long)blockIdx.x;
     if (!ENCODE)
         for (int i = tid; i < 256; i += kThreads) sh_hist[i] = 0;
     if (ENCODE)
@@ -359,6 +366,7 @@ store_kernel(StoreParams P, int stage_words) {
 #pragma unroll
                 for (int w = 0; w < kWarps; ++w) v += sh_whist[w][tid];
                 if (v) atomicAdd(&S.hist[tid], (unsigned long long)v);
+                if (P.blk_hist) P.blk_hist[((size_t)blockIdx.y * nb + b) * 32 + tid] = (uint16_t)v;
             }
         } else {
             for (int i = tid; i < 256; i += kThreads)
@@ -449,6 +457,17 @@ store_kernel(StoreParams P, int stage_words) {
             }
         }
         if (nacc) img_or_bits32(img, p, (uint32_t)(accb >> 32));
+    }
+
+    if (prescanned) {
+        if (bad) atomicCAS(&S.counters->err, 0, (int)KVC_ERR_CODEC);
+        __syncthreads();
+        const uint64_t off = S.offsets[P.nb0[blockIdx.y] + b];
+        if (off + size <= S.capacity && off + size <= 0xFFFFFFFFull) {
+            uint32_t *dst = reinterpret_cast<uint32_t *>(S.arena + off);
+            for (int i = tid; i < (int)(size >> 2); i += kThreads) dst[i] = __byte_perm(img[i], 0, 0x0123);
+        }
+        return;
     }
 
     // ---- decoupled look-back over block sizes (block_index order) ------
@@ -664,5 +683,219 @@ extern "C" int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtyp
     P.bs = bs;
     P.chunk_base = chunk_base;
     P.err = reinterpret_cast<int *>(w + 2 * per);
+    return launch_store(P, x_dtype, true, max_len, s);
+}
+
+// ---------------------------------------------------------------------------
+// Prefill fast path: block sizes from pass A's per-block histograms and the
+// code lengths (size = header + ceil(bits/8), padded to 4: codec.py:229-244),
+// exclusive scan in block_index order -> arena offsets (codec.py:308-326),
+// counters update.  One 1024-thread CTA per tensor (blockIdx.y).
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(1024)
+store_offsets_kernel(StoreParams P, unsigned long long *nb0) {
+    const StoreTensor S = P.t[blockIdx.y];
+    const long nb = (long)P.n_chunks * P.H_local;
+    const uint16_t *bh = P.blk_hist + (size_t)blockIdx.y * nb * 32;
+    const int n_units = S.mode == KVC_V_TOKEN ? P.bs : P.D;
+    const uint32_t hdr = kvc_header_bytes(P.bs, n_units);
+    __shared__ uint32_t len[32];
+    __shared__ unsigned long long wsum[32];
+    __shared__ unsigned long long carry_s;
+    __shared__ unsigned long long r_bits[32], r_bytes[32];
+    __shared__ uint32_t r_mx[32];
+    __shared__ int r_bad;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid < 32) len[tid] = S.cb->lengths[tid];
+    if (tid == 0) {
+        carry_s = 0;
+        r_bad = 0;
+    }
+    __syncthreads();
+    const uint64_t cursor = S.counters->cursor, n0 = S.counters->n_blocks;
+    unsigned long long pbits = 0, pbytes = 0;
+    uint32_t mx = 0;
+    bool bad = false;
+    for (long t0 = 0; t0 < nb; t0 += 1024) {
+        const long b = t0 + tid;
+        uint32_t size = 0;
+        if (b < nb) {
+            const uint4 *h4 = reinterpret_cast<const uint4 *>(bh + (size_t)b * 32);
+            uint32_t bits = 0;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const uint4 u = h4[qq];
+                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int s0 = 8 * qq + 2 * k;
+                    const uint32_t c0 = w[k] & 0xFFFFu, c1 = w[k] >> 16;
+                    bad |= (c0 && !len[s0]) || (c1 && !len[s0 + 1]);
+                    bits += c0 * len[s0] + c1 * len[s0 + 1];
+                }
+            }
+            const uint32_t by = (bits + 7) / 8;
+            size = (hdr + by + 3) & ~3u;
+            pbits += bits;
+            pbytes += by;
+            mx = max(mx, size);
+        }
+        unsigned long long v = size;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        if (lane == 31) wsum[warp] = v;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long w = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            wsum[lane] = w;
+        }
+        __syncthreads();
+        const unsigned long long carry = carry_s;
+        const unsigned long long excl = carry + (warp ? wsum[warp - 1] : 0ull) + v - size;
+        if (b < nb) S.offsets[n0 + b] = (uint32_t)(cursor + excl);
+        __syncthreads();
+        if (tid == 0) carry_s = carry + wsum[31];
+        __syncthreads();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        pbits += __shfl_xor_sync(0xffffffffu, pbits, o);
+        pbytes += __shfl_xor_sync(0xffffffffu, pbytes, o);
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (bad) r_bad = 1;
+    if (lane == 0) {
+        r_bits[warp] = pbits;
+        r_bytes[warp] = pbytes;
+        r_mx[warp] = mx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long tb = 0, ty = 0;
+        uint32_t m = 0;
+        for (int w = 0; w < 32; ++w) {
+            tb += r_bits[w];
+            ty += r_bytes[w];
+            m = max(m, r_mx[w]);
+        }
+        nb0[blockIdx.y] = n0;
+        const unsigned long long total = carry_s;
+        kvc_arena_counters *ct = S.counters;
+        if (r_bad) {
+            if (!ct->err) ct->err = KVC_ERR_CODEC;
+        } else if (cursor + total > S.capacity || cursor + total > 0xFFFFFFFFull) {
+            if (!ct->err) ct->err = KVC_ERR_ARENA_FULL;
+        } else {
+            ct->cursor = cursor + total;
+            ct->n_blocks = n0 + (uint64_t)nb;
+            ct->payload_bits += tb;
+            ct->payload_bytes += ty;
+            if (m > ct->max_extent) ct->max_extent = m;
+        }
+    }
+}
+}  // namespace
+
+extern "C" int kvc_store_prefill_supported(int bs, int D, double rel_k, double rel_v) {
+    return kvc_store_supported(bs, D, 1) && ceil(1.0 / rel_k) < 32 && ceil(1.0 / rel_v) < 32;
+}
+
+extern "C" size_t kvc_store_blk_hist_bytes(int n_chunks, int H) {
+    return (size_t)2 * (size_t)(n_chunks > 0 ? n_chunks : 1) * H * 32 * sizeof(uint16_t);
+}
+
+extern "C" int kvc_store_hist_blocks(const void *k_dev, const void *v_dev, int x_dtype,
+                                     long row_stride, int n_chunks, int H, int D, int bs,
+                                     int k_mode, double rel_k, double rel_v,
+                                     const float *k_ranges_dev, uint64_t *hist_dev,
+                                     uint16_t *blk_hist_dev, void *stream) {
+    if (k_mode != KVC_K_BLOCK && k_mode != KVC_K_CHANNEL) return kvc_fail(KVC_ERR_CONFIG, "bad K mode");
+    if (k_mode == KVC_K_CHANNEL && !k_ranges_dev)
+        return kvc_fail(KVC_ERR_CONFIG, "K_CHANNEL quantization requires whole-context channel_ranges");
+    if (!kvc_store_prefill_supported(bs, D, rel_k, rel_v) || !blk_hist_dev)
+        return kvc_fail(KVC_ERR_CONFIG, "shape / alphabet not covered by the prefill fast path");
+    if (n_chunks == 0) return KVC_OK;
+    StoreParams P{};
+    P.t[0].x = k_dev;
+    P.t[0].mode = k_mode;
+    P.t[0].ranges = k_ranges_dev;
+    P.t[0].rel = rel_k;
+    P.t[0].hist = reinterpret_cast<unsigned long long *>(hist_dev);
+    P.t[0].max_code = (int)ceil(1.0 / rel_k);
+    P.t[1].max_code = (int)ceil(1.0 / rel_v);
+    P.t[1].x = v_dev;
+    P.t[1].mode = KVC_V_TOKEN;
+    P.t[1].rel = rel_v;
+    P.t[1].hist = reinterpret_cast<unsigned long long *>(hist_dev) + 256;
+    P.row_stride = row_stride;
+    P.n_chunks = n_chunks;
+    P.H_local = H;
+    P.H_total = H;
+    P.D = D;
+    P.bs = bs;
+    P.blk_hist = blk_hist_dev;
+    return launch_store(P, x_dtype, false, 1, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int kvc_store_prefill(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
+                                 int n_chunks, int H_local, int H_total, int head_base, int D,
+                                 int bs, int k_mode, double rel_k, double rel_v,
+                                 const float *k_ranges_dev, uint32_t chunk_base,
+                                 const kvc_codebook_dev *k_cb_dev, int k_max_len,
+                                 const kvc_codebook_dev *v_cb_dev, int v_max_len,
+                                 uint8_t *k_arena_dev, uint64_t k_capacity, uint32_t *k_offsets_dev,
+                                 kvc_arena_counters *k_counters_dev, uint8_t *v_arena_dev,
+                                 uint64_t v_capacity, uint32_t *v_offsets_dev,
+                                 kvc_arena_counters *v_counters_dev, const uint16_t *blk_hist_dev,
+                                 void *workspace_dev, size_t workspace_bytes, void *stream) {
+    if (n_chunks == 0) return KVC_OK;
+    if (k_mode != KVC_K_BLOCK && k_mode != KVC_K_CHANNEL) return kvc_fail(KVC_ERR_CONFIG, "bad K mode");
+    if (k_mode == KVC_K_CHANNEL && !k_ranges_dev)
+        return kvc_fail(KVC_ERR_CONFIG, "K_CHANNEL quantization requires whole-context channel_ranges");
+    const int max_len = k_max_len > v_max_len ? k_max_len : v_max_len;
+    if (!kvc_store_prefill_supported(bs, D, rel_k, rel_v) || !kvc_store_supported(bs, D, max_len) ||
+        !blk_hist_dev)
+        return kvc_fail(KVC_ERR_CONFIG, "shape / alphabet not covered by the prefill fast path");
+    if (workspace_bytes < 64) return kvc_fail(KVC_ERR_CONFIG, "store workspace too small");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    StoreParams P{};
+    for (int t = 0; t < 2; ++t) {
+        StoreTensor &T = P.t[t];
+        T.x = t ? v_dev : k_dev;
+        T.mode = t ? KVC_V_TOKEN : k_mode;
+        T.rel = t ? rel_v : rel_k;
+        T.max_code = (int)ceil(1.0 / T.rel);
+        T.ranges = t ? nullptr : k_ranges_dev;
+        T.cb = t ? v_cb_dev : k_cb_dev;
+        T.arena = t ? v_arena_dev : k_arena_dev;
+        T.capacity = t ? v_capacity : k_capacity;
+        T.offsets = t ? v_offsets_dev : k_offsets_dev;
+        T.counters = t ? v_counters_dev : k_counters_dev;
+    }
+    P.row_stride = row_stride;
+    P.n_chunks = n_chunks;
+    P.H_local = H_local;
+    P.H_total = H_total;
+    P.head_base = head_base;
+    P.D = D;
+    P.bs = bs;
+    P.chunk_base = chunk_base;
+    P.blk_hist = const_cast<uint16_t *>(blk_hist_dev);
+    unsigned long long *nb0 = static_cast<unsigned long long *>(workspace_dev);  // [2]
+    P.err = reinterpret_cast<int *>(nb0 + 2);
+    KVC_CUDA_TRY(cudaMemsetAsync(P.err, 0, sizeof(int), s));
+    store_offsets_kernel<<<dim3(1, 2), 1024, 0, s>>>(P, nb0);
+    int st = kvc_check_launch("store_offsets_kernel");
+    if (st) return st;
+    P.nb0 = nb0;
     return launch_store(P, x_dtype, true, max_len, s);
 }

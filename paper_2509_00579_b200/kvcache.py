@@ -17,6 +17,8 @@ from __future__ import annotations
 
 from typing import Optional, Tuple
 
+import functools
+
 import numpy as np
 import torch
 
@@ -126,7 +128,21 @@ class LayerCacheState:
             codebooks[0].max_code_length, codebooks[1].max_code_length)))
         hist = torch.zeros(512, dtype=torch.int64, device=kt.device)
         kcodes = kmetas = vcodes = vmetas = None
-        if n_full and codebooks is None and fused:
+        # small alphabets: pass A also records per-block histograms, so pass B takes
+        # its arena offsets from one scan instead of the look-back (store_fused.cu)
+        blk_hist = None
+        if (n_full and codebooks is None and fused
+                and lib.kvc_store_prefill_supported(bs, D, cfg_k.rel_quant_scale,
+                                                    cfg_v.rel_quant_scale)):
+            blk_hist = torch.empty(lib.kvc_store_blk_hist_bytes(n_chunks, H) // 2,
+                                   dtype=torch.int16, device=kt.device)
+            _lib.check(lib.kvc_store_hist_blocks(kt.data_ptr(), vt.data_ptr(), dtype_code(kt),
+                                                 H * D, n_chunks, H, D, bs, cfg_k.mode.abi,
+                                                 cfg_k.rel_quant_scale, cfg_v.rel_quant_scale,
+                                                 ranges_dev.data_ptr() if ranges_dev is not None
+                                                 else None, hist.data_ptr(), blk_hist.data_ptr(),
+                                                 stream), "kvc_store_hist_blocks")
+        elif n_full and codebooks is None and fused:
             # pass A: quantise + histogram only (store_fused.cu)
             _lib.check(lib.kvc_store_hist(kt.data_ptr(), vt.data_ptr(), dtype_code(kt), H * D,
                                           n_chunks, H, D, bs, cfg_k.mode.abi,
@@ -155,7 +171,9 @@ class LayerCacheState:
                  head_base=head_base, head_total=head_total, capacity=capacity,
                  k_channel_ranges=k_channel_ranges)
         if n_full:
-            if st._fused_store:
+            if blk_hist is not None and st._fused_store:
+                st._store(kt, vt, n_chunks, blk_hist=blk_hist)
+            elif st._fused_store:
                 st._store(kt, vt, n_chunks)
             else:
                 if kcodes is None:
@@ -201,9 +219,12 @@ class LayerCacheState:
             arena.note_append(nb, worst)
         self.compressed_tokens += n_chunks * bs
 
-    def _store(self, k_src: torch.Tensor, v_src: torch.Tensor, n_chunks: int) -> None:
-        """Single-launch quantise + encode + append of n_chunks*H blocks per
-        tensor from k_src/v_src rows [0, n_chunks*bs) (store_fused.cu)."""
+    def _store(self, k_src: torch.Tensor, v_src: torch.Tensor, n_chunks: int,
+               blk_hist: Optional[torch.Tensor] = None) -> None:
+        """Quantise + encode + append of n_chunks*H blocks per tensor from
+        k_src/v_src rows [0, n_chunks*bs) (store_fused.cu): one look-back launch
+        (kvc_store_append), or, with the prefill's per-block histograms, the
+        offsets scan + encode (kvc_store_prefill)."""
         bs, H, D = self.cfg_k.block_size, self.head_num, self.head_dim
         lib = _lib.lib()
         nb = n_chunks * H
@@ -212,7 +233,9 @@ class LayerCacheState:
         self.k_arena.reserve(nb, kw)
         self.v_arena.reserve(nb, vw)
         ws = self._workspace(lib.kvc_store_workspace_bytes(n_chunks, H, D, bs))
-        st = lib.kvc_store_append(
+        fn = lib.kvc_store_append if blk_hist is None else functools.partial(
+            _prefill_call, lib.kvc_store_prefill, blk_hist.data_ptr())
+        st = fn(
             k_src.data_ptr(), v_src.data_ptr(), dtype_code(k_src), H * D, n_chunks, H,
             self.head_total, self.head_base, D, bs, self.cfg_k.mode.abi,
             self.cfg_k.rel_quant_scale, self.cfg_v.rel_quant_scale,
@@ -223,7 +246,7 @@ class LayerCacheState:
             self.k_arena.offsets_ptr, self.k_arena.counters_ptr, self.v_arena.buf_ptr,
             self.v_arena.alloc_capacity, self.v_arena.offsets_ptr, self.v_arena.counters_ptr,
             ws.data_ptr(), ws.numel(), torch.cuda.current_stream(self.device).cuda_stream)
-        _lib.check(st, "kvc_store_append")
+        _lib.check(st, "kvc_store_append" if blk_hist is None else "kvc_store_prefill")
         self.k_arena.note_append(nb, kw)
         self.v_arena.note_append(nb, vw)
         self.compressed_tokens += n_chunks * bs
@@ -354,3 +377,9 @@ class LayerCacheState:
             outs.append(out)
         _lib.raise_device_error(int(err.item()), "fetch_dequantized")
         return CacheTensor(outs[0]), CacheTensor(outs[1])
+
+
+def _prefill_call(fn, blk_hist_ptr, *args):
+    """kvc_store_prefill takes kvc_store_append's arguments plus the per-block
+    histograms before the workspace."""
+    return fn(*args[:-3], blk_hist_ptr, *args[-3:])

@@ -43,13 +43,19 @@ def main(ctx=32768, H=40, D=128, reps=10):
         st = kv.LayerCacheState.prefill(k, v, ck, cv, check=False)
     torch.cuda.synchronize()
     t_prefill = (time.perf_counter() - t0) / reps
-    # pass A alone
+    # pass A alone (as prefill runs it: + per-block histograms when supported)
     hist = torch.zeros(512, dtype=torch.int64, device=dev)
+    fast = bool(lib.kvc_store_prefill_supported(64, D, 0.05, 0.15))
+    blk = torch.empty(lib.kvc_store_blk_hist_bytes(nb_chunks, H) // 2, dtype=torch.int16, device=dev)
     a, b = ev(), ev()
     a.record(s)
     for _ in range(reps):
-        lib.kvc_store_hist(k.data_ptr(), v.data_ptr(), 0, H * D, nb_chunks, H, D, 64, 0, 0.05, 0.15,
-                           None, hist.data_ptr(), s.cuda_stream)
+        if fast:
+            lib.kvc_store_hist_blocks(k.data_ptr(), v.data_ptr(), 0, H * D, nb_chunks, H, D, 64, 0,
+                                      0.05, 0.15, None, hist.data_ptr(), blk.data_ptr(), s.cuda_stream)
+        else:
+            lib.kvc_store_hist(k.data_ptr(), v.data_ptr(), 0, H * D, nb_chunks, H, D, 64, 0, 0.05,
+                               0.15, None, hist.data_ptr(), s.cuda_stream)
     b.record(s)
     torch.cuda.synchronize()
     t_a = a.elapsed_time(b) / reps * 1e-3
@@ -61,14 +67,28 @@ def main(ctx=32768, H=40, D=128, reps=10):
         f.k_arena.reserve(nb_chunks * H, nb_chunks * H * 7400)
         f.v_arena.reserve(nb_chunks * H, nb_chunks * H * 7000)
         f._workspace(lib.kvc_store_workspace_bytes(nb_chunks, H, D, 64))
+    fresh2 = [kv.LayerCacheState(H, D, ck, cv, cbs[0], cbs[1], dtype=np.float16, device=dev)
+              for _ in range(reps)]
+    for f in fresh2:
+        f.k_arena.reserve(nb_chunks * H, nb_chunks * H * 7400)
+        f.v_arena.reserve(nb_chunks * H, nb_chunks * H * 7000)
+        f._workspace(lib.kvc_store_workspace_bytes(nb_chunks, H, D, 64))
     torch.cuda.synchronize()
     a.record(s)
     for f in fresh:
-        f._store(k, v, nb_chunks)
+        f._store(k, v, nb_chunks, blk_hist=blk if fast else None)
     b.record(s)
     torch.cuda.synchronize()
     t_b = a.elapsed_time(b) / reps * 1e-3
-    ok = fresh[0].k_arena.snapshot() == st.k_arena.snapshot()
+    # the growing-cache kernel (decoupled look-back) on the same slice, for reference
+    a.record(s)
+    for f in fresh2:
+        f._store(k, v, nb_chunks)
+    b.record(s)
+    torch.cuda.synchronize()
+    t_lb = a.elapsed_time(b) / reps * 1e-3
+    ok = all(f.k_arena.snapshot() == st.k_arena.snapshot() and
+             f.v_arena.snapshot() == st.v_arena.snapshot() for f in (fresh[0], fresh2[0]))
     # append event: 128 tokens x H heads from the f32 buffers (config 4 shape H=32)
     He = 32
     ke = kv.generate_synthetic_device(kv.SyntheticSpec(4096, He, D, seed=2), dev)
@@ -94,6 +114,8 @@ def main(ctx=32768, H=40, D=128, reps=10):
                           "passA_s": t_a, "passA_gbs": in_bytes / t_a / 1e9,
                           "passB_s": t_b, "passB_gbs": in_bytes / t_b / 1e9,
                           "device_gbs": in_bytes / (t_a + t_b) / 1e9,
+                          "prescanned_pass_b": fast,
+                          "lookback_pass_s": t_lb, "lookback_pass_gbs": in_bytes / t_lb / 1e9,
                           "passB_bit_exact_vs_prefill": ok},
         "append_event": {"tokens": 128, "heads": He, "us_per_event": t_ev * 1e6,
                          "gbs_f32_in": ev_bytes / t_ev / 1e9},
