@@ -196,6 +196,15 @@ __device__ __forceinline__ void img_or_bits32(uint32_t *img, uint32_t p, uint32_
     if (s) atomicOr(&img[(p >> 5) + 1], v << (32 - s));
 }
 
+// 16-bit little-endian field at even stream byte offset j of the block image
+// (img words are big-endian stream words, byte-swapped at write-out); the word
+// shared by the header's end and the payload's start is OR-ed
+__device__ __forceinline__ void img_u16(uint32_t *img, int j, uint32_t v, int shared_word) {
+    const uint32_t sw = ((v & 0xFFu) << 8) | ((v >> 8) & 0xFFu);
+    if ((j >> 2) == shared_word) atomicOr(&img[j >> 2], (j & 2) ? sw : (sw << 16));
+    else reinterpret_cast<uint16_t *>(img)[(j >> 1) ^ 1] = (uint16_t)sw;
+}
+
 // Shared-memory layout (dynamic): stage f32 [bs*D] (reused as the block image),
 // codes u8 [bs*D], unit lo/scale/r32 f32 [n_units], slice bits u32 [bs],
 // slice offsets u32 [bs], codebook words u32[256] + lengths u8[256].
@@ -375,88 +384,163 @@ store_kernel(StoreParams P, int stage_words) {
         return;
     }
 
-    // ---- slice bit counts: warp per slice, lane per run of codes --------
-    const int cpl = (D + 31) / 32;
     bool bad = false;
-    for (int r = warp; r < bs; r += kWarps) {
-        uint32_t bits = 0;
-        for (int k = 0; k < cpl; ++k) {
-            const int c = lane * cpl + k;
-            if (c < D) {
-                const uint32_t l = cl[codes[r * D + c]];
-                bad |= (l == 0);
-                bits += l;
-            }
-        }
-        bits = kvc_warp_incl_scan(bits, lane);
-        if (lane == 31) {
-            s_bits[r] = bits;
-            bad |= bits > 0xFFFFu;
-        }
-    }
-    if (bad) kvc_set_err(P.err, KVC_ERR_CODEC);
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t carry = 0;
-        for (int r0 = 0; r0 < bs; r0 += 32) {
-            const int r = r0 + lane;
-            const uint32_t v = r < bs ? s_bits[r] : 0;
-            const uint32_t inc = kvc_warp_incl_scan(v, lane);
-            if (r < bs) s_off[r] = carry + inc - v;
-            carry += __shfl_sync(0xffffffffu, inc, 31);
-        }
-        if (lane == 0) sh_total_bits = carry;
-    }
-    __syncthreads();
-    const uint32_t total_bits = sh_total_bits;
+    uint32_t total_bits, pbytes, size;
     const int hdr = kvc_header_bytes(bs, n_units);
-    const uint32_t pbytes = (total_bits + 7) / 8;
-    const uint32_t size = (hdr + pbytes + 3) & ~3u;
-
-    // ---- block image in shared memory (reuses the staging area) --------
-    uint32_t *img = reinterpret_cast<uint32_t *>(sm);
-    for (int i = tid; i < (int)(size >> 2); i += kThreads) img[i] = 0;
-    __syncthreads();
     const uint32_t block_index = (P.chunk_base + (uint32_t)chunk) * (uint32_t)P.H_total +
                                  (uint32_t)(P.head_base + hl);
-    if (tid < 4) img_or_byte(img, tid, block_index >> (8 * tid));
-    if (tid < 2) img_or_byte(img, 4 + tid, (uint32_t)bs >> (8 * tid));
-    for (int r = tid; r < bs; r += kThreads) {
-        img_or_byte(img, 6 + 2 * r, s_bits[r]);
-        img_or_byte(img, 7 + 2 * r, s_bits[r] >> 8);
-    }
-    for (int i = tid; i < 2 * n_units; i += kThreads) {
-        const uint32_t w = __float_as_uint((i & 1) ? u_sc[i >> 1] : u_lo[i >> 1]);
-        const int j0 = 6 + 2 * bs + 4 * i;
+    uint32_t *img = reinterpret_cast<uint32_t *>(sm);
+    bool hot = false;
+    if constexpr (DT == 128 && BST == 64) hot = S.cb->max_len <= 8;
+    if (hot) {
+        // hot shape, codes <= 8 bits: warp w owns rows w, w+8, ..; lane l the 4
+        // codes 4l..4l+3 of a row (one 32-bit load), their codewords packed into
+        // one <= 32-bit run kept in registers between the counts and the emission
+        constexpr int RW = 64 / kWarps;
+        uint32_t run[RW], ex[RW];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) img_or_byte(img, j0 + k, w >> (8 * k));
-    }
-    for (int r = warp; r < bs; r += kWarps) {
-        // lane's run of codes starts at the warp-exclusive prefix of lengths
-        uint32_t lbits = 0;
-        for (int k = 0; k < cpl; ++k) {
-            const int c = lane * cpl + k;
-            if (c < D) lbits += cl[codes[r * D + c]];
-        }
-        const uint32_t incl = kvc_warp_incl_scan(lbits, lane);
-        uint32_t p = (uint32_t)hdr * 8 + s_off[r] + incl - lbits;
-        uint64_t accb = 0;
-        int nacc = 0;
-        for (int k = 0; k < cpl; ++k) {
-            const int c = lane * cpl + k;
-            if (c >= D) break;
-            const uint32_t s = codes[r * D + c];
-            const int l = cl[s];
-            accb |= (uint64_t)cw[s] << (64 - nacc - l);
-            nacc += l;
-            if (nacc >= 32) {
-                img_or_bits32(img, p, (uint32_t)(accb >> 32));
-                p += 32;
-                accb <<= 32;
-                nacc -= 32;
+        for (int i = 0; i < RW; ++i) {
+            const int r = warp + kWarps * i;
+            const uint32_t w4 = *reinterpret_cast<const uint32_t *>(codes + r * 128 + 4 * lane);
+            uint32_t rn = 0, n = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t sym = (w4 >> (8 * k)) & 0xFFu;
+                const uint32_t l = cl[sym];
+                bad |= (l == 0);
+                rn = (rn << l) | cw[sym];
+                n += l;
+            }
+            run[i] = rn;
+            const uint32_t inc = kvc_warp_incl_scan(n, lane);
+            ex[i] = (inc - n) | (n << 24);
+            if (lane == 31) {
+                s_bits[r] = inc;
+                bad |= inc > 0xFFFFu;
             }
         }
-        if (nacc) img_or_bits32(img, p, (uint32_t)(accb >> 32));
+        if (bad) kvc_set_err(P.err, KVC_ERR_CODEC);
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t v0 = s_bits[lane], v1 = s_bits[lane + 32];
+            const uint32_t i0 = kvc_warp_incl_scan(v0, lane);
+            const uint32_t t0 = __shfl_sync(0xffffffffu, i0, 31);
+            const uint32_t i1 = kvc_warp_incl_scan(v1, lane);
+            s_off[lane] = i0 - v0;
+            s_off[lane + 32] = t0 + i1 - v1;
+            if (lane == 31) sh_total_bits = t0 + i1;
+        }
+        __syncthreads();
+        total_bits = sh_total_bits;
+        pbytes = (total_bits + 7) / 8;
+        size = (hdr + pbytes + 3) & ~3u;
+        for (int i = tid; i < (int)(size >> 4) + 1; i += kThreads)
+            reinterpret_cast<uint4 *>(img)[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+        // header: 16-bit little-endian fields at even offsets (plain stores; the
+        // word shared with the payload start takes an OR)
+        const int shw = (hdr & 3) ? (hdr >> 2) : -1;
+        if (tid == 0) img_u16(img, 0, block_index & 0xFFFFu, shw);
+        if (tid == 1) img_u16(img, 2, block_index >> 16, shw);
+        if (tid == 2) img_u16(img, 4, 64u, shw);
+        if (tid < 64) img_u16(img, 6 + 2 * tid, s_bits[tid], shw);
+        if (tid < n_units) {
+            const int j0 = 6 + 2 * 64 + 8 * tid;
+            const uint32_t lo = __float_as_uint(u_lo[tid]), sc = __float_as_uint(u_sc[tid]);
+            img_u16(img, j0, lo & 0xFFFFu, shw);
+            img_u16(img, j0 + 2, lo >> 16, shw);
+            img_u16(img, j0 + 4, sc & 0xFFFFu, shw);
+            img_u16(img, j0 + 6, sc >> 16, shw);
+        }
+#pragma unroll
+        for (int i = 0; i < RW; ++i) {
+            const uint32_t n = ex[i] >> 24;
+            if (!n) continue;
+            const int r = warp + kWarps * i;
+            const uint32_t p = (uint32_t)hdr * 8 + s_off[r] + (ex[i] & 0xFFFFFFu);
+            const uint32_t left = run[i] << (32 - n), sft = p & 31;
+            atomicOr(&img[p >> 5], left >> sft);
+            if (sft + n > 32) atomicOr(&img[(p >> 5) + 1], left << (32 - sft));
+        }
+    } else {
+        // ---- slice bit counts: warp per slice, lane per run of codes --------
+        const int cpl = (D + 31) / 32;
+        for (int r = warp; r < bs; r += kWarps) {
+            uint32_t bits = 0;
+            for (int k = 0; k < cpl; ++k) {
+                const int c = lane * cpl + k;
+                if (c < D) {
+                    const uint32_t l = cl[codes[r * D + c]];
+                    bad |= (l == 0);
+                    bits += l;
+                }
+            }
+            bits = kvc_warp_incl_scan(bits, lane);
+            if (lane == 31) {
+                s_bits[r] = bits;
+                bad |= bits > 0xFFFFu;
+            }
+        }
+        if (bad) kvc_set_err(P.err, KVC_ERR_CODEC);
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t carry = 0;
+            for (int r0 = 0; r0 < bs; r0 += 32) {
+                const int r = r0 + lane;
+                const uint32_t v = r < bs ? s_bits[r] : 0;
+                const uint32_t inc = kvc_warp_incl_scan(v, lane);
+                if (r < bs) s_off[r] = carry + inc - v;
+                carry += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            if (lane == 0) sh_total_bits = carry;
+        }
+        __syncthreads();
+        total_bits = sh_total_bits;
+        pbytes = (total_bits + 7) / 8;
+        size = (hdr + pbytes + 3) & ~3u;
+
+        // ---- block image in shared memory (reuses the staging area) --------
+        for (int i = tid; i < (int)(size >> 2); i += kThreads) img[i] = 0;
+        __syncthreads();
+        if (tid < 4) img_or_byte(img, tid, block_index >> (8 * tid));
+        if (tid < 2) img_or_byte(img, 4 + tid, (uint32_t)bs >> (8 * tid));
+        for (int r = tid; r < bs; r += kThreads) {
+            img_or_byte(img, 6 + 2 * r, s_bits[r]);
+            img_or_byte(img, 7 + 2 * r, s_bits[r] >> 8);
+        }
+        for (int i = tid; i < 2 * n_units; i += kThreads) {
+            const uint32_t w = __float_as_uint((i & 1) ? u_sc[i >> 1] : u_lo[i >> 1]);
+            const int j0 = 6 + 2 * bs + 4 * i;
+    #pragma unroll
+            for (int k = 0; k < 4; ++k) img_or_byte(img, j0 + k, w >> (8 * k));
+        }
+        for (int r = warp; r < bs; r += kWarps) {
+            // lane's run of codes starts at the warp-exclusive prefix of lengths
+            uint32_t lbits = 0;
+            for (int k = 0; k < cpl; ++k) {
+                const int c = lane * cpl + k;
+                if (c < D) lbits += cl[codes[r * D + c]];
+            }
+            const uint32_t incl = kvc_warp_incl_scan(lbits, lane);
+            uint32_t p = (uint32_t)hdr * 8 + s_off[r] + incl - lbits;
+            uint64_t accb = 0;
+            int nacc = 0;
+            for (int k = 0; k < cpl; ++k) {
+                const int c = lane * cpl + k;
+                if (c >= D) break;
+                const uint32_t s = codes[r * D + c];
+                const int l = cl[s];
+                accb |= (uint64_t)cw[s] << (64 - nacc - l);
+                nacc += l;
+                if (nacc >= 32) {
+                    img_or_bits32(img, p, (uint32_t)(accb >> 32));
+                    p += 32;
+                    accb <<= 32;
+                    nacc -= 32;
+                }
+            }
+            if (nacc) img_or_bits32(img, p, (uint32_t)(accb >> 32));
+        }
     }
 
     if (prescanned) {
