@@ -280,6 +280,72 @@ store_kernel(StoreParams P, int stage_words) {
             u_sc[c] = sc;
             u_r[c] = sc > 0.f ? __frcp_rn(sc) : 0.f;
         }
+    } else if (DT == 128 && BST == 64 && !is_v) {
+        // thread -> column pair (2j, 2j+1) over rows 16q..16q+15; quarters
+        // combined through shared memory (the codes area, unused until later)
+        const int j = tid & 63, q = tid >> 6;
+        float lo0, lo1, hi0, hi1;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int r = 16 * q + i;
+            float x0, x1;
+            if constexpr (sizeof(T) == 2) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(stage + r * 128 + 2 * j));
+                x0 = f.x; x1 = f.y;
+            } else {
+                const float2 f = *reinterpret_cast<const float2 *>(stage + r * 128 + 2 * j);
+                x0 = f.x; x1 = f.y;
+            }
+            if (i == 0) {
+                lo0 = hi0 = x0;
+                lo1 = hi1 = x1;
+            } else {
+                lo0 = fminf(lo0, x0); hi0 = fmaxf(hi0, x0);
+                lo1 = fminf(lo1, x1); hi1 = fmaxf(hi1, x1);
+            }
+        }
+        float4 *part = reinterpret_cast<float4 *>(codes);  // [4][64] (lo0, lo1, hi0, hi1)
+        part[q * 64 + j] = make_float4(lo0, lo1, hi0, hi1);
+        __syncthreads();
+        if (tid < 128) {
+            const int jj = tid >> 1, odd = tid & 1;
+            float lo = 3.4e38f, hi = -3.4e38f;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const float4 v = part[qq * 64 + jj];
+                lo = fminf(lo, odd ? v.y : v.x);
+                hi = fmaxf(hi, odd ? v.w : v.z);
+            }
+            const float sc = (float)__dmul_rn(S.rel, __dsub_rn((double)hi, (double)lo));
+            u_lo[tid] = lo;
+            u_sc[tid] = sc;
+            u_r[tid] = sc > 0.f ? __frcp_rn(sc) : 0.f;
+        }
+    } else if (DT == 128 && BST == 64) {
+        // V: warp per row, lane -> 4 consecutive values (one vector load)
+#pragma unroll 2
+        for (int r = warp; r < 64; r += kWarps) {
+            float v[4];
+            if constexpr (sizeof(T) == 2) {
+                const uint2 u = *reinterpret_cast<const uint2 *>(stage + r * 128 + 4 * lane);
+                const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&u.x));
+                const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&u.y));
+                v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+            } else {
+                const float4 u = *reinterpret_cast<const float4 *>(stage + r * 128 + 4 * lane);
+                v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+            }
+            float lo = fminf(fminf(v[0], v[1]), fminf(v[2], v[3]));
+            float hi = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+            lo = kvc_warp_min(lo);
+            hi = kvc_warp_max(hi);
+            if (lane == 0) {
+                const float sc = (float)__dmul_rn(S.rel, __dsub_rn((double)hi, (double)lo));
+                u_lo[r] = lo;
+                u_sc[r] = sc;
+                u_r[r] = sc > 0.f ? __frcp_rn(sc) : 0.f;
+            }
+        }
     } else if (!is_v) {
         for (int c = tid; c < D; c += kThreads) {
             float lo = kvc_load(&stage[c]), hi = lo;
