@@ -114,12 +114,15 @@ __device__ __forceinline__ uint8_t code_clamped(float x, float lo, float scale, 
 }
 
 // code_fast with the scale read only on the (rare) exact path
+// floor and the integer conversion without the XU pipe: t + 2^23 rounded toward
+// -inf holds floor(t) in its low mantissa bits (0 <= t < 2^23)
 __device__ __forceinline__ uint32_t code_fast_p(float x, float lo, float r32, const float *scale_p) {
     const float t = __fmul_rn(__fsub_rn(x, lo), r32);
     if (t < 300.f) {
-        const float c = floorf(t);
-        const float f = t - c;
-        if (fabsf(f - 0.5f) > (1.0f / 4096.0f)) return (uint32_t)(int)(c + (f >= 0.5f ? 1.f : 0.f));
+        const float m = __fadd_rd(t, 8388608.0f);
+        const float f = t - (m - 8388608.0f);  // both exact
+        if (fabsf(f - 0.5f) > (1.0f / 4096.0f))
+            return (__float_as_uint(m) & 0x1FFu) + (f >= 0.5f ? 1u : 0u);
     }
     const float sc = *scale_p;
     return sc > 0.f ? code_f64(x, lo, sc) : 0u;
