@@ -246,10 +246,18 @@ def main():
 
     import paper_2509_00579_b200 as kv
 
+    # KVC_BENCH_SHARE_GPU=1 (debug only): every rank on cuda:0 over gloo, to
+    # exercise the multi-rank path on a one-GPU box; never a bench number
+    share = os.environ.get("KVC_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
     if args.heads % world:
         raise SystemExit("heads must divide across ranks")
     hl = args.heads // world
@@ -286,7 +294,10 @@ def main():
         for layer in range(L):
             layer_call(layer)
         if world > 1:
-            dist.all_gather_into_tensor(gathered, outs)
+            if share:
+                dist.all_gather(list(gathered.unbind(0)), outs)
+            else:
+                dist.all_gather_into_tensor(gathered, outs)
 
     for _ in range(args.warmup):
         step()
@@ -302,6 +313,8 @@ def main():
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=device)
