@@ -423,6 +423,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": round(ach, 2), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
                          "traffic": _ncu_traffic(args.config), "peak_kind": peak_kind,
+                         "binding": _ncu_binding(args.config),
                          "kernel": ("fused_attn_ws_kernel" if G == 1 else "fused_attn_gqa_kernel")
                                    + " (+combine), one layer launch, compressed bytes"},
             "e2e": {"value": round(e2e_val, 2), "unit": "GB/s (equivalent fp16 KV)",
@@ -476,6 +477,22 @@ def quant_sweep(kv, torch, device, T, H, B):
                      "fetch_ms": round(ms, 4)})
         del states
     return rows
+
+
+def _ncu_binding(config):
+    """What bounds the fused kernel per the committed ncu capture: the shared-
+    memory wavefront pipe (LUT bank conflicts), issue and ALU utilisation."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"fused_ncu_cfg{config}.json")) as fh:
+            d = json.load(fh)
+        pct = lambda k: round(float(d[k].split()[0]) / 100.0, 3)
+        return {"smem_wavefront_pipe_frac": pct(
+                    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+                "issue_active_frac": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "alu_pipe_frac": pct("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                "source": f"profiles/fused_ncu_cfg{config}.json (ncu --set full, one layer launch)"}
+    except Exception:
+        return None
 
 
 def _ncu_traffic(config):

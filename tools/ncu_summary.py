@@ -50,7 +50,11 @@ def full(path):
         hdr, units, vals = rd[0], rd[1], rd[2]
         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
                   "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
-                  "smsp__sass_inst_executed_op_shared_ld.sum"):
+                  "smsp__sass_inst_executed_op_shared_ld.sum",
+                  "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+                  "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+                  "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+                  "smsp__issue_active.avg.pct_of_peak_sustained_active"):
             if m in hdr:
                 i = hdr.index(m)
                 res[m] = f"{vals[i]} {units[i]}"
