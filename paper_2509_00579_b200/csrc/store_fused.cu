@@ -132,6 +132,17 @@ __device__ __forceinline__ uint32_t code_fast_p(float x, float lo, float r32, co
 // q, q+4, ..., mode specialised so the unit parameters are hoisted (K: per
 // column, loaded once) or broadcast (V: per row, one warp shares the row).
 // Pass B stores the code pair with one 16-bit store; pass A counts them.
+// Branch-free fast code; `near` flags values the f32 estimate cannot decide
+// (round-half-up boundary within 2^-12, or t out of range), which must take
+// code_f64.  The result is only used when !near.
+__device__ __forceinline__ uint32_t code_fast_flag(float x, float lo, float r32, bool &near) {
+    const float t = __fmul_rn(__fsub_rn(x, lo), r32);
+    const float m = __fadd_rd(fminf(t, 512.f), 8388608.0f);  // floor(t) in the low bits
+    const float f = t - (m - 8388608.0f);
+    near = !(t < 300.f) || !(fabsf(f - 0.5f) > (1.0f / 4096.0f));
+    return ((__float_as_uint(m) & 0x1FFu) + (f >= 0.5f ? 1u : 0u)) & 0xFFu;
+}
+
 template <typename T, bool ENCODE, int MODE>
 __device__ __forceinline__ void quantize_hot(const T *stage, uint8_t *codes, const float *u_lo,
                                              const float *u_sc, const float *u_r, int max_code,
@@ -158,16 +169,24 @@ __device__ __forceinline__ void quantize_hot(const T *stage, uint8_t *codes, con
             x0 = f.x; x1 = f.y;
         }
         uint32_t a, b;
-        if (MODE == KVC_V_TOKEN) {
-            const float lo = u_lo[r], rr = u_r[r];
-            a = code_fast_p(x0, lo, rr, &u_sc[r]);
-            b = code_fast_p(x1, lo, rr, &u_sc[r]);
-        } else if (MODE == KVC_K_CHANNEL) {
+        if (MODE == KVC_K_CHANNEL) {
             a = code_clamped(x0, klo0, u_sc[c0], kr0, max_code);
             b = code_clamped(x1, klo1, u_sc[c0 + 1], kr1, max_code);
         } else {
-            a = code_fast_p(x0, klo0, kr0, &u_sc[c0]);
-            b = code_fast_p(x1, klo1, kr1, &u_sc[c0 + 1]);
+            // branch-free fast codes; near-ties (~0.05 % of fp16 values) are redone
+            // exactly behind one warp-uniform branch per pair (taken ~3 % of the time)
+            const float lo0 = MODE == KVC_V_TOKEN ? u_lo[r] : klo0;
+            const float lo1 = MODE == KVC_V_TOKEN ? lo0 : klo1;
+            const float r0 = MODE == KVC_V_TOKEN ? u_r[r] : kr0;
+            const float r1 = MODE == KVC_V_TOKEN ? r0 : kr1;
+            bool near_a, near_b;
+            a = code_fast_flag(x0, lo0, r0, near_a);
+            b = code_fast_flag(x1, lo1, r1, near_b);
+            if (__any_sync(0xffffffffu, near_a || near_b)) {
+                const int ua = MODE == KVC_V_TOKEN ? r : c0, ub = MODE == KVC_V_TOKEN ? r : c0 + 1;
+                if (near_a) a = u_sc[ua] > 0.f ? code_f64(x0, lo0, u_sc[ua]) : 0u;
+                if (near_b) b = u_sc[ub] > 0.f ? code_f64(x1, lo1, u_sc[ub]) : 0u;
+            }
         }
         if (ENCODE) {
             *reinterpret_cast<uint16_t *>(codes + r * D + c0) = (uint16_t)(a | (b << 8));
