@@ -135,12 +135,17 @@ __device__ __forceinline__ uint32_t code_fast_p(float x, float lo, float r32, co
 // Branch-free fast code; `near` flags values the f32 estimate cannot decide
 // (round-half-up boundary within 2^-12, or t out of range), which must take
 // code_f64.  The result is only used when !near.
+// With lo = unit min and scale = RN(rel*(max-min)), t <= (1/rel)(1 + 2^-22) <= 257
+// for rel >= 1/256, so v = RN(t + 1/2) < 512 and round-half-up is floor(v):
+// RD(v + 2^23) holds it in the low mantissa bits.  v rounds t + 1/2 only in
+// its last bit, which can move floor() only inside the flagged band.
 __device__ __forceinline__ uint32_t code_fast_flag(float x, float lo, float r32, bool &near) {
     const float t = __fmul_rn(__fsub_rn(x, lo), r32);
-    const float m = __fadd_rd(fminf(t, 512.f), 8388608.0f);  // floor(t) in the low bits
-    const float f = t - (m - 8388608.0f);
-    near = !(t < 300.f) || !(fabsf(f - 0.5f) > (1.0f / 4096.0f));
-    return ((__float_as_uint(m) & 0x1FFu) + (f >= 0.5f ? 1u : 0u)) & 0xFFu;
+    const float v = __fadd_rn(t, 0.5f);
+    const float m = __fadd_rd(v, 8388608.0f);
+    const float g = v - (m - 8388607.5f);  // frac(v) - 1/2, exact
+    near = fabsf(g) >= 0.5f - (1.0f / 4096.0f);
+    return __float_as_uint(m) & 0xFFu;
 }
 
 template <typename T, bool ENCODE, int MODE>
@@ -738,6 +743,11 @@ extern "C" size_t kvc_store_workspace_bytes(int n_chunks, int H, int D, int bs) 
 
 static int launch_store(const StoreParams &P, int x_dtype, bool encode, int max_len,
                         cudaStream_t s) {
+    // quantizer.py:60-66: rel_quant_scale in [1/255, 1] (codes fit u8; the fast
+    // quantiser relies on t <= 1/rel < 256)
+    for (int t = 0; t < 2; ++t)
+        if (!(P.t[t].rel >= 1.0 / 255.0 - 1e-15 && P.t[t].rel <= 1.0))
+            return kvc_fail(KVC_ERR_CONFIG, "rel_quant_scale outside [1/255, 1]");
     const int nb = P.n_chunks * P.H_local;
     const int nv = P.bs * P.D;
     size_t sm = smem_bytes(P.bs, P.D, encode ? max_len : 1, x_dtype == KVC_F16 ? 2 : 4);
