@@ -197,7 +197,11 @@ size_t kvc_store_blk_hist_bytes(int n_chunks, int H);
 int kvc_store_hist_blocks(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
                           int n_chunks, int H, int D, int bs, int k_mode, double rel_k,
                           double rel_v, const float *k_ranges_dev, uint64_t *hist_dev,
-                          uint16_t *blk_hist_dev, void *stream);
+                          uint16_t *blk_hist_dev, uint8_t *codes_dev, void *stream);
+/* codes_dev (optional, may be NULL; used for head_dim 128 / block 64): pass A
+ * leaves every block's codes and (min, scale) pairs there and pass B encodes
+ * from them instead of re-quantising the input (kvc_store_codes_bytes). */
+size_t kvc_store_codes_bytes(int n_chunks, int H);
 int kvc_store_prefill(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
                       int n_chunks, int H_local, int H_total, int head_base, int D, int bs,
                       int k_mode, double rel_k, double rel_v, const float *k_ranges_dev,
@@ -208,7 +212,8 @@ int kvc_store_prefill(const void *k_dev, const void *v_dev, int x_dtype, long ro
                       kvc_arena_counters *k_counters_dev, uint8_t *v_arena_dev,
                       uint64_t v_capacity, uint32_t *v_offsets_dev,
                       kvc_arena_counters *v_counters_dev, const uint16_t *blk_hist_dev,
-                      void *workspace_dev, size_t workspace_bytes, void *stream);
+                      const uint8_t *codes_dev, void *workspace_dev, size_t workspace_bytes,
+                      void *stream);
 
 /* ---------------------------------------------------------------- */
 /* Fetch — replaces attention.py:59-188 and kvcache.py:182-212        */

@@ -91,9 +91,10 @@ SIGNATURES = {
     "kvc_store_supported": (I, [I, I, I]),
     "kvc_store_prefill_supported": (I, [I, I, D_, D_]),
     "kvc_store_blk_hist_bytes": (SZ, [I, I]),
-    "kvc_store_hist_blocks": (I, [P, P, I, L, I, I, I, I, I, D_, D_, P, P, P, P]),
+    "kvc_store_hist_blocks": (I, [P, P, I, L, I, I, I, I, I, D_, D_, P, P, P, P, P]),
+    "kvc_store_codes_bytes": (SZ, [I, I]),
     "kvc_store_prefill": (I, [P, P, I, L, I, I, I, I, I, I, I, D_, D_, P, U32, P, I, P, I, P, U64,
-                              P, P, P, U64, P, P, P, P, SZ, P]),
+                              P, P, P, U64, P, P, P, P, P, SZ, P]),
     "kvc_k_scores": (I, [P, I, I, I, I, P, P, L, P, P]),
     "kvc_softmax_rows": (I, [P, I, L, L, P]),
     "kvc_v_output": (I, [P, I, I, I, I, P, L, P, P, P, P]),

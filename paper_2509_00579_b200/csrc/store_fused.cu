@@ -43,6 +43,11 @@ struct StoreTensor {
     unsigned long long *hist;   // 256 bins (histogram pass)
     int max_code;               // ceil(1/rel): codes lie in [0, max_code]
     const float *ranges;        // K_CHANNEL: [2][H_local][D] whole-context (min, max)
+    // prefill fast path, hot shape: pass A writes each block's codes [64][128] u8
+    // and unit (min, scale) f32 pairs here; pass B reads them instead of
+    // re-staging and re-quantising the input (same HBM bytes, fewer instructions)
+    uint8_t *codes_io;
+    float *metas_io;
 };
 
 struct StoreParams {
@@ -152,7 +157,7 @@ template <typename T, bool ENCODE, int MODE>
 __device__ __forceinline__ void quantize_hot(const T *stage, uint8_t *codes, const float *u_lo,
                                              const float *u_sc, const float *u_r, int max_code,
                                              bool small_alpha, uint32_t *whist, uint32_t *sh_hist,
-                                             int tid) {
+                                             int tid, uint8_t *codes_out) {
     constexpr int D = 128, BS = 64;
     const int j = tid & 63, q = tid >> 6;  // column pair, row phase (0..3)
     const int c0 = 2 * j;
@@ -195,6 +200,10 @@ __device__ __forceinline__ void quantize_hot(const T *stage, uint8_t *codes, con
         }
         if (ENCODE) {
             *reinterpret_cast<uint16_t *>(codes + r * D + c0) = (uint16_t)(a | (b << 8));
+        } else if (codes_out) {
+            *reinterpret_cast<uint16_t *>(codes_out + r * D + c0) = (uint16_t)(a | (b << 8));
+        }
+        if (ENCODE) {
         } else if (small_alpha) {
             atomicAdd(&whist[a], 1u);
             atomicAdd(&whist[b], 1u);
@@ -278,6 +287,18 @@ store_kernel(StoreParams P, int stage_words) {
     const uint64_t base = ENCODE ? S.counters->cursor : 0;
     const T *src = static_cast<const T *>(S.x) + (long)chunk * bs * P.row_stride + (long)hl * D;
 
+    const bool small_alpha = S.max_code < 32;
+    const bool from_codes = ENCODE && S.codes_io != nullptr;  // prescanned, hot shape
+    if (from_codes) {
+        const uint4 *cs = reinterpret_cast<const uint4 *>(S.codes_io + (size_t)b * 8192);
+        for (int i = tid; i < 8192 / 16; i += kThreads) reinterpret_cast<uint4 *>(codes)[i] = cs[i];
+        for (int i = tid; i < n_units; i += kThreads) {
+            const float2 m = reinterpret_cast<const float2 *>(S.metas_io)[(size_t)b * n_units + i];
+            u_lo[i] = m.x;
+            u_sc[i] = m.y;
+        }
+        __syncthreads();
+    } else {
     // ---- stage [bs, D] as f32 ------------------------------------------
     constexpr int VEC = 16 / sizeof(T);
     if (D % VEC == 0 && (P.row_stride % VEC) == 0 &&
@@ -406,10 +427,16 @@ store_kernel(StoreParams P, int stage_words) {
     }
     __syncthreads();
 
+    // pass A, hot shape, prefill fast path: this block's codes and metas go out
+    uint8_t *cout = (!ENCODE && S.codes_io) ? S.codes_io + (size_t)b * 8192 : nullptr;
+    if (!ENCODE && S.metas_io && tid < n_units) {
+        S.metas_io[((size_t)b * n_units + tid) * 2] = u_lo[tid];
+        S.metas_io[((size_t)b * n_units + tid) * 2 + 1] = u_sc[tid];
+    }
+
     // ---- codes (+ histogram in pass A) --------------------------------
     // Pass A: per-warp 32-bin shared histograms (small alphabets) keep atomic
     // contention inside a warp; wider alphabets use the shared 256-bin one.
-    const bool small_alpha = S.max_code < 32;
     uint32_t *whist = sh_whist[warp];
     if (!ENCODE) {
         whist[lane] = 0;
@@ -423,13 +450,13 @@ store_kernel(StoreParams P, int stage_words) {
     if constexpr (DT == 128 && BST == 64) {
         if (is_kc)
             quantize_hot<T, ENCODE, KVC_K_CHANNEL>(stage, codes, u_lo, u_sc, u_r, S.max_code,
-                                                   small_alpha, whist, sh_hist, tid);
+                                                   small_alpha, whist, sh_hist, tid, cout);
         else if (is_v)
             quantize_hot<T, ENCODE, KVC_V_TOKEN>(stage, codes, u_lo, u_sc, u_r, S.max_code,
-                                                 small_alpha, whist, sh_hist, tid);
+                                                 small_alpha, whist, sh_hist, tid, cout);
         else
             quantize_hot<T, ENCODE, KVC_K_BLOCK>(stage, codes, u_lo, u_sc, u_r, S.max_code,
-                                                 small_alpha, whist, sh_hist, tid);
+                                                 small_alpha, whist, sh_hist, tid, cout);
     } else if (D <= kThreads) {
         // thread -> fixed column c (one division per thread, none per element)
         const int rstep = kThreads / D;
@@ -461,6 +488,7 @@ store_kernel(StoreParams P, int stage_words) {
         }
     }
     __syncthreads();
+    }  // !from_codes
     if (!ENCODE) {
         if (small_alpha) {
             if (tid < 32) {
@@ -995,11 +1023,27 @@ extern "C" size_t kvc_store_blk_hist_bytes(int n_chunks, int H) {
     return (size_t)2 * (size_t)(n_chunks > 0 ? n_chunks : 1) * H * 32 * sizeof(uint16_t);
 }
 
+// codes_dev (optional, hot shape head_dim 128 / block 64 only): [2][nb][64*128] u8
+// codes, then f32 (min, scale) pairs [nb][128] for K and [nb][64] for V
+extern "C" size_t kvc_store_codes_bytes(int n_chunks, int H) {
+    const size_t nb = (size_t)(n_chunks > 0 ? n_chunks : 1) * H;
+    return nb * (2 * 8192 + 8 * (128 + 64));
+}
+
+static void codes_layout(StoreParams &P, uint8_t *codes_dev, long nb) {
+    if (!codes_dev || P.D != 128 || P.bs != 64) return;
+    P.t[0].codes_io = codes_dev;
+    P.t[1].codes_io = codes_dev + (size_t)nb * 8192;
+    float *m = reinterpret_cast<float *>(codes_dev + (size_t)nb * 2 * 8192);
+    P.t[0].metas_io = m;
+    P.t[1].metas_io = m + (size_t)nb * 128 * 2;
+}
+
 extern "C" int kvc_store_hist_blocks(const void *k_dev, const void *v_dev, int x_dtype,
                                      long row_stride, int n_chunks, int H, int D, int bs,
                                      int k_mode, double rel_k, double rel_v,
                                      const float *k_ranges_dev, uint64_t *hist_dev,
-                                     uint16_t *blk_hist_dev, void *stream) {
+                                     uint16_t *blk_hist_dev, uint8_t *codes_dev, void *stream) {
     if (k_mode != KVC_K_BLOCK && k_mode != KVC_K_CHANNEL) return kvc_fail(KVC_ERR_CONFIG, "bad K mode");
     if (k_mode == KVC_K_CHANNEL && !k_ranges_dev)
         return kvc_fail(KVC_ERR_CONFIG, "K_CHANNEL quantization requires whole-context channel_ranges");
@@ -1025,6 +1069,7 @@ extern "C" int kvc_store_hist_blocks(const void *k_dev, const void *v_dev, int x
     P.D = D;
     P.bs = bs;
     P.blk_hist = blk_hist_dev;
+    codes_layout(P, codes_dev, (long)n_chunks * H);
     return launch_store(P, x_dtype, false, 1, static_cast<cudaStream_t>(stream));
 }
 
@@ -1038,7 +1083,8 @@ extern "C" int kvc_store_prefill(const void *k_dev, const void *v_dev, int x_dty
                                  kvc_arena_counters *k_counters_dev, uint8_t *v_arena_dev,
                                  uint64_t v_capacity, uint32_t *v_offsets_dev,
                                  kvc_arena_counters *v_counters_dev, const uint16_t *blk_hist_dev,
-                                 void *workspace_dev, size_t workspace_bytes, void *stream) {
+                                 const uint8_t *codes_dev, void *workspace_dev,
+                                 size_t workspace_bytes, void *stream) {
     if (n_chunks == 0) return KVC_OK;
     if (k_mode != KVC_K_BLOCK && k_mode != KVC_K_CHANNEL) return kvc_fail(KVC_ERR_CONFIG, "bad K mode");
     if (k_mode == KVC_K_CHANNEL && !k_ranges_dev)
@@ -1079,5 +1125,6 @@ extern "C" int kvc_store_prefill(const void *k_dev, const void *v_dev, int x_dty
     int st = kvc_check_launch("store_offsets_kernel");
     if (st) return st;
     P.nb0 = nb0;
+    codes_layout(P, const_cast<uint8_t *>(codes_dev), (long)n_chunks * H_local);
     return launch_store(P, x_dtype, true, max_len, s);
 }

@@ -130,18 +130,22 @@ class LayerCacheState:
         kcodes = kmetas = vcodes = vmetas = None
         # small alphabets: pass A also records per-block histograms, so pass B takes
         # its arena offsets from one scan instead of the look-back (store_fused.cu)
-        blk_hist = None
+        blk_hist = blk_codes = None
         if (n_full and codebooks is None and fused
                 and lib.kvc_store_prefill_supported(bs, D, cfg_k.rel_quant_scale,
                                                     cfg_v.rel_quant_scale)):
             blk_hist = torch.empty(lib.kvc_store_blk_hist_bytes(n_chunks, H) // 2,
                                    dtype=torch.int16, device=kt.device)
+            # hot shape: pass A also leaves the codes for pass B (no re-quantisation)
+            blk_codes = (torch.empty(lib.kvc_store_codes_bytes(n_chunks, H), dtype=torch.uint8,
+                                     device=kt.device) if (D == 128 and bs == 64) else None)
             _lib.check(lib.kvc_store_hist_blocks(kt.data_ptr(), vt.data_ptr(), dtype_code(kt),
                                                  H * D, n_chunks, H, D, bs, cfg_k.mode.abi,
                                                  cfg_k.rel_quant_scale, cfg_v.rel_quant_scale,
                                                  ranges_dev.data_ptr() if ranges_dev is not None
                                                  else None, hist.data_ptr(), blk_hist.data_ptr(),
-                                                 stream), "kvc_store_hist_blocks")
+                                                 blk_codes.data_ptr() if blk_codes is not None
+                                                 else None, stream), "kvc_store_hist_blocks")
         elif n_full and codebooks is None and fused:
             # pass A: quantise + histogram only (store_fused.cu)
             _lib.check(lib.kvc_store_hist(kt.data_ptr(), vt.data_ptr(), dtype_code(kt), H * D,
@@ -172,7 +176,7 @@ class LayerCacheState:
                  k_channel_ranges=k_channel_ranges)
         if n_full:
             if blk_hist is not None and st._fused_store:
-                st._store(kt, vt, n_chunks, blk_hist=blk_hist)
+                st._store(kt, vt, n_chunks, blk_hist=blk_hist, blk_codes=blk_codes)
             elif st._fused_store:
                 st._store(kt, vt, n_chunks)
             else:
@@ -220,7 +224,8 @@ class LayerCacheState:
         self.compressed_tokens += n_chunks * bs
 
     def _store(self, k_src: torch.Tensor, v_src: torch.Tensor, n_chunks: int,
-               blk_hist: Optional[torch.Tensor] = None) -> None:
+               blk_hist: Optional[torch.Tensor] = None,
+               blk_codes: Optional[torch.Tensor] = None) -> None:
         """Quantise + encode + append of n_chunks*H blocks per tensor from
         k_src/v_src rows [0, n_chunks*bs) (store_fused.cu): one look-back launch
         (kvc_store_append), or, with the prefill's per-block histograms, the
@@ -234,7 +239,8 @@ class LayerCacheState:
         self.v_arena.reserve(nb, vw)
         ws = self._workspace(lib.kvc_store_workspace_bytes(n_chunks, H, D, bs))
         fn = lib.kvc_store_append if blk_hist is None else functools.partial(
-            _prefill_call, lib.kvc_store_prefill, blk_hist.data_ptr())
+            _prefill_call, lib.kvc_store_prefill, blk_hist.data_ptr(),
+            blk_codes.data_ptr() if blk_codes is not None else None)
         st = fn(
             k_src.data_ptr(), v_src.data_ptr(), dtype_code(k_src), H * D, n_chunks, H,
             self.head_total, self.head_base, D, bs, self.cfg_k.mode.abi,
@@ -379,7 +385,7 @@ class LayerCacheState:
         return CacheTensor(outs[0]), CacheTensor(outs[1])
 
 
-def _prefill_call(fn, blk_hist_ptr, *args):
+def _prefill_call(fn, blk_hist_ptr, codes_ptr, *args):
     """kvc_store_prefill takes kvc_store_append's arguments plus the per-block
-    histograms before the workspace."""
-    return fn(*args[:-3], blk_hist_ptr, *args[-3:])
+    histograms and pass A's codes before the workspace."""
+    return fn(*args[:-3], blk_hist_ptr, codes_ptr, *args[-3:])

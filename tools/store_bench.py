@@ -47,12 +47,14 @@ def main(ctx=32768, H=40, D=128, reps=10):
     hist = torch.zeros(512, dtype=torch.int64, device=dev)
     fast = bool(lib.kvc_store_prefill_supported(64, D, 0.05, 0.15))
     blk = torch.empty(lib.kvc_store_blk_hist_bytes(nb_chunks, H) // 2, dtype=torch.int16, device=dev)
+    codes = torch.empty(lib.kvc_store_codes_bytes(nb_chunks, H), dtype=torch.uint8, device=dev)
     a, b = ev(), ev()
     a.record(s)
     for _ in range(reps):
         if fast:
             lib.kvc_store_hist_blocks(k.data_ptr(), v.data_ptr(), 0, H * D, nb_chunks, H, D, 64, 0,
-                                      0.05, 0.15, None, hist.data_ptr(), blk.data_ptr(), s.cuda_stream)
+                                      0.05, 0.15, None, hist.data_ptr(), blk.data_ptr(),
+                                      codes.data_ptr(), s.cuda_stream)
         else:
             lib.kvc_store_hist(k.data_ptr(), v.data_ptr(), 0, H * D, nb_chunks, H, D, 64, 0, 0.05,
                                0.15, None, hist.data_ptr(), s.cuda_stream)
@@ -76,7 +78,8 @@ def main(ctx=32768, H=40, D=128, reps=10):
     torch.cuda.synchronize()
     a.record(s)
     for f in fresh:
-        f._store(k, v, nb_chunks, blk_hist=blk if fast else None)
+        f._store(k, v, nb_chunks, blk_hist=blk if fast else None,
+                 blk_codes=codes if fast else None)
     b.record(s)
     torch.cuda.synchronize()
     t_b = a.elapsed_time(b) / reps * 1e-3
