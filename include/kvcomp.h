@@ -169,7 +169,7 @@ int kvc_store_supported(int bs, int D, int max_len);
 /* One Store event with known codebooks (kvcache.py:217-239): quantise K and
  * V from x[t, h, :] (t < n_chunks*bs), Huffman-encode and append both arenas
  * in one launch; arena offsets come from a decoupled look-back scan in
- * block_index order (deterministic, no code round trip through HBM). */
+ * block_index order (deterministic; the codes never leave shared memory). */
 int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtype, long row_stride,
                      int n_chunks, int H_local, int H_total, int head_base, int D, int bs,
                      int k_mode, double rel_k, double rel_v, const float *k_ranges_dev,

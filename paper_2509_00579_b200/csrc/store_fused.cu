@@ -1,11 +1,17 @@
-// store_fused.cu — single-pass Store: quantise -> Huffman encode -> append,
-// with the arena offset of each block found by a decoupled look-back scan
-// (deterministic block_index order, no code round trip through HBM).
+// store_fused.cu — the Store: quantise -> Huffman encode -> append.
 //
-//   prefill:  pass A  store_kernel<false>  quantise + code histogram (K, V)
-//             host    2x256 histogram -> smoothed canonical codebooks
-//             pass B  store_kernel<true>   quantise + encode + look-back + write
-//   append:   pass B only (codebooks fixed after prefill, SPEC / kvcache.py:150-177)
+//   append (growing cache, kvcache.py:150-177; codebooks fixed after prefill):
+//     store_kernel<true>: quantise + encode + decoupled look-back over block
+//     sizes (deterministic block_index order) + write, one launch
+//   prefill (kvcache.py:76-145):
+//     pass A  store_kernel<false>  quantise + code histogram (K, V); with small
+//             alphabets also per-block histograms, and on the hot shape the
+//             codes and (min, scale) pairs for pass B
+//     host    2x256 histogram -> smoothed canonical codebooks
+//     scan    store_offsets_kernel: per-block sizes -> arena offsets
+//     pass B  store_kernel<true>   encode (from pass A's codes) + write at the
+//             precomputed offsets; without per-block histograms, the append
+//             kernel with its look-back
 //
 // One CTA per (chunk, head) block; blockIdx.y selects K (0) or V (1).  The
 // block is staged in shared memory as f32 (16-byte vector loads), per-unit
