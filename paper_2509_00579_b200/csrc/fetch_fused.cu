@@ -1049,7 +1049,7 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
                 const float mn = lds_f32_a2(ks + 6 + 2 * BS + 8 * c);
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    qf[c * G + g] = sc * qreg[g][k];
+                    qf[((c >> 1) * G + g) * 2 + (c & 1)] = sc * qreg[g][k];  // [64][G][2]
                     base[g] = fmaf(mn, qreg[g][k], base[g]);
                 }
             }
@@ -1064,28 +1064,33 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
             float2 sA2[G], sB2[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) sA2[g] = sB2[g] = make_float2(0.f, 0.f);
-#pragma unroll 1
-            for (int c5 = 0; c5 < 65; c5 += 5) {
+            // 12 groups of 5 pair steps + a tail of 4, one reload per group; q'
+            // pairs (channels 2c2, 2c2+1) of every member come as float2s from
+            // [64][G][2] (2 members per LDS.128), ready for FFMA2 without moves
+            auto steps = [&](int c2base, auto np) {
                 cursor2_reload(cc[0]);
                 cursor2_reload(cc[1]);
 #pragma unroll
-                for (int t = 0; t < 5; ++t) {
-                    const int c2 = c5 + t;
-                    if (c2 < D / 2) {
-                        const float2 fA = cursor2_pair(cc[0], lut_s), fB = cursor2_pair(cc[1], lut_s);
-                        // q' of channels 2*c2 and 2*c2+1 for all G members (broadcast loads)
-                        float qa[G], qb[G];
-                        lds_vec<G>(qf_s + 4 * G * (2 * c2), qa);
-                        lds_vec<G>(qf_s + 4 * G * (2 * c2 + 1), qb);
+                for (int t = 0; t < decltype(np)::value; ++t) {
+                    const int c2 = c2base + t;
+                    const float2 fA = cursor2_pair(cc[0], lut_s), fB = cursor2_pair(cc[1], lut_s);
 #pragma unroll
-                        for (int g = 0; g < G; ++g) {
-                            const float2 q2 = make_float2(qa[g], qb[g]);
-                            sA2[g] = __ffma2_rn(fA, q2, sA2[g]);
-                            sB2[g] = __ffma2_rn(fB, q2, sB2[g]);
-                        }
+                    for (int g2 = 0; g2 < G; g2 += 2) {
+                        float4 q4;
+                        asm volatile(KVC_LD_SHARED ".v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(q4.x), "=f"(q4.y), "=f"(q4.z), "=f"(q4.w)
+                                     : "r"(qf_s + 8 * (c2 * G + g2)));
+                        const float2 qa = make_float2(q4.x, q4.y), qb = make_float2(q4.z, q4.w);
+                        sA2[g2] = __ffma2_rn(fA, qa, sA2[g2]);
+                        sB2[g2] = __ffma2_rn(fB, qa, sB2[g2]);
+                        sA2[g2 + 1] = __ffma2_rn(fA, qb, sA2[g2 + 1]);
+                        sB2[g2 + 1] = __ffma2_rn(fB, qb, sB2[g2 + 1]);
                     }
                 }
-            }
+            };
+#pragma unroll 1
+            for (int g5 = 0; g5 < 12; ++g5) steps(5 * g5, std::integral_constant<int, 5>());
+            steps(60, std::integral_constant<int, 4>());
             bad |= (((cc[0].p - p0A) & 0xFFFFu) != cA) | (((cc[1].p - p0B) & 0xFFFFu) != cB);
             mbar_wait(&sempty[sl], (u & 1) ^ 1);
 #pragma unroll
