@@ -13,6 +13,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
@@ -1483,8 +1485,8 @@ int num_sms() {
     return g_num_sms;
 }
 
-// Chunks per CTA split.  Candidates are multiples of 4 (one per K/V pair);
-// the model charges each CTA a pipeline fill of ~1 chunk per pair and counts
+// Chunks per CTA split.  Candidates are multiples of the pair count; the
+// model charges each CTA a start/drain cost of ~5 chunk-times and counts
 // the idle part of the last wave (resident CTAs = ctas_per_sm x SMs), and picks
 // the split with the lowest estimated time.
 int pick_chunks_per_split(int max_chunks, long n_heads_total, int ctas_per_sm = 2, int pairs = NW) {
@@ -1494,7 +1496,10 @@ int pick_chunks_per_split(int max_chunks, long n_heads_total, int ctas_per_sm = 
     for (long cps = 4 * pairs; cps <= 4096; cps += pairs) {
         const long splits = (max_chunks + cps - 1) / cps;
         const long ctas = splits * n_heads_total;
-        const double per_cta = (double)cps / pairs + 1.0;       // chunk-times per pair
+        // chunk-times per pair, plus ~5 for the CTA's start (LUT TMA, first ring
+        // fills) and drain (partial merge) — fitted to a cps sweep on config 2
+        // (64: 1.057, 104: 1.054, 128: 1.040, 172: 1.077 ms/layer)
+        const double per_cta = (double)cps / pairs + 5.0;
         const double waves = ceil((double)ctas / (double)slots);
         const double t = waves * per_cta;
         if (t < best - 1e-9) {
@@ -1580,7 +1585,11 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         const size_t g_smem = np * (size_t)gqa_per_pair(stage_k, stage_v, group, vsl);
         if (g_smem + 2 * 16384 + 256 > 227 * 1024)
             return kvc_fail(KVC_ERR_CONFIG, "block extents too large for GQA staging");
-        const int g_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H, 1, np);
+        int g_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H, 1, np);
+        if (const char *cenv = getenv("KVC_GQA_CPS")) {  // experiments: chunks per split
+            const int v = atoi(cenv);
+            if (v >= np && v % np == 0) g_cps = v;
+        }
         const int g_splits = (max_chunks + g_cps - 1) / g_cps;
         if (sizeof(Partial) * (size_t)n_seqs * H * group * g_splits > workspace_bytes)
             return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
@@ -1609,7 +1618,11 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
     const bool use_ws = !(impl && impl[0] == 'i');
     const size_t ws_smem = WS_PAIRS * (2 * (size_t)(stage_k + stage_v) + 1024 + 64);
     if (use_ws && max_chunks > 0 && ws_smem + lut_bytes + 256 <= 227 * 1024) {
-        const int ws_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H);
+        int ws_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H);
+        if (const char *cenv = getenv("KVC_FUSED_CPS")) {  // experiments: chunks per split
+            const int v = atoi(cenv);
+            if (v >= 4 && v % 4 == 0) ws_cps = v;
+        }
         const int ws_splits = (max_chunks + ws_cps - 1) / ws_cps;
         if (sizeof(Partial) * (size_t)n_seqs * H * ws_splits > workspace_bytes)
             return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
