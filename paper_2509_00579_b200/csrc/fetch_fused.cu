@@ -597,6 +597,37 @@ __device__ __forceinline__ void decode_two(Cursor *c, uint32_t lut_s, uint32_t l
     }
 }
 
+// Sum 128 floats (acc[64] float2, channel 2c + {0,1}) over the 32 lanes with a
+// halving reduce-scatter: at step k (xor 16, 8, .., 1) a lane keeps the half of
+// its live values selected by lane bit 4-k and adds the partner's copy of it.
+// Lane l ends with channels 4l .. 4l+3 in r[0], r[1].
+__device__ __forceinline__ void reduce_scatter_128(float2 (&acc)[D / 2], uint32_t lane, float2 (&r)[2]) {
+    float2 v[32];
+    {
+        const bool hi = (lane >> 4) & 1;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const float2 keep = hi ? acc[32 + i] : acc[i], send = hi ? acc[i] : acc[32 + i];
+            v[i] = make_float2(keep.x + __shfl_xor_sync(0xffffffffu, send.x, 16),
+                               keep.y + __shfl_xor_sync(0xffffffffu, send.y, 16));
+        }
+    }
+#pragma unroll
+    for (int o = 8, n = 16; o >= 1; o >>= 1, n >>= 1) {
+        const bool hi = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            if (i < n) {
+                const float2 keep = hi ? v[n + i] : v[i], send = hi ? v[i] : v[n + i];
+                v[i] = make_float2(keep.x + __shfl_xor_sync(0xffffffffu, send.x, o),
+                                   keep.y + __shfl_xor_sync(0xffffffffu, send.y, o));
+            }
+        }
+    }
+    r[0] = v[0];
+    r[1] = v[1];
+}
+
 // ---------------------------------------------------------------------------
 // Warp-specialized fused fetch-attention (default).  CTA = 2 warpgroups:
 // warps 0-3 decode K, warps 4-7 decode V; K warp w and V warp w+4 form a pair
@@ -883,14 +914,13 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
     wm = kvc_warp_sum(wm);
     __syncthreads();  // K warps are done: their rings are free scratch
     Partial *wp = reinterpret_cast<Partial *>(smem + pair * per_pair);
-#pragma unroll
-    for (int c = 0; c < D / 2; ++c) {
-        const float vx = kvc_warp_sum(acc[c].x);
-        const float vy = kvc_warp_sum(acc[c].y);
-        if (lane == ((2 * c) & 31)) {
-            wp->o[2 * c] = vx + wm;
-            wp->o[2 * c + 1] = vy + wm;
-        }
+    {
+        // reduce-scatter of the 128 channel sums over the warp: 5 halving steps
+        // (124 shuffles instead of 640); lane l ends with channels 4l..4l+3
+        float2 r[2];
+        reduce_scatter_128(acc, lane, r);
+        reinterpret_cast<float2 *>(wp->o)[2 * lane] = make_float2(r[0].x + wm, r[0].y + wm);
+        reinterpret_cast<float2 *>(wp->o)[2 * lane + 1] = make_float2(r[1].x + wm, r[1].y + wm);
     }
     if (lane == 0) {
         wp->m = m;
