@@ -402,3 +402,39 @@ def test_fused_gqa_corrupt_stream_raises(kv):
     q = torch.randn((1, H * G, 128), device="cuda")
     with pytest.raises(kv.CodecError):
         kv.attention_gqa([st], q, G)
+
+
+@pytest.mark.parametrize("ctxs", [(1000, 1300, 1600), (70, 5000, 20000, 300)])
+def test_batched_no_scores_persistent(kv, ctxs):
+    """attention_batched without score output (the decode-loop path): ragged
+    batches with short sequences (pairs with no chunk in a split) and buffered
+    tokens, against per-state attention_step."""
+    states, qs = [], []
+    for s, ctx in enumerate(ctxs):
+        k = kv.generate_synthetic(kv.SyntheticSpec(ctx + 17, 2, 128, seed=s)).values
+        v = kv.generate_synthetic(kv.SyntheticSpec(ctx + 17, 2, 128, seed=s + 9)).values
+        st = kv.LayerCacheState.prefill(kv.CacheTensor(k[:ctx].astype(np.float16)),
+                                        kv.CacheTensor(v[:ctx].astype(np.float16)),
+                                        kv.QuantConfig(kv.QuantMode.K_BLOCK),
+                                        kv.QuantConfig(kv.QuantMode.V_TOKEN))
+        for t in range(ctx, ctx + 17):
+            st.append_token(k[t], v[t])
+        states.append(st)
+        qs.append(np.random.default_rng(s).standard_normal((2, 128), dtype=np.float32))
+    q = torch.from_numpy(np.stack(qs)).cuda()
+    out, scores, err = kv.attention_batched(states, q)
+    assert scores is None and int(err.item()) == 0
+    for s, st in enumerate(states):
+        r = kv.attention_step(st, qs[s])
+        assert max_relative_error(out[s].cpu().numpy(), r.out.cpu().numpy()) <= 1e-5
+
+
+def test_batched_no_scores_corrupt_stream(kv):
+    g = load("c_fp16_d128")
+    st = _final_state(kv, g)
+    raw = st.v_arena.raw_tensor()
+    raw[6] ^= 1
+    st._desc_key = None
+    q = torch.from_numpy(np.asarray(g["q"][0], np.float32)).cuda().unsqueeze(0)
+    _, _, err = kv.attention_batched([st], q)
+    assert int(err.item()) != 0
