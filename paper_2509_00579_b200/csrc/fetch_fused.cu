@@ -1031,13 +1031,14 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     const int first = c_begin + pair;
     const int n = first < c_end ? (c_end - first + NP - 1) / NP : 0;
     const float sm_scale = kLog2e / sqrtf((float)D);
+    const long nb_k = (long)sd.k_counters->n_blocks, nb_v = (long)sd.v_counters->n_blocks;
+    const uint64_t cur_k = sd.k_counters->cursor, cur_v = sd.v_counters->cursor;
     auto issue = [&](bool v, int j) {
         const long ord = (long)(first + NP * j) * H + h;
         const uint32_t *offs = v ? sd.v_offsets : sd.k_offsets;
-        const kvc_arena_counters *ct = v ? sd.v_counters : sd.k_counters;
-        const long nb = (long)ct->n_blocks;
+        const long nb = v ? nb_v : nb_k;
         const uint64_t s0 = offs[ord];
-        const uint64_t e0 = (ord + 1 < nb) ? (uint64_t)offs[ord + 1] : ct->cursor;
+        const uint64_t e0 = (ord + 1 < nb) ? (uint64_t)offs[ord + 1] : (v ? cur_v : cur_k);
         const uint64_t a = s0 & ~15ull;
         uint32_t bytes = (uint32_t)(((e0 + 15) & ~15ull) - a);
         if (bytes > (uint32_t)(v ? stage_v : stage_k)) {
@@ -1067,11 +1068,12 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
                 qreg[g][k] = q[((long)sidx * H * G + (long)h * G + g) * D + lane + 32 * k];
         const uint32_t qf_s = smem_u32(qf), lut_s = smem_u32(s_lutK);
         mbar_wait(s_lbar, 0);
+        uint32_t kofs_next = n > 0 ? sd.k_offsets[(long)first * H + h] & 15u : 0u;
         for (int j = 0; j < n; ++j) {
             const int u = j >> 1, sl = j & 1;
+            const uint32_t kofs = kofs_next;
+            if (j + 1 < n) kofs_next = sd.k_offsets[(long)(first + NP * (j + 1)) * H + h] & 15u;
             mbar_wait(&kfull[sl], u & 1);
-            const long ord = (long)(first + NP * j) * H + h;
-            const uint32_t kofs = sd.k_offsets[ord] & 15u;
             const uint8_t *ks = kring + sl * stage_k + kofs;
             const uint32_t cA = lds_u16(ks + 6 + 2 * lane), cB = lds_u16(ks + 6 + 2 * (lane + 32));
             const uint32_t iA = kvc_warp_incl_scan(cA, lane);
@@ -1162,8 +1164,11 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     }
     const uint32_t lut_s = smem_u32(s_lutV), tile_s = smem_u32(tile), sa_s = smem_u32(sa);
     mbar_wait(s_lbar, 0);
+    uint32_t vofs_next = n > 0 ? sd.v_offsets[(long)first * H + h] & 15u : 0u;
     for (int j = 0; j < n; ++j) {
         const int u = j >> 1, sl = j & 1;
+        const uint32_t vofs_cur = vofs_next;
+        if (j + 1 < n) vofs_next = sd.v_offsets[(long)(first + NP * (j + 1)) * H + h] & 15u;
         mbar_wait(&sfull[sl], u & 1);
         float pA[G], pB[G];
 #pragma unroll
@@ -1189,8 +1194,7 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
         }
         const int vsl = VS == 2 ? sl : 0;
         mbar_wait(&vfull[vsl], VS == 2 ? (u & 1) : (j & 1));
-        const long ord = (long)(first + NP * j) * H + h;
-        const uint32_t vofs = sd.v_offsets[ord] & 15u;
+        const uint32_t vofs = vofs_cur;
         const uint8_t *vs = vring + vsl * stage_v + vofs;
         const uint32_t cA = lds_u16(vs + 6 + 2 * lane), cB = lds_u16(vs + 6 + 2 * (lane + 32));
         const uint32_t iA = kvc_warp_incl_scan(cA, lane);
