@@ -282,10 +282,14 @@ store_kernel(StoreParams P, int stage_words) {
     if (tid == 0) sh_b = (ENCODE && !prescanned) ? (long)atomicAdd(&S.acc[0], 1ull) : (long)blockIdx.x;
     if (!ENCODE)
         for (int i = tid; i < 256; i += kThreads) sh_hist[i] = 0;
+    // hot encode path (head_dim 128, block 64, codes <= 8 bits): cw holds
+    // codeword << 8 | length, one shared load per code
+    const bool hot_enc = ENCODE && DT == 128 && BST == 64 && S.cb->max_len <= 8;
     if (ENCODE)
         for (int i = tid; i < 256; i += kThreads) {
-            cw[i] = S.cb->words[i];
-            cl[i] = S.cb->lengths[i];
+            const uint32_t w = S.cb->words[i], l = S.cb->lengths[i];
+            cw[i] = hot_enc ? ((w << 8) | l) : w;
+            cl[i] = (uint8_t)l;
         }
     __syncthreads();
     const long b = sh_b;
@@ -517,9 +521,7 @@ store_kernel(StoreParams P, int stage_words) {
     const uint32_t block_index = (P.chunk_base + (uint32_t)chunk) * (uint32_t)P.H_total +
                                  (uint32_t)(P.head_base + hl);
     uint32_t *img = reinterpret_cast<uint32_t *>(sm);
-    bool hot = false;
-    if constexpr (DT == 128 && BST == 64) hot = S.cb->max_len <= 8;
-    if (hot) {
+    if (hot_enc) {
         // hot shape, codes <= 8 bits: warp w owns rows w, w+8, ..; lane l the 4
         // codes 4l..4l+3 of a row (one 32-bit load), their codewords packed into
         // one <= 32-bit run kept in registers between the counts and the emission
@@ -532,10 +534,10 @@ store_kernel(StoreParams P, int stage_words) {
             uint32_t rn = 0, n = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const uint32_t sym = (w4 >> (8 * k)) & 0xFFu;
-                const uint32_t l = cl[sym];
+                const uint32_t e = cw[(w4 >> (8 * k)) & 0xFFu];
+                const uint32_t l = e & 0xFFu;
                 bad |= (l == 0);
-                rn = (rn << l) | cw[sym];
+                rn = (rn << l) | (e >> 8);
                 n += l;
             }
             run[i] = rn;
