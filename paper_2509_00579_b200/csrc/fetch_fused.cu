@@ -980,7 +980,7 @@ __device__ __forceinline__ void lds_vec(uint32_t addr, float *v) {
 // so the 32 lanes' row stores land in 32 distinct banks)
 constexpr int kTileRow = 68;
 __host__ __device__ constexpr int gqa_per_pair(int stage_k, int stage_v, int G, int vslots) {
-    return 2 * stage_k + vslots * stage_v + 4 * (G * D + 2 * G * BS + G * BS) + BS * kTileRow + 64;
+    return 2 * stage_k + vslots * stage_v + 4 * (G * D + 2 * G * BS + G * BS + 4) + BS * kTileRow + 64;
 }
 
 template <int G, int NP, int VS>
@@ -1002,7 +1002,9 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     float *qf = reinterpret_cast<float *>(pb + 2 * stage_k + VS * stage_v);  // [128][G]
     float *sring = qf + G * D;                                            // [2][G][64]
     float *sa = sring + 2 * G * BS;                                       // [64][G]
-    uint8_t *tile = reinterpret_cast<uint8_t *>(sa + G * BS);            // [64][68]
+    uint8_t *tile = reinterpret_cast<uint8_t *>(sa + G * BS + 4);        // [64][68]
+    // sa: weights [64][G], tokens 32..63 shifted by G floats so the two half-warps'
+    // broadcast loads in the GEMV land in different banks
     uint64_t *bar = reinterpret_cast<uint64_t *>(tile + BS * kTileRow);
     uint64_t *kfull = bar, *vfull = bar + 2, *sfull = bar + 4, *sempty = bar + 6;
 
@@ -1154,13 +1156,15 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
         if (n > 0) issue(true, 0);
         if (VS == 2 && n > 1) issue(true, 1);
     }
-    float m[G], lsum[G], wm[G], acc[G][4];  // lane owns channels 2l, 2l+1, 64+2l, 65+2l
+    // GEMV ownership: lane (cg = l & 15, th = l >> 4) sums channels 64*half + 4cg..+3
+    // over tokens 32*th..32*th+31; the two token halves are added at the end
+    float m[G], lsum[G], wm[G], acc[G][8];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         m[g] = -INFINITY;
         lsum[g] = wm[g] = 0.f;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc[g][k] = 0.f;
+        for (int k = 0; k < 8; ++k) acc[g][k] = 0.f;
     }
     const uint32_t lut_s = smem_u32(s_lutV), tile_s = smem_u32(tile), sa_s = smem_u32(sa);
     mbar_wait(s_lbar, 0);
@@ -1183,7 +1187,7 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
             if (bm > m[g]) {
                 const float alpha = exp2f(m[g] - bm);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) acc[g][k] *= alpha;
+                for (int k = 0; k < 8; ++k) acc[g][k] *= alpha;
                 lsum[g] *= alpha;
                 wm[g] *= alpha;
                 m[g] = bm;
@@ -1207,7 +1211,7 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             sa[lane * G + g] = pA[g] * scA;
-            sa[(lane + 32) * G + g] = pB[g] * scB;
+            sa[(lane + 32) * G + G + g] = pB[g] * scB;
             wm[g] = fmaf(pA[g], mnA, fmaf(pB[g], mnB, wm[g]));
         }
         // decode V slices A (token lane) and B (token lane+32) half by half:
@@ -1241,21 +1245,31 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
             }
             __syncwarp();
             if (VS == 1 && half == 1 && lane == 0 && j + 1 < n) issue(true, j + 1);  // slot consumed
-            // GEMV over the 64 tokens: lane owns channels 64*half + 2*lane, +1
+            // GEMV: 4 codes per 32-bit load; the upper half-warp walks its tokens
+            // rotated by 16 so the two halves read disjoint banks
+            {
+                const uint32_t cg = lane & 15, th = lane >> 4;
 #pragma unroll 4
-            for (int t = 0; t < BS; ++t) {
-                uint32_t w;
-                asm volatile(KVC_LD_SHARED ".u16 %0, [%1];" : "=r"(w) : "r"(tile_s + t * kTileRow + 2 * lane));
-                const float2 f01 = __fadd2_rn(make_float2(sym_hi_byte(w, 0x7650), sym_hi_byte(w, 0x7651)), magic);
-                float av[G];
-                lds_vec<G>(sa_s + 4 * G * t, av);
+                for (int t = 0; t < 32; ++t) {
+                    const int tok = th ? 32 + ((t + 16) & 31) : t;
+                    uint32_t w;
+                    asm volatile(KVC_LD_SHARED ".u32 %0, [%1];" : "=r"(w) : "r"(tile_s + tok * kTileRow + 4 * cg));
+                    const float2 f01 = __fadd2_rn(make_float2(sym_hi_byte(w, 0x7650), sym_hi_byte(w, 0x7651)), magic);
+                    const float2 f23 = __fadd2_rn(make_float2(sym_hi_byte(w, 0x7652), sym_hi_byte(w, 0x7653)), magic);
+                    float av[G];
+                    lds_vec<G>(sa_s + 4 * (G * tok + (th ? G : 0)), av);
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const float2 a2 = make_float2(av[g], av[g]);
-                    float2 ac = make_float2(acc[g][2 * half], acc[g][2 * half + 1]);
-                    ac = __ffma2_rn(f01, a2, ac);
-                    acc[g][2 * half] = ac.x;
-                    acc[g][2 * half + 1] = ac.y;
+                    for (int g = 0; g < G; ++g) {
+                        const float2 a2 = make_float2(av[g], av[g]);
+                        float2 x = make_float2(acc[g][4 * half], acc[g][4 * half + 1]);
+                        float2 y = make_float2(acc[g][4 * half + 2], acc[g][4 * half + 3]);
+                        x = __ffma2_rn(f01, a2, x);
+                        y = __ffma2_rn(f23, a2, y);
+                        acc[g][4 * half] = x.x;
+                        acc[g][4 * half + 1] = x.y;
+                        acc[g][4 * half + 2] = y.x;
+                        acc[g][4 * half + 3] = y.y;
+                    }
                 }
             }
             __syncwarp();
@@ -1269,10 +1283,15 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const float l = kvc_warp_sum(lsum[g]), w2 = kvc_warp_sum(wm[g]);
-        wp[g].o[2 * lane] = acc[g][0] + w2;
-        wp[g].o[2 * lane + 1] = acc[g][1] + w2;
-        wp[g].o[64 + 2 * lane] = acc[g][2] + w2;
-        wp[g].o[65 + 2 * lane] = acc[g][3] + w2;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[g][k] += __shfl_xor_sync(0xffffffffu, acc[g][k], 16);
+        if (lane < 16) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                wp[g].o[4 * lane + k] = acc[g][k] + w2;
+                wp[g].o[64 + 4 * lane + k] = acc[g][4 + k] + w2;
+            }
+        }
         if (lane == 0) {
             wp[g].m = m[g];
             wp[g].l = l;
