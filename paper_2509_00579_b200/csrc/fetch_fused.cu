@@ -1225,7 +1225,9 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
         const float2 magic = make_float2(-8388608.f, -8388608.f);
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-            // 32 pair steps; reload every 5 (the cadence restarts at each half)
+            // 32 pair steps; reload every 5 (the cadence restarts at each half);
+            // two steps' symbol pairs go out as one 32-bit store per slice
+            uint32_t pA = 0, pB = 0;
 #pragma unroll
             for (int t = 0; t < 32; ++t) {
                 if (t % 5 == 0) {
@@ -1240,8 +1242,13 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
                 cc[1].hi = __funnelshift_l(cc[1].lo, cc[1].hi, eB);
                 cc[1].lo = __funnelshift_l(0u, cc[1].lo, eB);
                 cc[1].p += eB;
-                asm volatile("st.shared.u16 [%0], %1;" ::"r"(rowA + 2 * t), "h"((unsigned short)(eA >> 16)));
-                asm volatile("st.shared.u16 [%0], %1;" ::"r"(rowB + 2 * t), "h"((unsigned short)(eB >> 16)));
+                if (t % 2 == 0) {
+                    pA = eA;
+                    pB = eB;
+                } else {
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(rowA + 2 * (t - 1)), "r"(__byte_perm(pA, eA, 0x7632)));
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(rowB + 2 * (t - 1)), "r"(__byte_perm(pB, eB, 0x7632)));
+                }
             }
             __syncwarp();
             if (VS == 1 && half == 1 && lane == 0 && j + 1 < n) issue(true, j + 1);  // slot consumed
