@@ -44,13 +44,16 @@ def worst_block_bytes(bs: int, n_units: int, head_dim: int, max_len: int) -> int
 class DeviceArena:
     """Append-only device byte arena + u32 block offsets + device counters."""
 
+    # Bytes past the cursor and offsets past n_blocks are never read as data
+    # (TMA over-reads of the last block's rounded extent and the decoder's window
+    # tail are don't-care bits), so the buffers are allocated without a memset.
     def __init__(self, device, capacity: Optional[int] = None, initial_bytes: int = 1 << 16,
                  initial_blocks: int = 256):
         self.device = torch.device(device)
         self.capacity = capacity  # user limit (None = grow on demand)
         alloc = initial_bytes if capacity is None else capacity
-        self._buf = torch.zeros(alloc + TMA_SLACK, dtype=torch.uint8, device=self.device)
-        self._offsets = torch.zeros(max(initial_blocks, 1), dtype=torch.int32, device=self.device)
+        self._buf = torch.empty(alloc + TMA_SLACK, dtype=torch.uint8, device=self.device)
+        self._offsets = torch.empty(max(initial_blocks, 1), dtype=torch.int32, device=self.device)
         self._counters = torch.zeros(ctypes.sizeof(_lib.ArenaCounters), dtype=torch.uint8,
                                      device=self.device)
         self.n_blocks = 0          # host mirror (deterministic)
@@ -61,7 +64,7 @@ class DeviceArena:
         """Make room for n_blocks more blocks of at most worst_bytes total."""
         need_blocks = self.n_blocks + n_blocks
         if need_blocks > self._offsets.numel():
-            new = torch.zeros(max(need_blocks, 2 * self._offsets.numel()), dtype=torch.int32,
+            new = torch.empty(max(need_blocks, 2 * self._offsets.numel()), dtype=torch.int32,
                               device=self.device)
             new[: self.n_blocks] = self._offsets[: self.n_blocks]
             self._offsets = new
@@ -70,7 +73,7 @@ class DeviceArena:
         need = self._bound + worst_bytes
         if need > self._buf.numel() - TMA_SLACK:
             new_cap = max(need, 2 * (self._buf.numel() - TMA_SLACK))
-            new = torch.zeros(new_cap + TMA_SLACK, dtype=torch.uint8, device=self.device)
+            new = torch.empty(new_cap + TMA_SLACK, dtype=torch.uint8, device=self.device)
             new[: self._buf.numel()] = self._buf
             self._buf = new
 
@@ -81,7 +84,7 @@ class DeviceArena:
         cur = int(self.counters().cursor)
         size = cur + headroom
         if size + TMA_SLACK < self._buf.numel():
-            new = torch.zeros(size + TMA_SLACK, dtype=torch.uint8, device=self.device)
+            new = torch.empty(size + TMA_SLACK, dtype=torch.uint8, device=self.device)
             new[:cur] = self._buf[:cur]
             self._buf = new
 
