@@ -12,6 +12,9 @@
 #include <cstring>
 #include <type_traits>
 #include <vector>
+#include <algorithm>
+#include <mutex>
+#include <cstdio>
 
 #include <cstdlib>
 
@@ -639,6 +642,25 @@ __device__ __forceinline__ void reduce_scatter_128(float2 (&acc)[D / 2], uint32_
 // the V warpgroup (128 f32 accumulators per lane), which lets 2 CTAs = 16
 // warps share an SM; every warp runs two independent decode chains.
 // ---------------------------------------------------------------------------
+// Context split plan of a fused launch: split s covers chunks [begin[s],
+// begin[s+1]) of every (seq, head).  Splits need not be equal: the host plans
+// a few large splits followed by small tail splits so the last wave of CTAs
+// is short (pick_split_plan).  The grid is 1D and split-major, so every
+// (seq, head)'s large splits launch before any tail split.
+constexpr int kMaxPlan = 48;
+struct SplitPlan {
+    int n;
+    int begin[kMaxPlan + 1];
+};
+__device__ __forceinline__ void plan_decode(const SplitPlan &plan, int H, int &split, int &h,
+                                            int &sidx) {
+    const int units = gridDim.x / plan.n;  // n_seqs * H
+    split = blockIdx.x / units;
+    const int r = blockIdx.x - split * units;
+    sidx = r / H;
+    h = r - sidx * H;
+}
+
 constexpr int WS_PAIRS = 4;
 constexpr int kThreadsWS = 2 * WS_PAIRS * 32;
 constexpr int kRegK = 80, kRegV = 176;  // (80 + 176) * 128 threads = 32768 regs per CTA
@@ -651,7 +673,7 @@ template <int MODE, int VMODE>
 __global__ void __launch_bounds__(kThreadsWS, 2)
 fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__restrict__ q,
                      float *__restrict__ scores, long ctx_stride, Partial *__restrict__ partial,
-                     int chunks_per_split, int n_splits, int stage_k, int stage_v, int *err) {
+                     const SplitPlan plan, int stage_k, int stage_v, int *err) {
     __shared__ __align__(128) uint32_t s_lutK[Dec<MODE>::kLutWords];
     __shared__ __align__(128) uint32_t s_lutV[Dec<VMODE>::kLutWords];
     __shared__ uint64_t s_lbar[1];
@@ -668,7 +690,9 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
     uint64_t *bar = reinterpret_cast<uint64_t *>(pb + 2 * (stage_k + stage_v) + 1024);
     uint64_t *kfull = bar, *vfull = bar + 2, *sfull = bar + 4, *sempty = bar + 6;
 
-    const int split = blockIdx.x, h = blockIdx.y, sidx = blockIdx.z;
+    const int n_splits = plan.n;
+    int split, h, sidx;
+    plan_decode(plan, H, split, h, sidx);
     const kvc_seq_desc sd = seqs[sidx];
     if (!is_v && lane == 0) {
         mbar_init(&kfull[0], 1);
@@ -694,8 +718,8 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
     if (!kPV) build_lut<VMODE>(s_lutV, sd.v_cb);
     if (!kPK || !kPV) __syncthreads();
 
-    const int c_begin = split * chunks_per_split;
-    const int c_end = min(sd.n_chunks, c_begin + chunks_per_split);
+    const int c_begin = plan.begin[split];
+    const int c_end = min(sd.n_chunks, plan.begin[split + 1]);
     const int first = c_begin + pair;
     const int n = first < c_end ? (c_end - first + WS_PAIRS - 1) / WS_PAIRS : 0;
     const float sm_scale = kLog2e / sqrtf((float)D);
@@ -986,7 +1010,7 @@ __host__ __device__ constexpr int gqa_per_pair(int stage_k, int stage_v, int G, 
 template <int G, int NP, int VS>
 __global__ void __launch_bounds__(NP * 64, 1)
 fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__restrict__ q,
-                      Partial *__restrict__ partial, int chunks_per_split, int n_splits,
+                      Partial *__restrict__ partial, const SplitPlan plan,
                       int stage_k, int stage_v, int *err) {
     __shared__ __align__(128) uint32_t s_lutK[1 << KVC_LUT_BITS];
     __shared__ __align__(128) uint32_t s_lutV[1 << KVC_LUT_BITS];
@@ -1008,7 +1032,9 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     uint64_t *bar = reinterpret_cast<uint64_t *>(tile + BS * kTileRow);
     uint64_t *kfull = bar, *vfull = bar + 2, *sfull = bar + 4, *sempty = bar + 6;
 
-    const int split = blockIdx.x, h = blockIdx.y, sidx = blockIdx.z;
+    const int n_splits = plan.n;
+    int split, h, sidx;
+    plan_decode(plan, H, split, h, sidx);
     const kvc_seq_desc sd = seqs[sidx];
     if (!is_v && lane == 0) {
         mbar_init(&kfull[0], 1);
@@ -1028,8 +1054,8 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
         tma_load_1d(s_lutK, sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
         tma_load_1d(s_lutV, sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
     }
-    const int c_begin = split * chunks_per_split;
-    const int c_end = min(sd.n_chunks, c_begin + chunks_per_split);
+    const int c_begin = plan.begin[split];
+    const int c_end = min(sd.n_chunks, plan.begin[split + 1]);
     const int first = c_begin + pair;
     const int n = first < c_end ? (c_end - first + NP - 1) / NP : 0;
     const float sm_scale = kLog2e / sqrtf((float)D);
@@ -1577,6 +1603,119 @@ int pick_chunks_per_split(int max_chunks, long n_heads_total, int ctas_per_sm = 
     return (int)best_cps;
 }
 
+// Launch-time model of a split plan: list-schedule the CTAs in launch order
+// (split-major) onto num_sms * ctas_per_sm slots, a CTA costing its chunks per
+// pair + the ~5 chunk-time start/drain of pick_chunks_per_split.  Returns the
+// makespan in chunk-times.
+double plan_makespan(const int *parts, int n_parts, long units, long slots, int pairs) {
+    std::vector<double> heap((size_t)slots, 0.0);  // min-heap of slot free times
+    auto greater = [](double a, double b) { return a > b; };
+    double end = 0.0;
+    for (int s = 0; s < n_parts; ++s) {
+        const double cost = (double)parts[s] / pairs + 5.0;
+        for (long u = 0; u < units; ++u) {
+            std::pop_heap(heap.begin(), heap.end(), greater);
+            const double t = heap.back() + cost;
+            heap.back() = t;
+            std::push_heap(heap.begin(), heap.end(), greater);
+            end = t > end ? t : end;
+        }
+    }
+    return end;
+}
+
+// Split plan for a fused launch.  Candidates: the uniform split of
+// pick_chunks_per_split, and "k large splits of b chunks + 1 or 2 tail
+// splits", whose short last CTAs fill the final wave instead of leaving SMs
+// idle behind a partial wave of full-length CTAs (config 2: 1280 uniform CTAs
+// are 4.3 waves of 296 slots).  The best modelled makespan wins; plans are
+// cached per shape.  KVC_FUSED_PLAN="144:144:144:80" overrides (experiments);
+// KVC_PLAN_VERBOSE=1 prints each planned shape to stderr.
+SplitPlan pick_split_plan(int max_chunks, long units, int ctas_per_sm, int pairs, int max_splits,
+                          int uniform_cps) {
+    SplitPlan plan{};
+    auto set_parts = [&](const std::vector<int> &parts) {
+        plan.n = (int)parts.size();
+        plan.begin[0] = 0;
+        for (int i = 0; i < plan.n; ++i) plan.begin[i + 1] = plan.begin[i] + parts[i];
+    };
+    if (const char *env = getenv("KVC_FUSED_PLAN")) {
+        std::vector<int> parts;
+        for (const char *c = env; *c;) {
+            const int v = atoi(c);
+            if (v > 0) parts.push_back(v);
+            while (*c && *c != ',' && *c != ':') ++c;
+            if (*c) ++c;
+        }
+        long tot = 0;
+        for (int v : parts) tot += v;
+        if (!parts.empty() && (int)parts.size() <= kMaxPlan && (int)parts.size() <= max_splits &&
+            tot >= max_chunks) {
+            set_parts(parts);
+            return plan;
+        }
+    }
+    if (max_splits > kMaxPlan) max_splits = kMaxPlan;
+    const int ucps = uniform_cps > 0 ? uniform_cps : max_chunks;
+    std::vector<int> best;
+    for (int c0 = 0; c0 < max_chunks; c0 += ucps) best.push_back(std::min(ucps, max_chunks - c0));
+    if (best.empty()) best.push_back(1);
+    const bool uniform_forced = getenv("KVC_FUSED_CPS") != nullptr || getenv("KVC_GQA_CPS") != nullptr;
+    if (!uniform_forced && max_chunks > 0 && (long)best.size() <= max_splits) {
+        struct Key {
+            int mc;
+            long units;
+            int cps_sm, pairs, ms, ucps;
+        };
+        static std::mutex mu;
+        static std::vector<std::pair<Key, std::vector<int>>> cache;
+        std::lock_guard<std::mutex> lock(mu);
+        for (auto &e : cache)
+            if (e.first.mc == max_chunks && e.first.units == units && e.first.cps_sm == ctas_per_sm &&
+                e.first.pairs == pairs && e.first.ms == max_splits && e.first.ucps == ucps) {
+                set_parts(e.second);
+                return plan;
+            }
+        const long slots = (long)num_sms() * ctas_per_sm;
+        double best_t = plan_makespan(best.data(), (int)best.size(), units, slots, pairs);
+        std::vector<int> cand;
+        auto consider = [&]() {
+            if ((int)cand.size() > max_splits) return;
+            const double t = plan_makespan(cand.data(), (int)cand.size(), units, slots, pairs);
+            if (t < best_t * (1.0 - 1e-3)) {
+                best_t = t;
+                best = cand;
+            }
+        };
+        for (int b = 4 * pairs; b < max_chunks; b += pairs) {
+            const int k = max_chunks / b;
+            for (int kk = k; kk >= 1 && kk >= k - 1; --kk) {
+                const int r = max_chunks - kk * b;
+                if (r <= 0 || r >= 2 * b) continue;
+                cand.assign(kk, b);
+                cand.push_back(r);
+                consider();
+                for (int t = pairs; t < r; t *= 2) {  // two tails: r - t, t
+                    cand.assign(kk, b);
+                    cand.push_back(r - t);
+                    cand.push_back(t);
+                    consider();
+                }
+            }
+        }
+        if (getenv("KVC_PLAN_VERBOSE")) {
+            fprintf(stderr, "[kvc] split plan chunks=%d units=%ld slots=%ld pairs=%d:", max_chunks,
+                    units, slots, pairs);
+            for (int v : best) fprintf(stderr, " %d", v);
+            fprintf(stderr, " (model %.1f chunk-times)\n", best_t);
+        }
+        if (cache.size() > 64) cache.clear();
+        cache.push_back({Key{max_chunks, units, ctas_per_sm, pairs, max_splits, ucps}, best});
+    }
+    set_parts(best);
+    return plan;
+}
+
 }  // namespace
 
 extern "C" size_t kvc_attention_workspace_bytes(int n_seqs, int H, int group, int D_, int max_chunks) {
@@ -1656,16 +1795,18 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
             const int v = atoi(cenv);
             if (v >= np && v % np == 0) g_cps = v;
         }
-        const int g_splits = (max_chunks + g_cps - 1) / g_cps;
+        const long g_max_sp = (long)(workspace_bytes / (sizeof(Partial) * (size_t)n_seqs * H * group));
+        const SplitPlan g_plan = pick_split_plan(max_chunks, (long)n_seqs * H, 1, np, (int)std::min(g_max_sp, 1L << 20), g_cps);
+        const int g_splits = g_plan.n;
         if (sizeof(Partial) * (size_t)n_seqs * H * group * g_splits > workspace_bytes)
             return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
-        dim3 g3(g_splits, H, n_seqs);
+        dim3 g3((unsigned)(g_splits * H * n_seqs));
 #define KVC_LAUNCH_GQA(GG, NPP, VSS)                                                                   \
     do {                                                                                            \
         KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_gqa_kernel<GG, NPP, VSS>,                         \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g_smem)); \
         fused_attn_gqa_kernel<GG, NPP, VSS><<<g3, NPP * 64, g_smem, s>>>(                                \
-            seqs_dev, H, q_dev, part, g_cps, g_splits, stage_k, stage_v, err_dev);                  \
+            seqs_dev, H, q_dev, part, g_plan, stage_k, stage_v, err_dev);                           \
     } while (0)
         if (group == 2) {
             if (np == 8) KVC_LAUNCH_GQA(2, 8, 1); else if (np == 6) KVC_LAUNCH_GQA(2, 6, 2); else KVC_LAUNCH_GQA(2, 4, 2);
@@ -1689,10 +1830,13 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
             const int v = atoi(cenv);
             if (v >= 4 && v % 4 == 0) ws_cps = v;
         }
-        const int ws_splits = (max_chunks + ws_cps - 1) / ws_cps;
+        const long ws_max_sp = (long)(workspace_bytes / (sizeof(Partial) * (size_t)n_seqs * H));
+        const SplitPlan ws_plan = pick_split_plan(max_chunks, (long)n_seqs * H, 2, WS_PAIRS,
+                                                  (int)std::min(ws_max_sp, 1L << 20), ws_cps);
+        const int ws_splits = ws_plan.n;
         if (sizeof(Partial) * (size_t)n_seqs * H * ws_splits > workspace_bytes)
             return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
-        dim3 g2(ws_splits, H, n_seqs);
+        dim3 g2((unsigned)(ws_splits * H * n_seqs));
         // V decoder: pair LUT (measured fastest); KVC_FUSED_VMODE=0 selects the
         // lane-replicated, bank-conflict-free single-symbol LUT6 instead.
         const char *venv = getenv("KVC_FUSED_VMODE");
@@ -1709,8 +1853,8 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,       \
                                           (int)ws_smem));                                    \
         fused_attn_ws_kernel<M, VM><<<g2, kThreadsWS, ws_smem, s>>>(                         \
-            seqs_dev, H, q_dev, scores_dev, ctx_stride, part, ws_cps, ws_splits, stage_k,    \
-            stage_v, err_dev);                                                               \
+            seqs_dev, H, q_dev, scores_dev, ctx_stride, part, ws_plan, stage_k, stage_v,     \
+            err_dev);                                                                        \
     } while (0)
         if (mode == 2) KVC_LAUNCH_WS(2, 2);
         else if (mode == 0) KVC_LAUNCH_WS(0, 0);
