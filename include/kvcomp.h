@@ -74,6 +74,10 @@ typedef struct {
      * (l0+l1) | s0<<16 | s1<<24; otherwise one: l0 | s0<<16.  Low 4 bits =
      * bits consumed, bits 4..15 zero. */
     uint32_t fetch_lut[1 << KVC_LUT_BITS];
+    /* fetch_lut with its bank bits swizzled: entry i stored at
+     * i ^ ((i >> 7) & 31), so the bank of a lookup is window bits 7-11 XOR
+     * bits 0-4 (fewer shared-memory bank conflicts for short V pairs). */
+    uint32_t fetch_lut_x[1 << KVC_LUT_BITS];
     uint32_t first_code[33];        /* canonical decode (lengths > 12)         */
     uint32_t count[33];
     uint32_t first_index[33];

@@ -49,6 +49,7 @@ class CodebookTables(ctypes.Structure):
     _fields_ = [("words", ctypes.c_uint32 * 256), ("lengths", ctypes.c_uint8 * 256),
                 ("lut", ctypes.c_uint32 * (1 << LUT_BITS)),
                 ("fetch_lut", ctypes.c_uint32 * (1 << LUT_BITS)),
+                ("fetch_lut_x", ctypes.c_uint32 * (1 << LUT_BITS)),
                 ("first_code", ctypes.c_uint32 * 33),
                 ("count", ctypes.c_uint32 * 33), ("first_index", ctypes.c_uint32 * 33),
                 ("sorted_symbols", ctypes.c_uint8 * 256), ("fetch_syms", ctypes.c_int32),

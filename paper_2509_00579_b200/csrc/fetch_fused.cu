@@ -152,7 +152,7 @@ __device__ __forceinline__ float sym_hi_byte(uint32_t e, uint32_t sel) {
 template <int MODE>
 struct Dec {
     static constexpr int kLutWords = MODE == 0 ? 64 * 32 : (1 << KVC_LUT_BITS);
-    static constexpr bool kPair = MODE == 1 || MODE == 3;  // the 4096-entry pair LUT (TMA-loaded)
+    static constexpr bool kPair = MODE == 1 || MODE == 3 || MODE == 4;  // the 4096-entry pair LUT (TMA-loaded)
     // symbols decodable from one 32-bit window; MODE 0 uses 4 (not 5) so the
     // reload cadence divides the unrolled loop (24 of 32 bits)
     static constexpr int kSymsPerWin = MODE == 0 ? 4 : (MODE == 1 ? 4 : 2);
@@ -520,6 +520,20 @@ __device__ __forceinline__ float2 cursor2_pair(Cursor2 &c, uint32_t lut_s) {
                       make_float2(-8388608.f, -8388608.f));
 }
 
+// Pair step on the bank-swizzled table (fetch_lut_x): byte address
+// ((hi >> 18) ^ (hi >> 25)) & 0x3FFC = 4 * (i ^ ((i >> 7) & 31)) for the 12-bit
+// window i, so the bank is window bits 7-11 XOR bits 0-4.  With short V pairs
+// bits 7-11 belong to the next pair and cluster across lanes (4.4-way
+// conflicts); the XOR spreads them (3.1-way, measured on config-2 streams).
+__device__ __forceinline__ float2 cursor2_pair_x(Cursor2 &c, uint32_t lut_s) {
+    const uint32_t e = lds32(lut_s + (((c.hi >> 18) ^ (c.hi >> 25)) & 0x3FFCu));
+    c.hi = __funnelshift_l(c.lo, c.hi, e);
+    c.lo = __funnelshift_l(0u, c.lo, e);
+    c.p += e;
+    return __fadd2_rn(make_float2(sym_hi_byte(e, 0x7652), sym_hi_byte(e, 0x7653)),
+                      make_float2(-8388608.f, -8388608.f));
+}
+
 // Pair step with the low 5 index bits replaced by the lane id (MODE 3).  The
 // last 5 bits of a 12-bit window are don't-care whenever the pair is <= 7
 // bits long, so entry (idx & ~31) | lane equals entry idx and the lookup of
@@ -712,7 +726,7 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
     if (kTma && threadIdx.x == 0) {
         mbar_expect_tx(s_lbar, ((int)kPK + (int)kPV) * (4u << KVC_LUT_BITS));
         if (kPK) tma_load_1d(s_lutK, sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
-        if (kPV) tma_load_1d(s_lutV, sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+        if (kPV) tma_load_1d(s_lutV, VMODE == 1 ? sd.v_cb->fetch_lut_x : sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
     }
     if (!kPK) build_lut<MODE>(s_lutK, sd.k_cb);
     if (!kPV) build_lut<VMODE>(s_lutV, sd.v_cb);
@@ -901,7 +915,7 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
         cursor_init(cur[0], slot, bit0 + iA - cA);
         cursor_init(cur[1], slot, bit0 + totA + iB - cB);
         const uint32_t p0A = cur[0].p, p0B = cur[1].p;
-        if (VMODE == 1 || VMODE == 0 || VMODE == 3) {
+        if (VMODE == 1 || VMODE == 0 || VMODE == 3 || VMODE == 4) {
             // 64-bit windows; 5 pair steps (<= 60 bits at max_len 6) per reload
             Cursor2 c2c[2];
             cursor2_init(c2c[0], slot, bit0 + iA - cA);
@@ -912,7 +926,10 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
                     cursor2_reload(c2c[0]);
                     cursor2_reload(c2c[1]);
                 }
-                if (VMODE == 1) {
+                if (VMODE == 1) {  // bank-swizzled pair table (fetch_lut_x)
+                    acc[c2] = __ffma2_rn(cursor2_pair_x(c2c[0], lut_s), aA2, acc[c2]);
+                    acc[c2] = __ffma2_rn(cursor2_pair_x(c2c[1], lut_s), aB2, acc[c2]);
+                } else if (VMODE == 4) {  // plain pair table
                     acc[c2] = __ffma2_rn(cursor2_pair(c2c[0], lut_s), aA2, acc[c2]);
                     acc[c2] = __ffma2_rn(cursor2_pair(c2c[1], lut_s), aB2, acc[c2]);
                 } else if (VMODE == 3) {
@@ -1052,7 +1069,7 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     if (threadIdx.x == 0) {
         mbar_expect_tx(s_lbar, 2u * (4u << KVC_LUT_BITS));
         tma_load_1d(s_lutK, sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
-        tma_load_1d(s_lutV, sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+        tma_load_1d(s_lutV, sd.v_cb->fetch_lut_x, 4u << KVC_LUT_BITS, s_lbar);  // bank-swizzled
     }
     const int c_begin = plan.begin[split];
     const int c_end = min(sd.n_chunks, plan.begin[split + 1]);
@@ -1260,11 +1277,11 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
                     cursor2_reload(cc[0]);
                     cursor2_reload(cc[1]);
                 }
-                const uint32_t eA = lds32(lut_s + ((cc[0].hi >> 20) << 2));
+                const uint32_t eA = lds32(lut_s + (((cc[0].hi >> 18) ^ (cc[0].hi >> 25)) & 0x3FFCu));
                 cc[0].hi = __funnelshift_l(cc[0].lo, cc[0].hi, eA);
                 cc[0].lo = __funnelshift_l(0u, cc[0].lo, eA);
                 cc[0].p += eA;
-                const uint32_t eB = lds32(lut_s + ((cc[1].hi >> 20) << 2));
+                const uint32_t eB = lds32(lut_s + (((cc[1].hi >> 18) ^ (cc[1].hi >> 25)) & 0x3FFCu));
                 cc[1].hi = __funnelshift_l(cc[1].lo, cc[1].hi, eB);
                 cc[1].lo = __funnelshift_l(0u, cc[1].lo, eB);
                 cc[1].p += eB;
@@ -1844,7 +1861,8 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         // = 3 select the lane-substituted lookups (-16% smem wavefronts, but +14%
         // instructions and a dependent second LDS: measured 9% slower, profiles/)
         int vmode = (mode == 2) ? 2 : 1;
-        if (mode != 2 && venv && (venv[0] == '0' || venv[0] == '1' || venv[0] == '3')) vmode = venv[0] - '0';
+        if (mode != 2 && venv && (venv[0] == '0' || venv[0] == '1' || venv[0] == '3' || venv[0] == '4'))
+            vmode = venv[0] - '0';
         const char *kenv = getenv("KVC_FUSED_KMODE");
         const int kmode = (mode == 1 && kenv && kenv[0] == '3') ? 3 : mode;
 #define KVC_LAUNCH_WS(M, VM)                                                                 \
@@ -1861,6 +1879,7 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         else if (kmode == 3 && vmode == 3) KVC_LAUNCH_WS(3, 3);
         else if (vmode == 0) KVC_LAUNCH_WS(1, 0);
         else if (vmode == 1) KVC_LAUNCH_WS(1, 1);
+        else if (vmode == 4) KVC_LAUNCH_WS(1, 4);
         else KVC_LAUNCH_WS(1, 3);
 #undef KVC_LAUNCH_WS
         int st = kvc_check_launch("fused_attn_ws_kernel");

@@ -112,6 +112,7 @@ static void build_fetch_lut(kvc_codebook_dev *t) {
             t->fetch_lut[i] = l0 | (s0 << 16);
         }
     }
+    for (uint32_t i = 0; i < (1u << KVC_LUT_BITS); ++i) t->fetch_lut_x[i ^ ((i >> 7) & 31u)] = t->fetch_lut[i];
 }
 
 extern "C" int kvc_codebook_build_tables(const uint8_t *lengths, kvc_codebook_dev *t) {
