@@ -10,6 +10,7 @@ host reads them only when asked (stats, snapshot, error checks).
 from __future__ import annotations
 
 import ctypes
+import weakref
 from dataclasses import dataclass
 from typing import Optional, Tuple
 
@@ -20,6 +21,86 @@ from . import _lib
 from .errors import ArenaFullError, CodecError
 
 TMA_SLACK = 64  # bytes after the cursor the fetch kernel may over-read
+
+
+class _SlabPool:
+    """Arena byte buffers carved from large per-device slabs.
+
+    Compressed states live for the whole decode, so with the caching allocator
+    every prefill's arenas are fresh cudaMalloc calls (~0.3 ms each, with
+    multi-ms outliers).  Arenas instead take first-fit extents of 1 GiB slabs
+    (``KVC_ARENA_SLAB_MB``), returned when the arena grows, shrinks or is
+    collected.  Extents are stream-ordered like the caching allocator's blocks:
+    a released extent may be reused by work enqueued after the release.
+    """
+
+    ALIGN = 256
+
+    def __init__(self, device: torch.device):
+        import os
+        self.device = device
+        self.slab_bytes = int(os.environ.get("KVC_ARENA_SLAB_MB", "1024")) << 20
+        self.slabs = []   # torch uint8 tensors
+        self.free = []    # per slab: sorted list of [offset, size]
+
+    def alloc(self, nbytes: int):
+        n = max(self.ALIGN, (int(nbytes) + self.ALIGN - 1) // self.ALIGN * self.ALIGN)
+        for si, fl in enumerate(self.free):
+            for i, (off, size) in enumerate(fl):
+                if size >= n:
+                    if size == n:
+                        del fl[i]
+                    else:
+                        fl[i] = [off + n, size - n]
+                    return self.slabs[si][off: off + n], _Extent(self, si, off, n)
+        slab = max(self.slab_bytes, (n + (2 << 20) - 1) // (2 << 20) * (2 << 20))
+        self.slabs.append(torch.empty(slab, dtype=torch.uint8, device=self.device))
+        self.free.append([[n, slab - n]] if slab > n else [])
+        return self.slabs[-1][:n], _Extent(self, len(self.slabs) - 1, 0, n)
+
+    def release(self, si: int, off: int, n: int) -> None:
+        fl = self.free[si]
+        lo, hi = 0, len(fl)
+        while lo < hi:
+            mid = (lo + hi) // 2
+            if fl[mid][0] < off:
+                lo = mid + 1
+            else:
+                hi = mid
+        fl.insert(lo, [off, n])
+        if lo + 1 < len(fl) and fl[lo][0] + fl[lo][1] == fl[lo + 1][0]:
+            fl[lo][1] += fl[lo + 1][1]
+            del fl[lo + 1]
+        if lo > 0 and fl[lo - 1][0] + fl[lo - 1][1] == fl[lo][0]:
+            fl[lo - 1][1] += fl[lo][1]
+            del fl[lo]
+
+
+class _Extent:
+    __slots__ = ("pool", "si", "off", "n", "live")
+
+    def __init__(self, pool, si, off, n):
+        self.pool, self.si, self.off, self.n, self.live = pool, si, off, n, True
+
+    def release(self) -> None:
+        if self.live:
+            self.live = False
+            self.pool.release(self.si, self.off, self.n)
+
+
+_POOLS = {}
+
+
+def _pool(device: torch.device) -> _SlabPool:
+    idx = device.index
+    if idx is None and device.type == "cuda":
+        idx = torch.cuda.current_device()
+    key = (device.type, idx)
+    p = _POOLS.get(key)
+    if p is None:
+        p = _POOLS[key] = _SlabPool(torch.device(device.type, idx) if idx is not None
+                                    else torch.device(device.type))
+    return p
 
 
 @dataclass
@@ -52,12 +133,26 @@ class DeviceArena:
         self.device = torch.device(device)
         self.capacity = capacity  # user limit (None = grow on demand)
         alloc = initial_bytes if capacity is None else capacity
-        self._buf = torch.empty(alloc + TMA_SLACK, dtype=torch.uint8, device=self.device)
+        self._extent = None
+        self._set_buf(alloc + TMA_SLACK)
         self._offsets = torch.empty(max(initial_blocks, 1), dtype=torch.int32, device=self.device)
         self._counters = torch.zeros(ctypes.sizeof(_lib.ArenaCounters), dtype=torch.uint8,
                                      device=self.device)
         self.n_blocks = 0          # host mirror (deterministic)
         self._bound = 0            # host upper bound on the cursor
+
+    def _set_buf(self, nbytes: int, keep: int = 0) -> None:
+        """(Re)allocate the byte buffer from the slab pool, copying the first
+        ``keep`` bytes; the previous extent goes back to the pool."""
+        buf, ext = _pool(self.device).alloc(nbytes)
+        buf = buf[:nbytes]
+        if keep:
+            buf[:keep] = self._buf[:keep]
+        old = self._extent
+        self._buf, self._extent = buf, ext
+        weakref.finalize(self, ext.release)
+        if old is not None:
+            old.release()
 
     # ---- growth -------------------------------------------------------
     def reserve(self, n_blocks: int, worst_bytes: int) -> None:
@@ -73,9 +168,7 @@ class DeviceArena:
         need = self._bound + worst_bytes
         if need > self._buf.numel() - TMA_SLACK:
             new_cap = max(need, 2 * (self._buf.numel() - TMA_SLACK))
-            new = torch.empty(new_cap + TMA_SLACK, dtype=torch.uint8, device=self.device)
-            new[: self._buf.numel()] = self._buf
-            self._buf = new
+            self._set_buf(new_cap + TMA_SLACK, keep=self._buf.numel())
 
     def compact(self, headroom: int = 0) -> None:
         """Shrink the allocation to the written bytes (+headroom) after a big prefill."""
@@ -84,9 +177,7 @@ class DeviceArena:
         cur = int(self.counters().cursor)
         size = cur + headroom
         if size + TMA_SLACK < self._buf.numel():
-            new = torch.empty(size + TMA_SLACK, dtype=torch.uint8, device=self.device)
-            new[:cur] = self._buf[:cur]
-            self._buf = new
+            self._set_buf(size + TMA_SLACK, keep=cur)
 
     def load(self, data: bytes, offsets: np.ndarray, counters: bytes, headroom: int = 1 << 16):
         """Replace the contents with serialised blocks (container restore)."""
@@ -96,7 +187,8 @@ class DeviceArena:
             raise ArenaFullError("restored arena exceeds capacity")
         buf = torch.zeros(cap + TMA_SLACK, dtype=torch.uint8)
         buf[:n] = torch.frombuffer(bytearray(data), dtype=torch.uint8) if n else buf[:0]
-        self._buf = buf.to(self.device)
+        self._set_buf(cap + TMA_SLACK)
+        self._buf.copy_(buf)
         nb = len(offsets)
         offs = torch.zeros(max(nb, 1), dtype=torch.int32)
         if nb:

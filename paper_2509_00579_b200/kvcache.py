@@ -38,7 +38,8 @@ class LayerCacheState:
     def __init__(self, head_num: int, head_dim: int, cfg_k: QuantConfig, cfg_v: QuantConfig,
                  k_codebook: HuffmanCodebook, v_codebook: HuffmanCodebook, dtype=np.float32,
                  k_channel_ranges=None, device=None, head_base: int = 0,
-                 head_total: Optional[int] = None, capacity: Optional[int] = None):
+                 head_total: Optional[int] = None, capacity: Optional[int] = None,
+                 arena_bytes: Optional[Tuple[int, int]] = None, arena_blocks: int = 256):
         if not cfg_k.mode.is_key:
             raise ConfigError("cfg_k must use a K quantization mode")
         if cfg_v.mode is not QuantMode.V_TOKEN:
@@ -69,8 +70,13 @@ class LayerCacheState:
             self.k_channel_ranges = (t[0].numpy(), t[1].numpy())
         self.head_base = head_base
         self.head_total = head_total if head_total is not None else head_num
-        self.k_arena = DeviceArena(self.device, capacity)
-        self.v_arena = DeviceArena(self.device, capacity)
+        # arena_bytes: initial allocations sized by the caller (prefill knows a
+        # tight bound), so the prefill does not grow 64 KB arenas by a copy
+        ka, va = arena_bytes if arena_bytes is not None else (1 << 16, 1 << 16)
+        self.k_arena = DeviceArena(self.device, capacity, initial_bytes=ka,
+                                   initial_blocks=arena_blocks)
+        self.v_arena = DeviceArena(self.device, capacity, initial_bytes=va,
+                                   initial_blocks=arena_blocks)
         cap = cfg_k.buffer_size + 1
         self._k_buffer = torch.zeros((cap, head_num, head_dim), dtype=torch.float32,
                                      device=self.device)
@@ -171,14 +177,36 @@ class LayerCacheState:
             v_cb = build_smoothed_codebook(h[256:], cfg_v.max_code)
         else:
             k_cb, v_cb = codebooks
+        # Arena sizes: the histogram gives every prefill block's code bits, so
+        # sum(count * length) / 8 + (header + 4 B of byte/word padding) per block
+        # bounds each arena (codec.py:229-244) far tighter than the max-length
+        # worst case; a little headroom covers the first growing-cache appends.
+        nb = n_chunks * H
+        bounds = None
+        if codebooks is None and n_full:
+            bounds = []
+            for cb, hh, n_units in ((k_cb, h[:256], D), (v_cb, h[256:], bs)):
+                bits = int((hh.astype(np.uint64) * cb.code_lengths.astype(np.uint64)).sum())
+                tight = nb * (6 + 2 * bs + 8 * n_units + 4) + (bits + 7) // 8
+                worst = nb * worst_block_bytes(bs, n_units, D, cb.max_code_length)
+                bounds.append(min(tight, worst))
+        head = 2 * H * max(worst_block_bytes(bs, D, D, k_cb.max_code_length),
+                           worst_block_bytes(bs, bs, D, v_cb.max_code_length))
+        arena_bytes = None
+        if capacity is None and n_full:
+            arena_bytes = ((bounds[0] if bounds else nb * worst_block_bytes(
+                bs, D, D, k_cb.max_code_length)) + head,
+                (bounds[1] if bounds else nb * worst_block_bytes(
+                    bs, bs, D, v_cb.max_code_length)) + head)
         st = cls(H, D, cfg_k, cfg_v, k_cb, v_cb, dtype=src_dtype, device=kt.device,
                  head_base=head_base, head_total=head_total, capacity=capacity,
-                 k_channel_ranges=k_channel_ranges)
+                 k_channel_ranges=k_channel_ranges, arena_bytes=arena_bytes,
+                 arena_blocks=max(nb + 4 * H, 256))
         if n_full:
             if blk_hist is not None and st._fused_store:
-                st._store(kt, vt, n_chunks, blk_hist=blk_hist, blk_codes=blk_codes)
+                st._store(kt, vt, n_chunks, blk_hist=blk_hist, blk_codes=blk_codes, bounds=bounds)
             elif st._fused_store:
-                st._store(kt, vt, n_chunks)
+                st._store(kt, vt, n_chunks, bounds=bounds)
             else:
                 if kcodes is None:
                     kcodes, kmetas = quantize_tokens(kt, n_chunks, H, D, bs, cfg_k.mode,
@@ -186,6 +214,9 @@ class LayerCacheState:
                     vcodes, vmetas = quantize_tokens(vt, n_chunks, H, D, bs, QuantMode.V_TOKEN,
                                                      cfg_v.rel_quant_scale)
                 st._encode(kcodes, kmetas, vcodes, vmetas, n_chunks)
+        # the prefill workspace goes back to the allocator's cache for the next
+        # prefill; appends size their own
+        st._ws = torch.empty(0, dtype=torch.uint8, device=st.device)
         r = ctx - n_full
         if r:
             st._k_buffer[:r] = kt[n_full:].to(torch.float32)
@@ -225,7 +256,8 @@ class LayerCacheState:
 
     def _store(self, k_src: torch.Tensor, v_src: torch.Tensor, n_chunks: int,
                blk_hist: Optional[torch.Tensor] = None,
-               blk_codes: Optional[torch.Tensor] = None) -> None:
+               blk_codes: Optional[torch.Tensor] = None,
+               bounds: Optional[Tuple[int, int]] = None) -> None:
         """Quantise + encode + append of n_chunks*H blocks per tensor from
         k_src/v_src rows [0, n_chunks*bs) (store_fused.cu): one look-back launch
         (kvc_store_append), or, with the prefill's per-block histograms, the
@@ -235,6 +267,8 @@ class LayerCacheState:
         nb = n_chunks * H
         kw = nb * worst_block_bytes(bs, D, D, self.k_codebook.max_code_length)
         vw = nb * worst_block_bytes(bs, bs, D, self.v_codebook.max_code_length)
+        if bounds is not None:  # exact-histogram bounds from the prefill
+            kw, vw = min(kw, bounds[0]), min(vw, bounds[1])
         self.k_arena.reserve(nb, kw)
         self.v_arena.reserve(nb, vw)
         ws = self._workspace(lib.kvc_store_workspace_bytes(n_chunks, H, D, bs))

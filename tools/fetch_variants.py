@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5])
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--ctx", type=int, default=None)
+    ap.add_argument("--heads", type=int, default=None)
     ap.add_argument("--variants", default="base")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--check", action="store_true", help="compare every variant's output with base")
@@ -34,7 +35,7 @@ def main():
     p = dict(bench.PRESETS[a.config])
     B = a.batch or p["batch"]
     T = a.ctx or p["ctx"]
-    H, G = p["heads"], p["group"]
+    H, G = a.heads or p["heads"], p["group"]
     dev = torch.device("cuda", 0)
     states, _, _ = bench.build_cache(kv, torch, 1, B, T, H, 0, H, dev)
     row = states[0]
