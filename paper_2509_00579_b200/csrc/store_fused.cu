@@ -379,6 +379,59 @@ store_kernel(StoreParams P, int stage_words) {
             u_sc[tid] = sc;
             u_r[tid] = sc > 0.f ? __frcp_rn(sc) : 0.f;
         }
+    } else if (DT == 128 && BST == 64 && kWarps == 8) {
+        // V: warp w owns rows w, w+8, .., w+56; lane -> 4 consecutive values of
+        // each.  The 8 rows' (min, max) are reduced together by a halving
+        // reduce-scatter over the 16 values per lane (16 shuffles for 8 rows
+        // instead of 10 per row); lane pair (2i, 2i+1) ends with slot i =
+        // (row w + 8*(i>>1), min if i even else max) and computes its scale.
+        float v16[16];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int r = warp + 8 * k;
+            float v[4];
+            if constexpr (sizeof(T) == 2) {
+                const uint2 u = *reinterpret_cast<const uint2 *>(stage + r * 128 + 4 * lane);
+                const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&u.x));
+                const float2 b2 = __half22float2(*reinterpret_cast<const __half2 *>(&u.y));
+                v[0] = a.x; v[1] = a.y; v[2] = b2.x; v[3] = b2.y;
+            } else {
+                const float4 u = *reinterpret_cast<const float4 *>(stage + r * 128 + 4 * lane);
+                v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+            }
+            v16[2 * k] = fminf(fminf(v[0], v[1]), fminf(v[2], v[3]));
+            v16[2 * k + 1] = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+        }
+        // slot s in [0,16): even = min, odd = max of row s >> 1.  Steps xor 16,
+        // 8, 4 keep the half of the live slots selected by that lane bit and
+        // combine the partner's copy (halves have even length, so slot parity =
+        // index parity); then each lane holds (min, max) of row
+        // k = 4*bit4 + 2*bit3 + bit2 over 8 lanes, and xor 2, 1 finish it.
+#pragma unroll
+        for (int o = 16, n = 8; o >= 4; o >>= 1, n >>= 1) {
+            const bool hi = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (i < n) {
+                    const float keep = hi ? v16[n + i] : v16[i], send = hi ? v16[i] : v16[n + i];
+                    const float other = __shfl_xor_sync(0xffffffffu, send, o);
+                    v16[i] = (i & 1) ? fmaxf(keep, other) : fminf(keep, other);
+                }
+            }
+        }
+        float lo = v16[0], hi = v16[1];
+#pragma unroll
+        for (int o = 2; o >= 1; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if ((lane & 3) == 0) {
+            const int r = warp + 8 * (4 * ((lane >> 4) & 1) + 2 * ((lane >> 3) & 1) + ((lane >> 2) & 1));
+            const float sc = (float)__dmul_rn(S.rel, __dsub_rn((double)hi, (double)lo));
+            u_lo[r] = lo;
+            u_sc[r] = sc;
+            u_r[r] = sc > 0.f ? __frcp_rn(sc) : 0.f;
+        }
     } else if (DT == 128 && BST == 64) {
         // V: warp per row, lane -> 4 consecutive values (one vector load)
 #pragma unroll 2
