@@ -288,7 +288,9 @@ store_kernel(StoreParams P, int stage_words) {
     if (ENCODE)
         for (int i = tid; i < 256; i += kThreads) {
             const uint32_t w = S.cb->words[i], l = S.cb->lengths[i];
-            cw[i] = hot_enc ? ((w << 8) | l) : w;
+            // hot: codeword left-aligned, length in the low bits (l <= 8, so the
+            // two fields never overlap): one funnel shift appends a code
+            cw[i] = hot_enc ? (l ? ((w << (32 - l)) | l) : 0u) : w;
             cl[i] = (uint8_t)l;
         }
     __syncthreads();
@@ -579,26 +581,37 @@ store_kernel(StoreParams P, int stage_words) {
         // codes 4l..4l+3 of a row (one 32-bit load), their codewords packed into
         // one <= 32-bit run kept in registers between the counts and the emission
         constexpr int RW = 64 / kWarps;
-        uint32_t run[RW], ex[RW];
+        static_assert(RW % 2 == 0, "rows are scanned in pairs");
+        uint32_t run[RW], ex[RW], nn[RW];
 #pragma unroll
         for (int i = 0; i < RW; ++i) {
             const int r = warp + kWarps * i;
             const uint32_t w4 = *reinterpret_cast<const uint32_t *>(codes + r * 128 + 4 * lane);
-            uint32_t rn = 0, n = 0;
+            uint32_t rn = 0, nsum = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const uint32_t e = cw[(w4 >> (8 * k)) & 0xFFu];
-                const uint32_t l = e & 0xFFu;
-                bad |= (l == 0);
-                rn = (rn << l) | (e >> 8);
-                n += l;
+                // entry = codeword << (32 - l) | l (0 = symbol absent)
+                const uint32_t e = cw[__byte_perm(w4, 0u, 0x4440u | k)];
+                bad |= (e == 0);
+                rn = __funnelshift_l(e, rn, e);  // (rn << l) | codeword
+                nsum += e;                       // low 6 bits: sum of the 4 lengths
             }
             run[i] = rn;
-            const uint32_t inc = kvc_warp_incl_scan(n, lane);
-            ex[i] = (inc - n) | (n << 24);
-            if (lane == 31) {
-                s_bits[r] = inc;
-                bad |= inc > 0xFFFFu;
+            nn[i] = nsum & 63u;
+        }
+        // two rows per scan: a row's lane-run totals are <= 1024 bits, so the
+        // 16-bit halves never carry into each other
+#pragma unroll
+        for (int i = 0; i < RW; i += 2) {
+            const uint32_t inc2 = kvc_warp_incl_scan(nn[i] | (nn[i + 1] << 16), lane);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t n = nn[i + h], inc = h ? (inc2 >> 16) : (inc2 & 0xFFFFu);
+                ex[i + h] = (inc - n) | (n << 24);
+                if (lane == 31) {
+                    s_bits[warp + kWarps * (i + h)] = inc;
+                    bad |= inc > 0xFFFFu;
+                }
             }
         }
         if (bad) kvc_set_err(P.err, KVC_ERR_CODEC);
