@@ -13,7 +13,7 @@ from .attention import (AttentionOutput, attention_batched, attention_gqa, atten
 from .codebook import (HuffmanCodebook, build_codebook, build_histogram, build_smoothed_codebook,
                        codebook_from_lengths, deserialize_codebook, histogram_entropy,
                        serialize_codebook, smooth_histogram)
-from .codec import DataMovement, DeviceArena
+from .codec import DataMovement, DeviceArena, reserve_arena_pool
 from .container import load_state, read_header, save_state
 from .errors import (ArenaFullError, CodebookError, CodecError, ConfigError,
                      ContainerFormatError, KvpackError, TensorFormatError)

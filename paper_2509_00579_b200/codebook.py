@@ -78,8 +78,8 @@ class HuffmanCodebook:
         key = str(torch.device(device))
         t = self._device.get(key)
         if t is None:
-            raw = np.frombuffer(bytes(self.tables), dtype=np.uint8).copy()
-            t = torch.from_numpy(raw).to(device)
+            # straight from the ctypes struct's memory (no intermediate copies)
+            t = torch.frombuffer(self.tables, dtype=torch.uint8).to(device)
             self._device[key] = t
         return t
 

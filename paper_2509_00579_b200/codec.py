@@ -45,6 +45,15 @@ class _SlabPool:
 
     def alloc(self, nbytes: int):
         n = max(self.ALIGN, (int(nbytes) + self.ALIGN - 1) // self.ALIGN * self.ALIGN)
+        # fast path: the tail of the newest slab (prefills carve slabs in order)
+        if self.free and self.free[-1] and self.free[-1][-1][1] >= n:
+            si = len(self.free) - 1
+            off, size = self.free[si][-1]
+            if size == n:
+                self.free[si].pop()
+            else:
+                self.free[si][-1] = [off + n, size - n]
+            return self.slabs[si][off: off + n], _Extent(self, si, off, n)
         for si, fl in enumerate(self.free):
             for i, (off, size) in enumerate(fl):
                 if size >= n:
@@ -89,6 +98,25 @@ class _Extent:
 
 
 _POOLS = {}
+
+
+def reserve_arena_pool(nbytes: int, device=None) -> int:
+    """Pre-grow the arena slab pool of `device` to >= nbytes of free space.
+
+    Fresh device memory costs ~3-5 us per MB to map (cudaMalloc), so a serving
+    process reserves its compressed-cache memory once at startup (as paged KV
+    managers reserve their block pool) instead of inside each prefill.
+    Returns the pool's total free bytes."""
+    dev = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    pool = _pool(dev)
+    free = sum(sz for fl in pool.free for _, sz in fl)
+    while free < nbytes:
+        slab = pool.slab_bytes
+        pool.slabs.append(torch.empty(slab, dtype=torch.uint8, device=pool.device))
+        pool.free.append([[0, slab]])
+        free += slab
+    return free
 
 
 def _pool(device: torch.device) -> _SlabPool:

@@ -39,7 +39,8 @@ class LayerCacheState:
                  k_codebook: HuffmanCodebook, v_codebook: HuffmanCodebook, dtype=np.float32,
                  k_channel_ranges=None, device=None, head_base: int = 0,
                  head_total: Optional[int] = None, capacity: Optional[int] = None,
-                 arena_bytes: Optional[Tuple[int, int]] = None, arena_blocks: int = 256):
+                 arena_bytes: Optional[Tuple[int, int]] = None, arena_blocks: int = 256,
+                 _pre: Optional[dict] = None):
         if not cfg_k.mode.is_key:
             raise ConfigError("cfg_k must use a K quantization mode")
         if cfg_v.mode is not QuantMode.V_TOKEN:
@@ -78,9 +79,12 @@ class LayerCacheState:
         self.v_arena = DeviceArena(self.device, capacity, initial_bytes=va,
                                    initial_blocks=arena_blocks)
         cap = cfg_k.buffer_size + 1
-        self._k_buffer = torch.zeros((cap, head_num, head_dim), dtype=torch.float32,
-                                     device=self.device)
-        self._v_buffer = torch.zeros_like(self._k_buffer)
+        if _pre is not None:  # allocated by prefill while its pass A ran
+            self._k_buffer, self._v_buffer = _pre["k_buffer"], _pre["v_buffer"]
+        else:
+            self._k_buffer = torch.zeros((cap, head_num, head_dim), dtype=torch.float32,
+                                         device=self.device)
+            self._v_buffer = torch.zeros_like(self._k_buffer)
         self._k_tab = k_codebook.device_tables(self.device)
         self._v_tab = v_codebook.device_tables(self.device)
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
@@ -169,6 +173,14 @@ class LayerCacheState:
             vcodes, vmetas = quantize_tokens(vt, n_chunks, H, D, bs, QuantMode.V_TOKEN,
                                              cfg_v.rel_quant_scale,
                                              hist[256:] if codebooks is None else None)
+        # everything that does not depend on the histogram is allocated while
+        # pass A runs, so the host work between its completion and pass B is
+        # only the codebook build, the table upload and the arena carve-out
+        cap = cfg_k.buffer_size + 1
+        pre = {"k_buffer": torch.zeros((cap, H, D), dtype=torch.float32, device=kt.device)}
+        pre["v_buffer"] = torch.zeros_like(pre["k_buffer"])
+        pre_ws = (torch.empty(lib.kvc_store_workspace_bytes(n_chunks, H, D, bs), dtype=torch.uint8,
+                              device=kt.device) if n_full and fused else None)
         if codebooks is None:
             if process_group is not None:
                 torch.distributed.all_reduce(hist, group=process_group)
@@ -201,7 +213,9 @@ class LayerCacheState:
         st = cls(H, D, cfg_k, cfg_v, k_cb, v_cb, dtype=src_dtype, device=kt.device,
                  head_base=head_base, head_total=head_total, capacity=capacity,
                  k_channel_ranges=k_channel_ranges, arena_bytes=arena_bytes,
-                 arena_blocks=max(nb + 4 * H, 256))
+                 arena_blocks=max(nb + 4 * H, 256), _pre=pre)
+        if pre_ws is not None:
+            st._ws = pre_ws
         if n_full:
             if blk_hist is not None and st._fused_store:
                 st._store(kt, vt, n_chunks, blk_hist=blk_hist, blk_codes=blk_codes, bounds=bounds)

@@ -1,5 +1,6 @@
-import cProfile, pstats, time, sys, torch
-sys.path.insert(0, '.')
+"""Host-side profile of LayerCacheState.prefill (cProfile, sorted by cumulative time)."""
+import cProfile, pstats, time, sys, os, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2509_00579_b200 as kv
 dev = torch.device('cuda', 0)
 for (T, H) in ((32768, 40), (131072, 8)):
@@ -9,16 +10,18 @@ for (T, H) in ((32768, 40), (131072, 8)):
     kv.generate_synthetic_device(kv.SyntheticSpec(T, H, 128, seed=2), dev, out=v)
     ck, cv = kv.QuantConfig(kv.QuantMode.K_BLOCK), kv.QuantConfig(kv.QuantMode.V_TOKEN)
     keep = []
+    kv.reserve_arena_pool(8 << 30, dev)
     for _ in range(3):
         keep.append(kv.LayerCacheState.prefill(k, v, ck, cv, check=False))
     torch.cuda.synchronize()
     ts = []
-    for _ in range(5):
+    for _ in range(8):
         t0 = time.perf_counter(); st = kv.LayerCacheState.prefill(k, v, ck, cv, check=False); torch.cuda.synchronize(); ts.append(time.perf_counter() - t0); keep.append(st)
     print(T, H, 'prefill ms', [round(t * 1e3, 3) for t in ts])
     pr = cProfile.Profile(); pr.enable()
-    for _ in range(5):
+    for _ in range(10):
         keep.append(kv.LayerCacheState.prefill(k, v, ck, cv, check=False))
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
     pr.disable()
-    pstats.Stats(pr).sort_stats('tottime').print_stats(14)
+    pstats.Stats(pr).sort_stats('tottime').print_stats(18)
+    break

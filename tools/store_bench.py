@@ -8,6 +8,7 @@ Times, with CUDA events on the launching stream:
     through LayerCacheState._store, i.e. one kvc_store_append launch.
 Prints one JSON line.
 """
+import gc
 import json
 import os
 import sys
@@ -26,6 +27,20 @@ def ev():
 
 
 def main(ctx=32768, H=40, D=128, reps=10):
+    # timed regions run with the cyclic GC off (as timeit does): in a process
+    # holding hundreds of compressed states a collection costs milliseconds,
+    # which the ~20 us append events would otherwise absorb at random
+    gc_was = gc.isenabled()
+    gc.collect()
+    gc.disable()
+    try:
+        return _main(ctx, H, D, reps)
+    finally:
+        if gc_was:
+            gc.enable()
+
+
+def _main(ctx, H, D, reps):
     dev = torch.device("cuda")
     k = kv.generate_synthetic_device(kv.SyntheticSpec(ctx, H, D, seed=0), dev)
     v = kv.generate_synthetic_device(kv.SyntheticSpec(ctx, H, D, seed=1), dev)
