@@ -75,13 +75,49 @@ class HuffmanCodebook:
 
     def device_tables(self, device) -> torch.Tensor:
         """The kvc_codebook_dev blob on `device` (uploaded once, cached)."""
-        key = str(torch.device(device))
+        dev = torch.device(device)
+        key = str(dev)
         t = self._device.get(key)
         if t is None:
-            # straight from the ctypes struct's memory (no intermediate copies)
-            t = torch.frombuffer(self.tables, dtype=torch.uint8).to(device)
+            t = _upload(self.tables, dev)
             self._device[key] = t
         return t
+
+
+class _PinnedStage:
+    """Ring of pinned host buffers for the codebook-table uploads: an upload
+    is one memmove plus an asynchronous H2D copy (a pageable copy of the 52 KB
+    blob is synchronous, ~50 us).  A slot is rewritten only after the event of
+    its previous copy has completed."""
+
+    def __init__(self, nbytes: int, slots: int = 8):
+        self.bufs = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(slots)]
+        self.events = [None] * slots
+        self.i = 0
+
+
+_STAGE = {}
+
+
+def _upload(tables, dev: torch.device) -> torch.Tensor:
+    n = ctypes.sizeof(tables)
+    if dev.type != "cuda":
+        return torch.frombuffer(bytearray(bytes(tables)), dtype=torch.uint8).to(dev)
+    stage = _STAGE.get(n)
+    if stage is None:
+        stage = _STAGE[n] = _PinnedStage(n)
+    i = stage.i
+    stage.i = (i + 1) % len(stage.bufs)
+    if stage.events[i] is not None:
+        stage.events[i].synchronize()
+    buf = stage.bufs[i]
+    ctypes.memmove(buf.data_ptr(), ctypes.addressof(tables), n)
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    out.copy_(buf, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(dev))
+    stage.events[i] = ev
+    return out
 
 
 def codebook_from_lengths(lengths) -> HuffmanCodebook:
