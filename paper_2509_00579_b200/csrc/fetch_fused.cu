@@ -1624,12 +1624,13 @@ int pick_chunks_per_split(int max_chunks, long n_heads_total, int ctas_per_sm = 
 // (split-major) onto num_sms * ctas_per_sm slots, a CTA costing its chunks per
 // pair + the ~5 chunk-time start/drain of pick_chunks_per_split.  Returns the
 // makespan in chunk-times.
-double plan_makespan(const int *parts, int n_parts, long units, long slots, int pairs) {
+double plan_makespan(const int *parts, int n_parts, long units, long slots, int pairs,
+                     double start) {
     std::vector<double> heap((size_t)slots, 0.0);  // min-heap of slot free times
     auto greater = [](double a, double b) { return a > b; };
     double end = 0.0;
     for (int s = 0; s < n_parts; ++s) {
-        const double cost = (double)parts[s] / pairs + 5.0;
+        const double cost = (double)parts[s] / pairs + start;
         for (long u = 0; u < units; ++u) {
             std::pop_heap(heap.begin(), heap.end(), greater);
             const double t = heap.back() + cost;
@@ -1649,7 +1650,7 @@ double plan_makespan(const int *parts, int n_parts, long units, long slots, int 
 // cached per shape.  KVC_FUSED_PLAN="144:144:144:80" overrides (experiments);
 // KVC_PLAN_VERBOSE=1 prints each planned shape to stderr.
 SplitPlan pick_split_plan(int max_chunks, long units, int ctas_per_sm, int pairs, int max_splits,
-                          int uniform_cps) {
+                          int uniform_cps, double start) {
     SplitPlan plan{};
     auto set_parts = [&](const std::vector<int> &parts) {
         plan.n = (int)parts.size();
@@ -1683,22 +1684,24 @@ SplitPlan pick_split_plan(int max_chunks, long units, int ctas_per_sm, int pairs
             int mc;
             long units;
             int cps_sm, pairs, ms, ucps;
+            double start;
         };
         static std::mutex mu;
         static std::vector<std::pair<Key, std::vector<int>>> cache;
         std::lock_guard<std::mutex> lock(mu);
         for (auto &e : cache)
             if (e.first.mc == max_chunks && e.first.units == units && e.first.cps_sm == ctas_per_sm &&
-                e.first.pairs == pairs && e.first.ms == max_splits && e.first.ucps == ucps) {
+                e.first.pairs == pairs && e.first.ms == max_splits && e.first.ucps == ucps &&
+                e.first.start == start) {
                 set_parts(e.second);
                 return plan;
             }
         const long slots = (long)num_sms() * ctas_per_sm;
-        double best_t = plan_makespan(best.data(), (int)best.size(), units, slots, pairs);
+        double best_t = plan_makespan(best.data(), (int)best.size(), units, slots, pairs, start);
         std::vector<int> cand;
         auto consider = [&]() {
             if ((int)cand.size() > max_splits) return;
-            const double t = plan_makespan(cand.data(), (int)cand.size(), units, slots, pairs);
+            const double t = plan_makespan(cand.data(), (int)cand.size(), units, slots, pairs, start);
             if (t < best_t * (1.0 - 1e-3)) {
                 best_t = t;
                 best = cand;
@@ -1718,6 +1721,14 @@ SplitPlan pick_split_plan(int max_chunks, long units, int ctas_per_sm, int pairs
                     cand.push_back(t);
                     consider();
                 }
+                if (r >= 3) {  // three near-equal tails
+                    const int t3 = r / 3;
+                    cand.assign(kk, b);
+                    cand.push_back(r - 2 * t3);
+                    cand.push_back(t3);
+                    cand.push_back(t3);
+                    consider();
+                }
             }
         }
         if (getenv("KVC_PLAN_VERBOSE")) {
@@ -1727,7 +1738,7 @@ SplitPlan pick_split_plan(int max_chunks, long units, int ctas_per_sm, int pairs
             fprintf(stderr, " (model %.1f chunk-times)\n", best_t);
         }
         if (cache.size() > 64) cache.clear();
-        cache.push_back({Key{max_chunks, units, ctas_per_sm, pairs, max_splits, ucps}, best});
+        cache.push_back({Key{max_chunks, units, ctas_per_sm, pairs, max_splits, ucps, start}, best});
     }
     set_parts(best);
     return plan;
@@ -1813,7 +1824,10 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
             if (v >= np && v % np == 0) g_cps = v;
         }
         const long g_max_sp = (long)(workspace_bytes / (sizeof(Partial) * (size_t)n_seqs * H * group));
-        const SplitPlan g_plan = pick_split_plan(max_chunks, (long)n_seqs * H, 1, np, (int)std::min(g_max_sp, 1L << 20), g_cps);
+        // start/drain cost per CTA in chunk-times: ~0.5 for the one-CTA-per-SM GQA
+        // kernel (config 3: 448x4+86+85+85 0.558 ms vs 0.565 with 5)
+        const SplitPlan g_plan = pick_split_plan(max_chunks, (long)n_seqs * H, 1, np,
+                                                 (int)std::min(g_max_sp, 1L << 20), g_cps, 0.5);
         const int g_splits = g_plan.n;
         if (sizeof(Partial) * (size_t)n_seqs * H * group * g_splits > workspace_bytes)
             return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
@@ -1848,8 +1862,10 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
             if (v >= 4 && v % 4 == 0) ws_cps = v;
         }
         const long ws_max_sp = (long)(workspace_bytes / (sizeof(Partial) * (size_t)n_seqs * H));
+        // 5 chunk-times: fitted on config 2 (two CTAs per SM hide a short tail,
+        // which a slot model without co-residency cannot see)
         const SplitPlan ws_plan = pick_split_plan(max_chunks, (long)n_seqs * H, 2, WS_PAIRS,
-                                                  (int)std::min(ws_max_sp, 1L << 20), ws_cps);
+                                                  (int)std::min(ws_max_sp, 1L << 20), ws_cps, 5.0);
         const int ws_splits = ws_plan.n;
         if (sizeof(Partial) * (size_t)n_seqs * H * ws_splits > workspace_bytes)
             return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
