@@ -438,3 +438,46 @@ def test_batched_no_scores_corrupt_stream(kv):
     q = torch.from_numpy(np.asarray(g["q"][0], np.float32)).cuda().unsqueeze(0)
     _, _, err = kv.attention_batched([st], q)
     assert int(err.item()) != 0
+
+
+def _ragged_states(kv, ctxs, H, seed0):
+    states = []
+    for s, ctx in enumerate(ctxs):
+        k = kv.generate_synthetic(kv.SyntheticSpec(ctx + 23, H, 128, seed=seed0 + s)).values
+        v = kv.generate_synthetic(kv.SyntheticSpec(ctx + 23, H, 128, seed=seed0 + 50 + s)).values
+        st = kv.LayerCacheState.prefill(kv.CacheTensor(k[:ctx].astype(np.float16)),
+                                        kv.CacheTensor(v[:ctx].astype(np.float16)),
+                                        kv.QuantConfig(kv.QuantMode.K_BLOCK),
+                                        kv.QuantConfig(kv.QuantMode.V_TOKEN))
+        for t in range(ctx, ctx + 23):
+            st.append_token(k[t], v[t])
+        states.append(st)
+    return states
+
+
+@pytest.mark.parametrize("plan", [None, "7:1:5:300", "3:3:3:3:3:3:3:3:3:3:1000", "1000",
+                                  "100:50:25:13:7:3:1:1:500"])
+def test_split_plans_match_per_state(kv, plan, monkeypatch):
+    """Any split plan (KVC_FUSED_PLAN: unequal splits, boundaries off the
+    4-pair stride, splits past a short sequence's end, tails of one chunk)
+    gives the per-state attention_step result, for the warp-specialised G = 1
+    kernel and the decode-once GQA kernel, on a ragged batch."""
+    if plan is not None:
+        monkeypatch.setenv("KVC_FUSED_PLAN", plan)
+    ctxs = (70, 2600, 9000, 1300)  # 1, 40, 140, 20 chunks + buffered tokens
+    states = _ragged_states(kv, ctxs, 2, 300)
+    rng = np.random.default_rng(11)
+    q = rng.standard_normal((len(ctxs), 2, 128), dtype=np.float32)
+    out, _, err = kv.attention_batched(states, torch.from_numpy(q).cuda())
+    assert int(err.item()) == 0
+    for s, st in enumerate(states):
+        r = kv.attention_step(st, q[s])
+        assert max_relative_error(out[s].cpu().numpy(), r.out.cpu().numpy()) <= 1e-5
+    G = 4
+    qg = rng.standard_normal((len(ctxs), 2 * G, 128), dtype=np.float32)
+    og = kv.attention_gqa(states, torch.from_numpy(qg).cuda(), G)
+    for s, st in enumerate(states):
+        for j in range(G):
+            r = kv.attention_step(st, qg[s].reshape(2, G, 128)[:, j])
+            assert max_relative_error(og[s].view(2, G, 128)[:, j].cpu().numpy(),
+                                      r.out.cpu().numpy()) <= 1e-5
