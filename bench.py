@@ -437,6 +437,12 @@ def main():
                       "device_passA_gbs": round(store_detail["prefill_slice"]["passA_gbs"], 2),
                       "device_passB_gbs": round(store_detail["prefill_slice"]["passB_gbs"], 2),
                       "device_prefill_gbs": round(store_detail["prefill_slice"]["device_gbs"], 2),
+                      # HBM bytes the two prefill passes move per fp16 input byte: input
+                      # 1 + codes scratch (1 B/value written by A, read by B) 1 + arena
+                      # out ~1/ratio; against the same peak as the fetch roofline
+                      "device_prefill_hbm_frac": round(
+                          store_detail["prefill_slice"]["device_gbs"] * (2.0 + 1.0 / ratio)
+                          / hbm_peak, 4),
                       "append_event_us": round(store_detail["append_event"]["us_per_event"], 2),
                       "append_event": "config 4: 128 tokens x 32 heads x 128 from the f32 "
                                       "buffer, one kvc_store_append launch"},
