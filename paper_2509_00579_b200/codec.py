@@ -38,12 +38,27 @@ class _SlabPool:
 
     def __init__(self, device: torch.device):
         import os
+        import threading
+        # states may be built and dropped from several threads, and an arena's
+        # finalizer can run inside alloc (a GC pass): releases that find the
+        # lock taken are queued and applied by the next alloc / release
+        self.lock = threading.Lock()
+        self.pending = []
         self.device = device
         self.slab_bytes = int(os.environ.get("KVC_ARENA_SLAB_MB", "1024")) << 20
         self.slabs = []   # torch uint8 tensors
         self.free = []    # per slab: sorted list of [offset, size]
 
     def alloc(self, nbytes: int):
+        with self.lock:
+            self._drain()
+            return self._alloc(nbytes)
+
+    def _drain(self) -> None:
+        while self.pending:
+            self._release(*self.pending.pop())
+
+    def _alloc(self, nbytes: int):
         n = max(self.ALIGN, (int(nbytes) + self.ALIGN - 1) // self.ALIGN * self.ALIGN)
         # fast path: the tail of the newest slab (prefills carve slabs in order)
         if self.free and self.free[-1] and self.free[-1][-1][1] >= n:
@@ -68,6 +83,14 @@ class _SlabPool:
         return self.slabs[-1][:n], _Extent(self, len(self.slabs) - 1, 0, n)
 
     def release(self, si: int, off: int, n: int) -> None:
+        self.pending.append((si, off, n))
+        if self.lock.acquire(blocking=False):
+            try:
+                self._drain()
+            finally:
+                self.lock.release()
+
+    def _release(self, si: int, off: int, n: int) -> None:
         fl = self.free[si]
         lo, hi = 0, len(fl)
         while lo < hi:
@@ -110,12 +133,14 @@ def reserve_arena_pool(nbytes: int, device=None) -> int:
     dev = torch.device(device) if device is not None else torch.device(
         "cuda", torch.cuda.current_device())
     pool = _pool(dev)
-    free = sum(sz for fl in pool.free for _, sz in fl)
-    while free < nbytes:
-        slab = pool.slab_bytes
-        pool.slabs.append(torch.empty(slab, dtype=torch.uint8, device=pool.device))
-        pool.free.append([[0, slab]])
-        free += slab
+    with pool.lock:
+        pool._drain()
+        free = sum(sz for fl in pool.free for _, sz in fl)
+        while free < nbytes:
+            slab = pool.slab_bytes
+            pool.slabs.append(torch.empty(slab, dtype=torch.uint8, device=pool.device))
+            pool.free.append([[0, slab]])
+            free += slab
     return free
 
 

@@ -113,3 +113,18 @@ def test_histogram_bound_covers_every_block_layout():
             actual = int(sum((hdr + (int(b) + 7) // 8 + 3) & ~3 for b in bits))
             bound = nb * (hdr + 4) + (int(bits.sum()) + 7) // 8
             assert actual <= bound <= nb * worst_block_bytes(bs, n_units, D, 6) + 4 * nb
+
+
+def test_release_inside_alloc_is_deferred_not_lost():
+    """A release arriving while the pool lock is held (an arena finalizer run
+    by a GC pass inside alloc, or another thread) is queued and applied by the
+    next pool operation."""
+    p = pool()
+    _, e1 = p.alloc(4096)
+    with p.lock:
+        e1.release()  # cannot take the lock: queued
+        assert p.pending
+    _, e2 = p.alloc(1024)  # drains the queue first
+    assert not p.pending
+    e2.release()
+    assert p.free == [[[0, p.slabs[0].numel()]]]
