@@ -481,3 +481,25 @@ def test_split_plans_match_per_state(kv, plan, monkeypatch):
             r = kv.attention_step(st, qg[s].reshape(2, G, 128)[:, j])
             assert max_relative_error(og[s].view(2, G, 128)[:, j].cpu().numpy(),
                                       r.out.cpu().numpy()) <= 1e-5
+
+
+def test_prefill_many_matches_prefill(kv):
+    """The pipelined prefill_many (pass A of item i+1 in flight while item i's
+    codebooks are built) produces byte-identical arenas, offsets and codebooks."""
+    items = []
+    for s, ctx in enumerate((5000, 64 * 40, 777, 9100)):
+        k = kv.generate_synthetic(kv.SyntheticSpec(ctx, 4, 128, seed=400 + s)).values
+        v = kv.generate_synthetic(kv.SyntheticSpec(ctx, 4, 128, seed=450 + s)).values
+        items.append((torch.from_numpy(k.astype(np.float16)).cuda(),
+                      torch.from_numpy(v.astype(np.float16)).cuda()))
+    ck, cv = kv.QuantConfig(kv.QuantMode.K_BLOCK), kv.QuantConfig(kv.QuantMode.V_TOKEN)
+    many = kv.LayerCacheState.prefill_many(items, ck, cv)
+    for (k, v), st in zip(items, many):
+        ref = kv.LayerCacheState.prefill(k, v, ck, cv)
+        st.check()
+        for a, b in ((st.k_arena, ref.k_arena), (st.v_arena, ref.v_arena)):
+            assert a.snapshot() == b.snapshot()
+            assert np.array_equal(a.block_offsets, b.block_offsets)
+        assert np.array_equal(st.k_codebook.code_lengths, ref.k_codebook.code_lengths)
+        assert np.array_equal(st.v_codebook.code_lengths, ref.v_codebook.code_lengths)
+        assert (st.context_len, st.buffered) == (ref.context_len, ref.buffered)
