@@ -79,9 +79,11 @@ class KVCompLayer(CacheLayerMixin):
             # prefill: [B, H, T, D] -> per row [T, H, D]
             kk = key_states.detach().transpose(1, 2)
             vv = value_states.detach().transpose(1, 2)
-            self.states = [LayerCacheState.prefill(kk[b].contiguous(), vv[b].contiguous(),
-                                                   self.cfg_k, self.cfg_v, check=False)
-                           for b in range(B)]
+            # the batch rows through the pipelined prefill (row b+1's pass A runs
+            # while row b's codebooks are built on the host)
+            self.states = LayerCacheState.prefill_many(
+                [(kk[b].contiguous(), vv[b].contiguous()) for b in range(B)],
+                self.cfg_k, self.cfg_v)
             self.cumulative_length = T
             return key_states, value_states
         if len(self.states) != B:
