@@ -18,18 +18,52 @@ from __future__ import annotations
 from typing import Optional, Tuple
 
 import functools
+import weakref
 
 import numpy as np
 import torch
 
 from . import _lib
 from .codebook import HuffmanCodebook, build_smoothed_codebook
-from .codec import DeviceArena, worst_block_bytes
+from .codec import DeviceArena, pooled_zeros, worst_block_bytes
 from .errors import CodecError, ConfigError
 from .quantizer import QuantConfig, QuantMode, as_device_tensor, dtype_code, quantize_tokens
 from .tensor_io import CacheTensor
 
 MAX_SLICE_BITS = 0xFFFF
+
+
+class _HistRing:
+    """Pinned host slots for the prefill histogram readback (allocated once:
+    a pinned allocation per prefill costs a cudaHostAlloc).  A slot is reused
+    only after the event of its previous copy has completed, and callers
+    consume a slot (prefill_many: at most two in flight) long before the
+    ring wraps."""
+
+    def __init__(self, slots: int = 8):
+        self.bufs = [torch.empty(512, dtype=torch.int64, pin_memory=True) for _ in range(slots)]
+        self.events = [None] * slots
+        self.i = 0
+
+
+_HIST_RING = None
+
+
+def _hist_readback(hist: torch.Tensor):
+    global _HIST_RING
+    if _HIST_RING is None:
+        _HIST_RING = _HistRing()
+    r = _HIST_RING
+    i = r.i
+    r.i = (i + 1) % len(r.bufs)
+    if r.events[i] is not None:
+        r.events[i].synchronize()
+    buf = r.bufs[i]
+    buf.copy_(hist, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(hist.device))
+    r.events[i] = ev
+    return buf, ev
 
 
 class LayerCacheState:
@@ -81,6 +115,8 @@ class LayerCacheState:
         cap = cfg_k.buffer_size + 1
         if _pre is not None:  # allocated by prefill while its pass A ran
             self._k_buffer, self._v_buffer = _pre["k_buffer"], _pre["v_buffer"]
+            for ext in _pre.get("extents", ()):
+                weakref.finalize(self, ext.release)
         else:
             self._k_buffer = torch.zeros((cap, head_num, head_dim), dtype=torch.float32,
                                          device=self.device)
@@ -206,18 +242,20 @@ class LayerCacheState:
         # pass A runs, so the host work between its completion and pass B is
         # only the codebook build, the table upload and the arena carve-out
         cap = cfg_k.buffer_size + 1
-        pre = {"k_buffer": torch.zeros((cap, H, D), dtype=torch.float32, device=kt.device)}
-        pre["v_buffer"] = torch.zeros_like(pre["k_buffer"])
+        if kt.device.type == "cuda":  # long-lived: from the slab pool
+            kb, ke = pooled_zeros((cap, H, D), torch.float32, kt.device)
+            vb, ve = pooled_zeros((cap, H, D), torch.float32, kt.device)
+            pre = {"k_buffer": kb, "v_buffer": vb, "extents": (ke, ve)}
+        else:
+            pre = {"k_buffer": torch.zeros((cap, H, D), dtype=torch.float32, device=kt.device)}
+            pre["v_buffer"] = torch.zeros_like(pre["k_buffer"])
         pre_ws = (torch.empty(lib.kvc_store_workspace_bytes(n_chunks, H, D, bs), dtype=torch.uint8,
                               device=kt.device) if n_full and fused else None)
         hist_host = ev = None
         if codebooks is None:
             if process_group is not None:
                 torch.distributed.all_reduce(hist, group=process_group)
-            hist_host = torch.empty(512, dtype=torch.int64, pin_memory=True)
-            hist_host.copy_(hist, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(torch.cuda.current_stream(kt.device))
+            hist_host, ev = _hist_readback(hist)
         return dict(cls=cls, kt=kt, vt=vt, cfg_k=cfg_k, cfg_v=cfg_v, codebooks=codebooks,
                     k_channel_ranges=k_channel_ranges, head_base=head_base,
                     head_total=head_total, capacity=capacity, src_dtype=src_dtype, ctx=ctx,
@@ -238,7 +276,7 @@ class LayerCacheState:
         kcodes, kmetas, vcodes, vmetas = c["kcodes"], c["kmetas"], c["vcodes"], c["vmetas"]
         if codebooks is None:
             c["ev"].synchronize()  # this item's pass A only, not later launches
-            h = c["hist_host"].numpy().astype(np.uint64)
+            h = c["hist_host"].numpy().astype(np.uint64)  # a copy: the slot may be reused
             k_cb = build_smoothed_codebook(h[:256], cfg_k.max_code)
             v_cb = build_smoothed_codebook(h[256:], cfg_v.max_code)
         else:
