@@ -270,7 +270,14 @@ def attention_gqa(states: Sequence[LayerCacheState], q: torch.Tensor, group: int
         need = lib.kvc_attention_workspace_bytes(B, H, group, D, max_chunks)
         if workspace is None or workspace.numel() < need:
             workspace = torch.empty(need, dtype=torch.uint8, device=dev)
-        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        if check:
+            err = torch.zeros(1, dtype=torch.int32, device=dev)
+        else:
+            # never read on this path: a per-cache scratch word, not zeroed (one
+            # fill launch less per decode step)
+            if getattr(cache, "scratch_err", None) is None or cache.scratch_err.device != dev:
+                cache.scratch_err = torch.zeros(1, dtype=torch.int32, device=dev)
+            err = cache.scratch_err
         qc = q.contiguous()
         st = lib.kvc_attention(ddev.data_ptr(), ctypes_addr(dhost), B, H, D,
                                states[0].cfg_k.block_size, group, qc.data_ptr(), out.data_ptr(),
