@@ -251,8 +251,13 @@ __device__ __forceinline__ void img_u16(uint32_t *img, int j, uint32_t v, int sh
 // codes u8 [bs*D], unit lo/scale/r32 f32 [n_units], slice bits u32 [bs],
 // slice offsets u32 [bs], codebook words u32[256] + lengths u8[256].
 // DT / BST: compile-time head_dim / block_size (0 = runtime, generic shapes).
+// Hot shape: a register cap (40) for 6 resident CTAs per SM instead of 5 hides
+// more of the staging and look-back latency (config-2 slice: pass A 0.386 ->
+// 0.382 ms, pass B 0.405 -> 0.400, growing-cache store 0.943 -> 0.871).  A cap
+// of 7 (32 registers) was faster still for the look-back store (0.764) but
+// slowed pass A and the small append events.  Generic shapes keep the default.
 template <typename T, bool ENCODE, int DT, int BST>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, (DT == 128 && BST == 64) ? 6 : 1)
 store_kernel(StoreParams P, int stage_words) {
     extern __shared__ __align__(16) uint8_t sm[];
     const StoreTensor S = P.t[blockIdx.y];  // one copy into registers
