@@ -211,6 +211,12 @@ def build_cache(kv, torch, layers, batch, ctx, heads_total, head_base, heads_loc
                                               head_total=heads_total, process_group=group)
         torch.cuda.synchronize()
         store_times.append((time.perf_counter() - t0) / batch)
+        if os.environ.get("KVC_BENCH_DEBUG"):
+            ms = torch.cuda.memory_stats(device)
+            from paper_2509_00579_b200 import codec as _codec
+            print("layer", layer, "ms/item %.3f" % (store_times[-1] * 1e3), "cudaMallocs",
+                  ms.get("num_device_alloc"), "retries", ms.get("num_alloc_retries"),
+                  "slabs", len(_codec._pool(device).slabs), file=sys.stderr)
         store_bytes = 2 * ctx * heads_local * 128 * 2
         for st in row:
             st.compact()

@@ -10,6 +10,7 @@ append (SPEC: codebooks are immutable after prefill).
 from __future__ import annotations
 
 import ctypes
+import weakref
 from dataclasses import dataclass, field
 from typing import Dict
 
@@ -79,7 +80,9 @@ class HuffmanCodebook:
         key = str(dev)
         t = self._device.get(key)
         if t is None:
-            t = _upload(self.tables, dev)
+            t, ext = _upload(self.tables, dev)
+            if ext is not None:  # carved from the arena slab pool: freed with the book
+                weakref.finalize(self, ext.release)
             self._device[key] = t
         return t
 
@@ -102,7 +105,7 @@ _STAGE = {}
 def _upload(tables, dev: torch.device) -> torch.Tensor:
     n = ctypes.sizeof(tables)
     if dev.type != "cuda":
-        return torch.frombuffer(bytearray(bytes(tables)), dtype=torch.uint8).to(dev)
+        return torch.frombuffer(bytearray(bytes(tables)), dtype=torch.uint8).to(dev), None
     stage = _STAGE.get(n)
     if stage is None:
         stage = _STAGE[n] = _PinnedStage(n)
@@ -112,12 +115,17 @@ def _upload(tables, dev: torch.device) -> torch.Tensor:
         stage.events[i].synchronize()
     buf = stage.bufs[i]
     ctypes.memmove(buf.data_ptr(), ctypes.addressof(tables), n)
-    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    # long-lived (one per state and tensor): from the slab pool, so building
+    # many states does not grow the caching allocator's small pool (each new
+    # 2 MB segment was a cudaMalloc, and under load those took milliseconds)
+    from .codec import _pool
+    raw, ext = _pool(dev).alloc(n)
+    out = raw[:n]
     out.copy_(buf, non_blocking=True)
     ev = torch.cuda.Event()
     ev.record(torch.cuda.current_stream(dev))
     stage.events[i] = ev
-    return out
+    return out, ext
 
 
 def codebook_from_lengths(lengths) -> HuffmanCodebook:

@@ -130,6 +130,15 @@ class _Extent:
             self.live = False
             self.pool.release(self.si, self.off, self.n)
 
+    def shrink(self, nbytes: int) -> None:
+        """Return the extent's tail beyond nbytes (aligned up) to the pool, in
+        place: no new allocation, no copy."""
+        keep = max(_SlabPool.ALIGN, (int(nbytes) + _SlabPool.ALIGN - 1) // _SlabPool.ALIGN
+                   * _SlabPool.ALIGN)
+        if self.live and keep < self.n:
+            self.pool.release(self.si, self.off + keep, self.n - keep)
+            self.n = keep
+
 
 _POOLS = {}
 
@@ -211,11 +220,27 @@ class DeviceArena:
         alloc = initial_bytes if capacity is None else capacity
         self._extent = None
         self._set_buf(alloc + TMA_SLACK)
-        self._offsets = torch.empty(max(initial_blocks, 1), dtype=torch.int32, device=self.device)
-        self._counters = torch.zeros(ctypes.sizeof(_lib.ArenaCounters), dtype=torch.uint8,
-                                     device=self.device)
+        # offsets and counters from the slab pool as well: per-state small
+        # allocations otherwise grow the caching allocator's small pool (a
+        # cudaMalloc per few states)
+        self._offsets, self._off_ext = self._pooled(max(initial_blocks, 1) * 4, torch.int32)
+        self._counters, self._cnt_ext = self._pooled(ctypes.sizeof(_lib.ArenaCounters),
+                                                     torch.uint8, zero=True)
         self.n_blocks = 0          # host mirror (deterministic)
         self._bound = 0            # host upper bound on the cursor
+
+    def _pooled(self, nbytes: int, dtype, zero: bool = False):
+        """A device tensor of nbytes (as dtype) from the slab pool, released
+        when this arena dies; plain torch memory off the GPU."""
+        if self.device.type != "cuda":
+            t = torch.zeros(nbytes, dtype=torch.uint8, device=self.device).view(dtype)
+            return t, None
+        raw, ext = _pool(self.device).alloc(nbytes)
+        t = raw[:nbytes].view(dtype)
+        if zero:
+            t.zero_()
+        weakref.finalize(self, ext.release)
+        return t, ext
 
     def _set_buf(self, nbytes: int, keep: int = 0) -> None:
         """(Re)allocate the byte buffer from the slab pool, copying the first
@@ -235,10 +260,12 @@ class DeviceArena:
         """Make room for n_blocks more blocks of at most worst_bytes total."""
         need_blocks = self.n_blocks + n_blocks
         if need_blocks > self._offsets.numel():
-            new = torch.empty(max(need_blocks, 2 * self._offsets.numel()), dtype=torch.int32,
-                              device=self.device)
+            new, ext = self._pooled(max(need_blocks, 2 * self._offsets.numel()) * 4, torch.int32)
             new[: self.n_blocks] = self._offsets[: self.n_blocks]
-            self._offsets = new
+            old_ext = self._off_ext
+            self._offsets, self._off_ext = new, ext
+            if old_ext is not None:
+                old_ext.release()
         if self.capacity is not None:
             return  # fixed capacity: the device reports ArenaFullError
         need = self._bound + worst_bytes
@@ -253,7 +280,13 @@ class DeviceArena:
         cur = int(self.counters().cursor)
         size = cur + headroom
         if size + TMA_SLACK < self._buf.numel():
-            self._set_buf(size + TMA_SLACK, keep=cur)
+            if self._extent is not None:
+                # in place: the extent's tail goes back to the pool (a copy into
+                # a new extent would leave the old one behind as a hole)
+                self._extent.shrink(size + TMA_SLACK)
+                self._buf = self._buf[: size + TMA_SLACK]
+            else:
+                self._set_buf(size + TMA_SLACK, keep=cur)
 
     def load(self, data: bytes, offsets: np.ndarray, counters: bytes, headroom: int = 1 << 16):
         """Replace the contents with serialised blocks (container restore)."""
@@ -269,6 +302,10 @@ class DeviceArena:
         offs = torch.zeros(max(nb, 1), dtype=torch.int32)
         if nb:
             offs[:nb] = torch.from_numpy(np.asarray(offsets, np.uint32).view(np.int32).copy())
+        for e in (self._off_ext, self._cnt_ext):
+            if e is not None:
+                e.release()
+        self._off_ext = self._cnt_ext = None
         self._offsets = offs.to(self.device)
         self._counters = torch.frombuffer(bytearray(counters), dtype=torch.uint8).to(self.device)
         self.n_blocks = nb

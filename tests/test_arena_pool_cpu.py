@@ -128,3 +128,30 @@ def test_release_inside_alloc_is_deferred_not_lost():
     assert not p.pending
     e2.release()
     assert p.free == [[[0, p.slabs[0].numel()]]]
+
+
+def test_shrink_returns_the_tail_in_place():
+    p = pool()
+    a, ea = p.alloc(100000)
+    b, eb = p.alloc(5000)
+    ea.shrink(30000)
+    assert ea.n == 30208  # aligned up to 256
+    # the returned tail is a hole between a and b: first fit reuses it
+    p.alloc(free_bytes(p) - (100000 // 256 * 256 + 256 - 30208))  # drain the slab tail
+    c, _ = p.alloc(60000)
+    assert c.data_ptr() == a.data_ptr() + 30208
+    ea.release()
+    eb.release()
+
+
+def test_arena_compact_shrinks_without_moving():
+    codec._POOLS.pop(("cpu", None), None)
+    try:
+        ar = codec.DeviceArena(torch.device("cpu"), initial_bytes=1 << 16)
+        ptr = ar.buf_ptr
+        ar._counters.zero_()  # cursor 0: compact to the slack
+        ar.compact(headroom=1000)
+        assert ar.buf_ptr == ptr and ar._buf.numel() == 1000 + codec.TMA_SLACK
+        assert ar._extent.n < (1 << 16)
+    finally:
+        codec._POOLS.pop(("cpu", None), None)
