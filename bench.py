@@ -396,10 +396,33 @@ def main():
     qh.copy_(q.cpu())
     oh = torch.empty((L, B, hl * G, 128), dtype=torch.float32).pin_memory()
 
+    cs = torch.cuda.Stream(device)
+    ev_q = [torch.cuda.Event() for _ in range(L)]
+    ev_o = [torch.cuda.Event() for _ in range(L)]
+
     def e2e_step():
-        q.copy_(qh, non_blocking=True)
-        step()
-        oh.copy_(outs, non_blocking=True)
+        if world > 1:
+            q.copy_(qh, non_blocking=True)
+            step()
+            oh.copy_(outs, non_blocking=True)
+            return
+        # per-layer copies on a side stream, overlapped with the attention of
+        # the neighbouring layers: layer l's q lands while layer l-1 computes,
+        # its output leaves while layer l+1 computes
+        main = torch.cuda.current_stream(device)
+        cs.wait_stream(main)  # the previous step is done with q and outs
+        with torch.cuda.stream(cs):
+            for layer in range(L):
+                q[layer].copy_(qh[layer], non_blocking=True)
+                ev_q[layer].record(cs)
+        for layer in range(L):
+            main.wait_event(ev_q[layer])
+            layer_call(layer)
+            ev_o[layer].record(main)
+            cs.wait_event(ev_o[layer])
+            with torch.cuda.stream(cs):
+                oh[layer].copy_(outs[layer], non_blocking=True)
+        main.wait_stream(cs)
 
     for _ in range(2):
         e2e_step()
