@@ -344,8 +344,8 @@ def main():
             kv.attention_batched(states[layer], q[layer], desc_cache=caches[layer], workspace=ws,
                                  out=outs[layer])
         else:
-            outs[layer] = kv.attention_gqa(states[layer], q[layer], G, desc_cache=caches[layer],
-                                           workspace=ws, check=False)
+            kv.attention_gqa(states[layer], q[layer], G, desc_cache=caches[layer], workspace=ws,
+                             check=False, out=outs[layer])
 
     def step():
         for layer in range(L):

@@ -248,7 +248,8 @@ def multistage_attention(state: LayerCacheState, q,
 
 def attention_gqa(states: Sequence[LayerCacheState], q: torch.Tensor, group: int,
                   desc_cache: Optional["_BatchDesc"] = None,
-                  workspace: Optional[torch.Tensor] = None, check: bool = True) -> torch.Tensor:
+                  workspace: Optional[torch.Tensor] = None, check: bool = True,
+                  out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """Grouped-query decode attention: q [B, H_kv*group, D], query head
     h*group+j reads KV head h (Llama-3 layout).  The reference has no GQA
     (SPEC non-goal; its oracle runs one attention_step per group member).
@@ -260,7 +261,11 @@ def attention_gqa(states: Sequence[LayerCacheState], q: torch.Tensor, group: int
     B, HQ, D = q.shape
     H = HQ // group
     dev = q.device
-    out = torch.empty((B, HQ, D), dtype=torch.float32, device=dev)
+    if out is None:
+        out = torch.empty((B, HQ, D), dtype=torch.float32, device=dev)
+    elif (tuple(out.shape) != (B, HQ, D) or out.dtype != torch.float32 or not out.is_contiguous()
+          or out.device != dev):
+        raise CodecError("out must be a contiguous float32 [B, H*group, D] tensor on q's device")
     cache = desc_cache if desc_cache is not None else _BatchDesc()
     if group in (2, 4) and _fused_supported(states) and all(
             max(s.k_codebook.max_code_length, s.v_codebook.max_code_length) <= 6 for s in states):
