@@ -342,7 +342,7 @@ def main():
     def layer_call(layer):
         if G == 1:
             kv.attention_batched(states[layer], q[layer], desc_cache=caches[layer], workspace=ws,
-                                 out=outs[layer])
+                                 out=outs[layer], want_err=False)
         else:
             kv.attention_gqa(states[layer], q[layer], G, desc_cache=caches[layer], workspace=ws,
                              check=False, out=outs[layer])

@@ -146,9 +146,13 @@ _default_desc_cache = _BatchDesc()
 
 def attention_batched(states: Sequence[LayerCacheState], q: torch.Tensor,
                       want_scores: bool = False, desc_cache: Optional[_BatchDesc] = None,
-                      workspace: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None):
+                      workspace: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                      want_err: bool = True):
     """One fused launch over a batch of same-shape states.  q: [B, H, D] f32
-    on the device.  Returns (out [B, H, D], scores [B, H, max_ctx] or None)."""
+    on the device.  Returns (out [B, H, D], scores [B, H, max_ctx] or None,
+    err [1] int32: the device error word of this call, or None with
+    want_err=False -- the decode loop's fire-and-forget path, which skips the
+    per-call zero fill)."""
     B = len(states)
     s0 = states[0]
     H, D, bs = s0.head_num, s0.head_dim, s0.cfg_k.block_size
@@ -159,8 +163,13 @@ def attention_batched(states: Sequence[LayerCacheState], q: torch.Tensor,
     if out is None:
         out = torch.empty((B, H, D), dtype=torch.float32, device=dev)
     scores = torch.zeros((B, H, max_ctx), dtype=torch.float32, device=dev) if want_scores else None
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
     cache = desc_cache if desc_cache is not None else _BatchDesc()
+    if want_err or not _fused_supported(states):
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+    else:
+        if getattr(cache, "scratch_err", None) is None or cache.scratch_err.device != dev:
+            cache.scratch_err = torch.zeros(1, dtype=torch.int32, device=dev)
+        err = cache.scratch_err
     ddev, dhost = cache.get(states)
     if _fused_supported(states):
         need = lib.kvc_attention_workspace_bytes(B, H, 1, D, max_chunks)
@@ -189,7 +198,7 @@ def attention_batched(states: Sequence[LayerCacheState], q: torch.Tensor,
                               ws.data_ptr(), err.data_ptr(), _stream(dev))
         _lib.check(st, "kvc_v_output")
         scores = sc if want_scores else None
-    return out, scores, err
+    return out, scores, (err if want_err else None)
 
 
 def ctypes_addr(arr) -> int:
