@@ -503,3 +503,27 @@ def test_prefill_many_matches_prefill(kv):
         assert np.array_equal(st.k_codebook.code_lengths, ref.k_codebook.code_lengths)
         assert np.array_equal(st.v_codebook.code_lengths, ref.v_codebook.code_lengths)
         assert (st.context_len, st.buffered) == (ref.context_len, ref.buffered)
+
+
+def test_decode_loop_entry_points(kv):
+    """The bench/decode-loop variants write the same results: attention_gqa
+    into a caller buffer (out=), attention_batched without the per-call error
+    word (want_err=False)."""
+    states = _ragged_states(kv, (3000, 700), 2, 600)
+    rng = np.random.default_rng(5)
+    q = torch.from_numpy(rng.standard_normal((2, 2, 128), dtype=np.float32)).cuda()
+    ref, _, err = kv.attention_batched(states, q)
+    out = torch.empty_like(ref)
+    o2, sc, e2 = kv.attention_batched(states, q, out=out, want_err=False)
+    torch.cuda.synchronize()
+    assert e2 is None and sc is None and o2.data_ptr() == out.data_ptr()
+    assert torch.equal(out, ref) and int(err.item()) == 0
+    G = 4
+    qg = torch.from_numpy(rng.standard_normal((2, 2 * G, 128), dtype=np.float32)).cuda()
+    ref_g = kv.attention_gqa(states, qg, G)
+    buf = torch.empty_like(ref_g)
+    got = kv.attention_gqa(states, qg, G, check=False, out=buf)
+    torch.cuda.synchronize()
+    assert got.data_ptr() == buf.data_ptr() and torch.equal(buf, ref_g)
+    with pytest.raises(kv.CodecError):
+        kv.attention_gqa(states, qg, G, out=torch.empty((2, 2 * G, 64), device="cuda"))
