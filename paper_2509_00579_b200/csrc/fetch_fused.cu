@@ -1626,6 +1626,18 @@ int pick_chunks_per_split(int max_chunks, long n_heads_total, int ctas_per_sm = 
 // makespan in chunk-times.
 double plan_makespan(const int *parts, int n_parts, long units, long slots, int pairs,
                      double start) {
+    // identical CTAs per split: g = gcd(units, slots) independent copies of a
+    // (units/g, slots/g) schedule have the same makespan, at 1/g the cost
+    long a = units, b = slots;
+    while (b) {
+        const long t = a % b;
+        a = b;
+        b = t;
+    }
+    if (a > 1) {
+        units /= a;
+        slots /= a;
+    }
     std::vector<double> heap((size_t)slots, 0.0);  // min-heap of slot free times
     auto greater = [](double a, double b) { return a > b; };
     double end = 0.0;
