@@ -299,6 +299,30 @@ def main():
     dense_gbs = 2 * B * hl * T * 128 * 2 / (dense_ms * 1e-3) / 1e9
     del dk, dv, dq, dout
     torch.cuda.empty_cache()
+    # library reference point: flash-attn's fp16 decode kernel on the same shape
+    # (token-major [B, T, H, D] cache), when the package is importable
+    fa = None
+    try:
+        from flash_attn import flash_attn_with_kvcache
+        fk = torch.randn((B, T, hl, 128), device=device, dtype=torch.float16)
+        fv = torch.randn_like(fk)
+        fq = torch.randn((B, 1, hl * G, 128), device=device, dtype=torch.float16)
+        for _ in range(3):
+            flash_attn_with_kvcache(fq, fk, fv)
+        torch.cuda.synchronize()
+        d0.record()
+        for _ in range(10):
+            flash_attn_with_kvcache(fq, fk, fv)
+        d1.record()
+        torch.cuda.synchronize()
+        fa_ms = d0.elapsed_time(d1) / 10
+        fa = {"value": round(2 * B * hl * T * 128 * 2 / (fa_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+              "ms_per_layer": round(fa_ms, 4),
+              "note": "flash-attn flash_attn_with_kvcache (library, fp16), one layer, same shape"}
+        del fk, fv, fq
+        torch.cuda.empty_cache()
+    except Exception as exc:  # not installed / unsupported: reported as such
+        fa = {"value": None, "note": f"flash-attn unavailable: {type(exc).__name__}"}
 
     # reserve the compressed-cache memory up front, as a serving process would
     # (about 0.28 of the fp16 bytes at default scales, + 10 %): prefill timings
@@ -472,6 +496,7 @@ def main():
                            round(dense_ms, 4), "note": "our uncompressed fp16 decode-attention "
                            "kernel, one layer, same shape"},
             "speedup_vs_dense_fp16": round(value / dense_gbs, 3),
+            "flash_attn_fp16": fa,
             "store": {"compress_gbs": round(store_gbs, 3), "unit": "GB/s fp16 K+V in",
                       "note": "LayerCacheState.prefill_many over a layer's sequences, wall clock "
                               "per (seq, layer) incl. histogram readback + host codebook "
