@@ -527,3 +527,25 @@ def test_decode_loop_entry_points(kv):
     assert got.data_ptr() == buf.data_ptr() and torch.equal(buf, ref_g)
     with pytest.raises(kv.CodecError):
         kv.attention_gqa(states, qg, G, out=torch.empty((2, 2 * G, 64), device="cuda"))
+
+
+def test_prefill_many_fixed_codebooks_and_kchannel(kv):
+    """prefill_many with given codebooks (no histogram readback) and with
+    K_CHANNEL quantisation matches prefill() byte for byte."""
+    items = []
+    for s, ctx in enumerate((1500, 4100)):
+        k = kv.generate_synthetic(kv.SyntheticSpec(ctx, 2, 128, seed=700 + s)).values
+        v = kv.generate_synthetic(kv.SyntheticSpec(ctx, 2, 128, seed=750 + s)).values
+        items.append((torch.from_numpy(k.astype(np.float16)).cuda(),
+                      torch.from_numpy(v.astype(np.float16)).cuda()))
+    cv = kv.QuantConfig(kv.QuantMode.V_TOKEN)
+    ck = kv.QuantConfig(kv.QuantMode.K_BLOCK)
+    base = kv.LayerCacheState.prefill(items[0][0], items[0][1], ck, cv)
+    books = (base.k_codebook, base.v_codebook)
+    for cfg_k, extra in ((ck, {"codebooks": books}),
+                         (kv.QuantConfig(kv.QuantMode.K_CHANNEL), {})):
+        many = kv.LayerCacheState.prefill_many(items, cfg_k, cv, **extra)
+        for (k, v), st in zip(items, many):
+            ref = kv.LayerCacheState.prefill(k, v, cfg_k, cv, **extra)
+            for a, b in ((st.k_arena, ref.k_arena), (st.v_arena, ref.v_arena)):
+                assert a.snapshot() == b.snapshot()
