@@ -320,17 +320,43 @@ class DeviceArena:
         return self.capacity if self.capacity is not None else self._buf.numel() - TMA_SLACK
 
     # ---- device pointers ---------------------------------------------
+    # the three device tensors keep their data pointers cached: descriptors of
+    # every state are rebuilt-checked on each decode-step launch
+    @property
+    def _buf(self) -> torch.Tensor:
+        return self.__buf
+
+    @_buf.setter
+    def _buf(self, t: torch.Tensor) -> None:
+        self.__buf, self._buf_ptr = t, t.data_ptr()
+
+    @property
+    def _offsets(self) -> torch.Tensor:
+        return self.__offsets
+
+    @_offsets.setter
+    def _offsets(self, t: torch.Tensor) -> None:
+        self.__offsets, self._off_ptr = t, t.data_ptr()
+
+    @property
+    def _counters(self) -> torch.Tensor:
+        return self.__counters
+
+    @_counters.setter
+    def _counters(self, t: torch.Tensor) -> None:
+        self.__counters, self._cnt_ptr = t, t.data_ptr()
+
     @property
     def buf_ptr(self) -> int:
-        return self._buf.data_ptr()
+        return self._buf_ptr
 
     @property
     def offsets_ptr(self) -> int:
-        return self._offsets.data_ptr()
+        return self._off_ptr
 
     @property
     def counters_ptr(self) -> int:
-        return self._counters.data_ptr()
+        return self._cnt_ptr
 
     # ---- host views (synchronising) ----------------------------------
     def counters(self) -> _lib.ArenaCounters:
