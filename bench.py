@@ -16,11 +16,16 @@ dequant -> q.K^T -> online softmax -> .V, then the split combine).  Inputs
                buffered tokens + q/out)
   roofline   : the fused kernel's compressed-byte GB/s vs MEASURED_PEAKS hbm
   dense_fp16 : our uncompressed fp16 decode-attention kernel on one layer
-  store      : compress GB/s (fp16 K+V input bytes / prefill time, config 2
-               (seq, layer) slices) and per-event latency of the growing-cache
-               append path (config 4)
-  e2e        : the public API call with host buffers: H2D of q (pinned),
-               fused attention for all layers, D2H of outputs, per step
+               (timed first, on a fresh allocator)
+  flash_attn_fp16 : flash-attn's fp16 decode kernel on the same shape (a
+               library reference point; null when not importable)
+  store      : compress GB/s (fp16 K+V input bytes / wall time of
+               LayerCacheState.prefill_many over each layer's sequences), the
+               device passes, their HBM fraction, and the per-event latency of
+               the growing-cache append path (config 4)
+  e2e        : the public API call with host buffers: per layer H2D of q
+               (pinned) and D2H of the output on a side stream, overlapped
+               with the neighbouring layers' fused attention, per step
   cpu_baseline / --impl reference : the C oracle (a port of the reference's
                algorithm; the reference itself is Python/numpy) on host cores
 
