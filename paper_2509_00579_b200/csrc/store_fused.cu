@@ -1006,15 +1006,27 @@ store_offsets_kernel(StoreParams P, unsigned long long *nb0) {
     unsigned long long pbits = 0, pbytes = 0;
     uint32_t mx = 0;
     bool bad = false;
-    for (long t0 = 0; t0 < nb; t0 += 1024) {
-        const long b = t0 + tid;
-        uint32_t size = 0;
+    // this thread's block histogram for the next round is loaded one round
+    // ahead, so the dependent global load is off the scan's critical path
+    // (single-CTA kernel: ~20 rounds of load -> scan on a config-2 slice)
+    uint4 hcur[4], hnxt[4];
+    auto load_h = [&](long b, uint4 (&h)[4]) {
         if (b < nb) {
             const uint4 *h4 = reinterpret_cast<const uint4 *>(bh + (size_t)b * 32);
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) h[qq] = h4[qq];
+        }
+    };
+    load_h(tid, hcur);
+    for (long t0 = 0; t0 < nb; t0 += 1024) {
+        const long b = t0 + tid;
+        load_h(b + 1024, hnxt);
+        uint32_t size = 0;
+        if (b < nb) {
             uint32_t bits = 0;
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
-                const uint4 u = h4[qq];
+                const uint4 u = hcur[qq];
                 const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -1054,6 +1066,8 @@ store_offsets_kernel(StoreParams P, unsigned long long *nb0) {
         __syncthreads();
         if (tid == 0) carry_s = carry + wsum[31];
         __syncthreads();
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) hcur[qq] = hnxt[qq];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
