@@ -982,106 +982,109 @@ extern "C" int kvc_store_append(const void *k_dev, const void *v_dev, int x_dtyp
 // counters update.  One 1024-thread CTA per tensor (blockIdx.y).
 // ---------------------------------------------------------------------------
 namespace {
+// Arena offsets for the prefill fast path, all CTAs at once: CTA (c, t) takes
+// blocks [1024c, 1024c + 1024) of tensor t, sizes them from pass A's block
+// histograms and the code lengths, scans them locally, and gets the prefix of
+// the CTAs before it by a decoupled look-back over per-CTA status words (the
+// config-2 slice's 20 CTAs).  The last CTA to finish (ticket) writes the arena
+// counters.  ws per tensor: [0] bits, [1] bytes, [2] max extent, [3] bad,
+// [4] ticket, [5..7] pad, [8..8+NC) status (flag << 62 | value); zeroed by the
+// launcher.  Replaces a single-CTA loop over the blocks (52 us -> a few us).
 __global__ void __launch_bounds__(1024)
-store_offsets_kernel(StoreParams P, unsigned long long *nb0) {
-    const StoreTensor S = P.t[blockIdx.y];
+store_offsets_kernel(StoreParams P, unsigned long long *nb0, unsigned long long *ws_all, int NC) {
+    const int t = blockIdx.y, c = blockIdx.x;
+    const StoreTensor S = P.t[t];
     const long nb = (long)P.n_chunks * P.H_local;
-    const uint16_t *bh = P.blk_hist + (size_t)blockIdx.y * nb * 32;
+    const uint16_t *bh = P.blk_hist + (size_t)t * nb * 32;
     const int n_units = S.mode == KVC_V_TOKEN ? P.bs : P.D;
     const uint32_t hdr = kvc_header_bytes(P.bs, n_units);
+    unsigned long long *ws = ws_all + (size_t)t * (8 + NC);
+    unsigned long long *status = ws + 8;
     __shared__ uint32_t len[32];
     __shared__ unsigned long long wsum[32];
-    __shared__ unsigned long long carry_s;
+    __shared__ unsigned long long s_prefix;
     __shared__ unsigned long long r_bits[32], r_bytes[32];
     __shared__ uint32_t r_mx[32];
     __shared__ int r_bad;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid < 32) len[tid] = S.cb->lengths[tid];
-    if (tid == 0) {
-        carry_s = 0;
-        r_bad = 0;
-    }
-    __syncthreads();
+    if (tid == 0) r_bad = 0;
     const uint64_t cursor = S.counters->cursor, n0 = S.counters->n_blocks;
-    unsigned long long pbits = 0, pbytes = 0;
-    uint32_t mx = 0;
+    __syncthreads();
+    const long b = (long)c * 1024 + tid;
+    uint32_t size = 0, bits = 0, by = 0;
     bool bad = false;
-    // this thread's block histogram for the next round is loaded one round
-    // ahead, so the dependent global load is off the scan's critical path
-    // (single-CTA kernel: ~20 rounds of load -> scan on a config-2 slice)
-    uint4 hcur[4], hnxt[4];
-    auto load_h = [&](long b, uint4 (&h)[4]) {
-        if (b < nb) {
-            const uint4 *h4 = reinterpret_cast<const uint4 *>(bh + (size_t)b * 32);
+    if (b < nb) {
+        const uint4 *h4 = reinterpret_cast<const uint4 *>(bh + (size_t)b * 32);
 #pragma unroll
-            for (int qq = 0; qq < 4; ++qq) h[qq] = h4[qq];
-        }
-    };
-    load_h(tid, hcur);
-    for (long t0 = 0; t0 < nb; t0 += 1024) {
-        const long b = t0 + tid;
-        load_h(b + 1024, hnxt);
-        uint32_t size = 0;
-        if (b < nb) {
-            uint32_t bits = 0;
+        for (int qq = 0; qq < 4; ++qq) {
+            const uint4 u = h4[qq];
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-            for (int qq = 0; qq < 4; ++qq) {
-                const uint4 u = hcur[qq];
-                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int s0 = 8 * qq + 2 * k;
-                    const uint32_t c0 = w[k] & 0xFFFFu, c1 = w[k] >> 16;
-                    bad |= (c0 && !len[s0]) || (c1 && !len[s0 + 1]);
-                    bits += c0 * len[s0] + c1 * len[s0 + 1];
-                }
+            for (int k = 0; k < 4; ++k) {
+                const int s0 = 8 * qq + 2 * k;
+                const uint32_t c0 = w[k] & 0xFFFFu, c1 = w[k] >> 16;
+                bad |= (c0 && !len[s0]) || (c1 && !len[s0 + 1]);
+                bits += c0 * len[s0] + c1 * len[s0 + 1];
             }
-            const uint32_t by = (bits + 7) / 8;
-            size = (hdr + by + 3) & ~3u;
-            pbits += bits;
-            pbytes += by;
-            mx = max(mx, size);
         }
-        unsigned long long v = size;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += y;
-        }
-        if (lane == 31) wsum[warp] = v;
-        __syncthreads();
-        if (warp == 0) {
-            unsigned long long w = wsum[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
-            }
-            wsum[lane] = w;
-        }
-        __syncthreads();
-        const unsigned long long carry = carry_s;
-        const unsigned long long excl = carry + (warp ? wsum[warp - 1] : 0ull) + v - size;
-        if (b < nb) S.offsets[n0 + b] = (uint32_t)(cursor + excl);
-        __syncthreads();
-        if (tid == 0) carry_s = carry + wsum[31];
-        __syncthreads();
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) hcur[qq] = hnxt[qq];
+        by = (bits + 7) / 8;
+        size = (hdr + by + 3) & ~3u;
     }
+    unsigned long long v = size;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) wsum[warp] = v;
+    unsigned long long pbits = bits, pbytes = by;
+    uint32_t mx = size;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         pbits += __shfl_xor_sync(0xffffffffu, pbits, o);
         pbytes += __shfl_xor_sync(0xffffffffu, pbytes, o);
         mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
-    if (bad) r_bad = 1;
     if (lane == 0) {
         r_bits[warp] = pbits;
         r_bytes[warp] = pbytes;
         r_mx[warp] = mx;
     }
+    if (bad) r_bad = 1;
     __syncthreads();
+    if (warp == 0) {
+        unsigned long long w = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        wsum[lane] = w;
+        const unsigned long long total = __shfl_sync(0xffffffffu, w, 31);  // this CTA's sum
+        // decoupled look-back (thread 0): publish the aggregate, then walk back
+        if (lane == 0) {
+            const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kMask = (1ull << 62) - 1;
+            if (c == 0) {
+                st_release(&status[0], kInc | total);
+                s_prefix = 0;
+            } else {
+                st_release(&status[c], kAgg | total);
+                unsigned long long pre = 0;
+                for (int q = c - 1; q >= 0; --q) {
+                    unsigned long long sw;
+                    do { sw = ld_acquire(&status[q]); } while ((sw >> 62) == 0);
+                    pre += sw & kMask;
+                    if ((sw >> 62) == 2) break;
+                }
+                st_release(&status[c], kInc | (pre + total));
+                s_prefix = pre;
+            }
+        }
+    }
+    __syncthreads();
+    const unsigned long long excl = s_prefix + (warp ? wsum[warp - 1] : 0ull) + v - size;
+    if (b < nb) S.offsets[n0 + b] = (uint32_t)(cursor + excl);
     if (tid == 0) {
         unsigned long long tb = 0, ty = 0;
         uint32_t m = 0;
@@ -1090,19 +1093,32 @@ store_offsets_kernel(StoreParams P, unsigned long long *nb0) {
             ty += r_bytes[w];
             m = max(m, r_mx[w]);
         }
-        nb0[blockIdx.y] = n0;
-        const unsigned long long total = carry_s;
-        kvc_arena_counters *ct = S.counters;
-        if (r_bad) {
-            if (!ct->err) ct->err = KVC_ERR_CODEC;
-        } else if (cursor + total > S.capacity || cursor + total > 0xFFFFFFFFull) {
-            if (!ct->err) ct->err = KVC_ERR_ARENA_FULL;
-        } else {
-            ct->cursor = cursor + total;
-            ct->n_blocks = n0 + (uint64_t)nb;
-            ct->payload_bits += tb;
-            ct->payload_bytes += ty;
-            if (m > ct->max_extent) ct->max_extent = m;
+        atomicAdd(&ws[0], tb);
+        atomicAdd(&ws[1], ty);
+        atomicMax(&ws[2], (unsigned long long)m);
+        if (r_bad) atomicOr(&ws[3], 1ull);
+        __threadfence();
+        if (atomicAdd(&ws[4], 1ull) == (unsigned long long)(NC - 1)) {
+            __threadfence();
+            // last CTA: every status is inclusive by now; its own holds the total
+            const unsigned long long total = ld_acquire(&status[NC - 1]) & ((1ull << 62) - 1);
+            const unsigned long long bits_all = atomicAdd(&ws[0], 0ull);
+            const unsigned long long bytes_all = atomicAdd(&ws[1], 0ull);
+            const unsigned long long mx_all = atomicAdd(&ws[2], 0ull);
+            const bool bad_all = atomicAdd(&ws[3], 0ull) != 0;
+            nb0[t] = n0;
+            kvc_arena_counters *ct = S.counters;
+            if (bad_all) {
+                if (!ct->err) ct->err = KVC_ERR_CODEC;
+            } else if (cursor + total > S.capacity || cursor + total > 0xFFFFFFFFull) {
+                if (!ct->err) ct->err = KVC_ERR_ARENA_FULL;
+            } else {
+                ct->cursor = cursor + total;
+                ct->n_blocks = n0 + (uint64_t)nb;
+                ct->payload_bits += bits_all;
+                ct->payload_bytes += bytes_all;
+                if ((uint32_t)mx_all > ct->max_extent) ct->max_extent = (uint32_t)mx_all;
+            }
         }
     }
 }
@@ -1213,8 +1229,14 @@ extern "C" int kvc_store_prefill(const void *k_dev, const void *v_dev, int x_dty
     P.blk_hist = const_cast<uint16_t *>(blk_hist_dev);
     unsigned long long *nb0 = static_cast<unsigned long long *>(workspace_dev);  // [2]
     P.err = reinterpret_cast<int *>(nb0 + 2);
-    KVC_CUDA_TRY(cudaMemsetAsync(P.err, 0, sizeof(int), s));
-    store_offsets_kernel<<<dim3(1, 2), 1024, 0, s>>>(P, nb0);
+    const long nbl = (long)n_chunks * H_local;
+    const int NC = (int)((nbl + 1023) / 1024);
+    // offsets-kernel scratch at +256: per tensor 8 accumulators + NC status words
+    unsigned long long *ows = reinterpret_cast<unsigned long long *>(static_cast<char *>(workspace_dev) + 256);
+    const size_t scratch = 256 + (size_t)2 * (8 + NC) * 8;
+    if (workspace_bytes < scratch) return kvc_fail(KVC_ERR_CONFIG, "store workspace too small");
+    KVC_CUDA_TRY(cudaMemsetAsync(workspace_dev, 0, scratch, s));
+    store_offsets_kernel<<<dim3(NC, 2), 1024, 0, s>>>(P, nb0, ows, NC);
     int st = kvc_check_launch("store_offsets_kernel");
     if (st) return st;
     P.nb0 = nb0;
