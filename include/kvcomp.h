@@ -140,8 +140,11 @@ size_t kvc_codebook_bytes(void);
  * NULL.  row_stride = elements between consecutive tokens of x (H*D for
  * a contiguous [ctx, H, D] tensor). */
 int kvc_quantize(const void *x_dev, int x_dtype, long row_stride, int n_chunks, int H, int D,
-                 int bs, int mode, double rel, uint8_t *codes_dev, float *metas_dev,
-                 uint64_t *hist_dev, void *stream);
+                 int bs, int mode, double rel, const float *k_ranges_dev, uint8_t *codes_dev,
+                 float *metas_dev, uint64_t *hist_dev, void *stream);
+/*   mode KVC_K_CHANNEL (quantizer.py:191-197): k_ranges_dev = f32 [2][H][D]
+ *   whole-context (min, max) per channel; codes clipped to [0, ceil(1/rel)].
+ *   k_ranges_dev is ignored (may be NULL) for the other modes. */
 
 /* Entropy-code n_chunks*H_local quantised blocks (order b = chunk*H_local +
  * h) and append them to an arena in that order, reading and advancing the

@@ -618,7 +618,10 @@ int orc_k_scores(const uint8_t *arena, const uint32_t *offsets, long n_blocks, l
     return c.err;
 }
 
-/* attention.py:168-173 */
+/* attention.py:168-173.  The reference's e.sum() is numpy's pairwise
+ * summation (error ~ eps log n); a naive f32 running sum drifts by ~1e-4
+ * relative over a 128K-token row, so the sum is accumulated in binary64 and
+ * rounded once (closer to the exact sum than either). */
 void orc_softmax_rows(const float *x, long rows, long cols, float *out)
 {
     for (long r = 0; r < rows; ++r) {
@@ -626,9 +629,10 @@ void orc_softmax_rows(const float *x, long rows, long cols, float *out)
         float *o = out + r * cols;
         float m = xr[0];
         for (long j = 1; j < cols; ++j) if (xr[j] > m) m = xr[j];
-        float s = 0.f;
-        for (long j = 0; j < cols; ++j) { o[j] = expf(xr[j] - m); s += o[j]; }
-        for (long j = 0; j < cols; ++j) o[j] /= s;
+        double s = 0.0;
+        for (long j = 0; j < cols; ++j) { o[j] = expf(xr[j] - m); s += (double)o[j]; }
+        const float sf = (float)s;
+        for (long j = 0; j < cols; ++j) o[j] /= sf;
     }
 }
 

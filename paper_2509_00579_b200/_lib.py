@@ -82,7 +82,7 @@ SIGNATURES = {
     "kvc_codebook_lengths": (I, [P, I, P]),
     "kvc_codebook_build_tables": (I, [P, P]),
     "kvc_codebook_bytes": (SZ, []),
-    "kvc_quantize": (I, [P, I, L, I, I, I, I, I, D_, P, P, P, P]),
+    "kvc_quantize": (I, [P, I, L, I, I, I, I, I, D_, P, P, P, P, P]),
     "kvc_encode_append": (I, [P, P, I, I, I, I, U32, I, I, I, I, P, P, U64, P, P, P, P]),
     "kvc_encode_workspace_bytes": (SZ, [I, I]),
     "kvc_store_append": (I, [P, P, I, L, I, I, I, I, I, I, I, D_, D_, P, U32, P, I, P, I, P, U64,

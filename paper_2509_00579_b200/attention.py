@@ -20,7 +20,7 @@ import torch
 
 from . import _lib
 from .codec import DataMovement
-from .errors import CodecError
+from .errors import CodecError, ConfigError
 from .kvcache import LayerCacheState
 from .tensor_io import CacheTensor
 
@@ -151,6 +151,34 @@ class _BatchDesc:
 _default_desc_cache = _BatchDesc()
 
 
+def _check_batch(states: Sequence[LayerCacheState], q: torch.Tensor, n_q_heads_per_kv: int,
+                 out: Optional[torch.Tensor]):
+    """Shape/dtype/device validation before raw pointers reach the kernels:
+    every state shares (H, D, block size, device); q is a contiguous f32
+    [B, H*group, D] tensor on that device, out likewise (ConfigError for
+    mixed states, CodecError for tensors, as the reference's shape checks,
+    attention.py:44-47)."""
+    if len(states) == 0:
+        raise ConfigError("attention over an empty batch of states")
+    s0 = states[0]
+    for s in states[1:]:
+        if (s.head_num, s.head_dim, s.cfg_k.block_size, s.device) != (
+                s0.head_num, s0.head_dim, s0.cfg_k.block_size, s0.device):
+            raise ConfigError("batched states must share head_num, head_dim, block_size and device")
+    shape = (len(states), s0.head_num * n_q_heads_per_kv, s0.head_dim)
+    if not isinstance(q, torch.Tensor) or tuple(q.shape) != shape:
+        raise CodecError(f"query must be a tensor of shape {shape}")
+    if q.dtype != torch.float32 or q.device != s0.device or not q.is_contiguous():
+        raise CodecError("query must be a contiguous float32 tensor on the states' device")
+    if out is not None and (tuple(out.shape) != shape or out.dtype != torch.float32
+                            or out.device != s0.device or not out.is_contiguous()):
+        raise CodecError(f"out must be a contiguous float32 tensor of shape {shape} on the "
+                         "states' device")
+    for s in states:
+        if s.context_len < 1:
+            raise CodecError("attention over an empty context")
+
+
 def attention_batched(states: Sequence[LayerCacheState], q: torch.Tensor,
                       want_scores: bool = False, desc_cache: Optional[_BatchDesc] = None,
                       workspace: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
@@ -160,6 +188,7 @@ def attention_batched(states: Sequence[LayerCacheState], q: torch.Tensor,
     err [1] int32: the device error word of this call, or None with
     want_err=False -- the decode loop's fire-and-forget path, which skips the
     per-call zero fill)."""
+    _check_batch(states, q, 1, out)
     B = len(states)
     s0 = states[0]
     H, D, bs = s0.head_num, s0.head_dim, s0.cfg_k.block_size
@@ -274,14 +303,16 @@ def attention_gqa(states: Sequence[LayerCacheState], q: torch.Tensor, group: int
     launch per member.  check=True synchronises and raises the device error
     word (CodecError on a corrupt stream); check=False leaves the launch
     asynchronous (the bench's decode loop)."""
+    if not isinstance(group, int) or group < 1:
+        raise ConfigError("group must be a positive integer")
+    if q.ndim != 3 or q.shape[1] % group != 0:
+        raise CodecError("query heads must be a multiple of the group size")
+    _check_batch(states, q, group, out)
     B, HQ, D = q.shape
     H = HQ // group
     dev = q.device
     if out is None:
         out = torch.empty((B, HQ, D), dtype=torch.float32, device=dev)
-    elif (tuple(out.shape) != (B, HQ, D) or out.dtype != torch.float32 or not out.is_contiguous()
-          or out.device != dev):
-        raise CodecError("out must be a contiguous float32 [B, H*group, D] tensor on q's device")
     cache = desc_cache if desc_cache is not None else _BatchDesc()
     if group in (2, 4) and _fused_supported(states) and all(
             max(s.k_codebook.max_code_length, s.v_codebook.max_code_length) <= 6 for s in states):

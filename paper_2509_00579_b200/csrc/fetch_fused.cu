@@ -1665,6 +1665,10 @@ SplitPlan pick_split_plan(int max_chunks, long units, int ctas_per_sm, int pairs
                           int uniform_cps, double start) {
     SplitPlan plan{};
     auto set_parts = [&](const std::vector<int> &parts) {
+        if (parts.size() > (size_t)kMaxPlan) {  // unreachable: every candidate is bounded above
+            fprintf(stderr, "[kvc] split plan of %zu parts exceeds %d\n", parts.size(), kMaxPlan);
+            abort();
+        }
         plan.n = (int)parts.size();
         plan.begin[0] = 0;
         for (int i = 0; i < plan.n; ++i) plan.begin[i + 1] = plan.begin[i] + parts[i];
@@ -1686,7 +1690,14 @@ SplitPlan pick_split_plan(int max_chunks, long units, int ctas_per_sm, int pairs
         }
     }
     if (max_splits > kMaxPlan) max_splits = kMaxPlan;
-    const int ucps = uniform_cps > 0 ? uniform_cps : max_chunks;
+    if (max_splits < 1) max_splits = 1;
+    int ucps = uniform_cps > 0 ? uniform_cps : max_chunks;
+    // the plan is a fixed-size kernel parameter: never more than max_splits
+    // uniform splits (few heads x long contexts would otherwise ask for more)
+    if (ucps > 0 && (max_chunks + ucps - 1) / ucps > max_splits) {
+        const int need = (max_chunks + max_splits - 1) / max_splits;
+        ucps = (need + pairs - 1) / pairs * pairs;
+    }
     std::vector<int> best;
     for (int c0 = 0; c0 < max_chunks; c0 += ucps) best.push_back(std::min(ucps, max_chunks - c0));
     if (best.empty()) best.push_back(1);

@@ -53,10 +53,30 @@ __device__ __forceinline__ void hist_add(uint32_t *sh_hist, uint32_t code, bool 
     if ((threadIdx.x & 31) == leader) atomicAdd(&sh_hist[code], (uint32_t)__popc(peers));
 }
 
+// K_CHANNEL (quantizer.py:191-197): whole-context ranges, codes clipped to
+// [0, clamp_max] (values outside the ranges appear after they were fixed).
+__device__ __forceinline__ uint8_t quant_code_clip(float x, float vmin, double s64, double r64,
+                                                   int clamp_max) {
+    if (!(s64 > 0.0)) return 0;
+    double d = __dsub_rn((double)x, (double)vmin);
+    double t = __dmul_rn(d, r64);
+    double f = floor(t);
+    double frac = __dsub_rn(t, f);
+    if (fabs(frac - 0.5) < 1.0e-11 * (fabs(t) + 1.0)) {
+        t = __ddiv_rn(d, s64);
+        f = floor(t);
+        frac = __dsub_rn(t, f);
+    }
+    if (frac >= 0.5) f += 1.0;
+    f = fmin(fmax(f, 0.0), (double)clamp_max);
+    return (uint8_t)(int)f;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kQuantThreads)
 quantize_kernel(const T *__restrict__ x, long row_stride, int H, int D, int bs, int mode,
-                double rel, uint8_t *__restrict__ codes, float *__restrict__ metas,
+                double rel, const float *__restrict__ ranges, int clamp_max,
+                uint8_t *__restrict__ codes, float *__restrict__ metas,
                 unsigned long long *__restrict__ hist) {
     __shared__ uint32_t sh_hist[256];
     const long b = blockIdx.x;
@@ -104,17 +124,24 @@ quantize_kernel(const T *__restrict__ x, long row_stride, int H, int D, int bs, 
             int c = c0 + threadIdx.x;
             bool ok = c < D;
             float lo = 3.4e38f, hi = -3.4e38f;
-            if (ok)
+            if (ok && ranges) {  // K_CHANNEL: ranges [2][H][D]
+                lo = ranges[(long)head * D + c];
+                hi = ranges[(long)(H + head) * D + c];
+            } else if (ok) {
                 for (int r = 0; r < bs; ++r) {
                     float v = kvc_load(blk + (long)r * row_stride + c);
                     lo = fminf(lo, v);
                     hi = fmaxf(hi, v);
                 }
+            }
             float scale = ok ? (float)__dmul_rn(rel, __dsub_rn((double)hi, (double)lo)) : 0.f;
             double s64 = (double)scale;
             double r64 = s64 > 0.0 ? __drcp_rn(s64) : 0.0;
             for (int r = 0; r < bs; ++r) {
-                uint8_t code = ok ? quant_code(kvc_load(blk + (long)r * row_stride + c), lo, s64, r64) : 0;
+                const float xv = ok ? kvc_load(blk + (long)r * row_stride + c) : 0.f;
+                uint8_t code = !ok ? 0
+                               : ranges ? quant_code_clip(xv, lo, s64, r64, clamp_max)
+                                        : quant_code(xv, lo, s64, r64);
                 if (ok) out[(long)r * D + c] = code;
                 if (do_hist) hist_add(sh_hist, code, ok);
             }
@@ -348,24 +375,29 @@ extern "C" size_t kvc_encode_workspace_bytes(int nb, int bs) {
 }
 
 extern "C" int kvc_quantize(const void *x_dev, int x_dtype, long row_stride, int n_chunks, int H,
-                            int D, int bs, int mode, double rel, uint8_t *codes_dev,
-                            float *metas_dev, uint64_t *hist_dev, void *stream) {
+                            int D, int bs, int mode, double rel, const float *k_ranges_dev,
+                            uint8_t *codes_dev, float *metas_dev, uint64_t *hist_dev,
+                            void *stream) {
     if (n_chunks < 0 || H < 1 || D < 1 || bs < 1) return kvc_fail(KVC_ERR_CONFIG, "bad shape");
-    if (mode != KVC_K_BLOCK && mode != KVC_V_TOKEN)
-        return kvc_fail(KVC_ERR_CONFIG, "kvc_quantize supports K_BLOCK and V_TOKEN");
+    if (mode != KVC_K_BLOCK && mode != KVC_V_TOKEN && mode != KVC_K_CHANNEL)
+        return kvc_fail(KVC_ERR_CONFIG, "unknown quantisation mode");
+    if (mode == KVC_K_CHANNEL && k_ranges_dev == nullptr)
+        return kvc_fail(KVC_ERR_CONFIG, "K_CHANNEL quantization requires whole-context channel_ranges");
+    if (mode != KVC_K_CHANNEL) k_ranges_dev = nullptr;
     if (!(rel >= 1.0 / 255.0 && rel <= 1.0)) return kvc_fail(KVC_ERR_CONFIG, "rel outside [1/255, 1]");
+    const int clamp_max = (int)ceil(1.0 / rel);
     long nb = (long)n_chunks * H;
     if (nb == 0) return KVC_OK;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     auto *hist = reinterpret_cast<unsigned long long *>(hist_dev);
     if (x_dtype == KVC_F16)
         quantize_kernel<__half><<<(unsigned)nb, kQuantThreads, 0, s>>>(
-            static_cast<const __half *>(x_dev), row_stride, H, D, bs, mode, rel, codes_dev,
-            metas_dev, hist);
+            static_cast<const __half *>(x_dev), row_stride, H, D, bs, mode, rel, k_ranges_dev,
+            clamp_max, codes_dev, metas_dev, hist);
     else if (x_dtype == KVC_F32)
         quantize_kernel<float><<<(unsigned)nb, kQuantThreads, 0, s>>>(
-            static_cast<const float *>(x_dev), row_stride, H, D, bs, mode, rel, codes_dev,
-            metas_dev, hist);
+            static_cast<const float *>(x_dev), row_stride, H, D, bs, mode, rel, k_ranges_dev,
+            clamp_max, codes_dev, metas_dev, hist);
     else
         return kvc_fail(KVC_ERR_TENSOR, "unsupported dtype");
     return kvc_check_launch("quantize_kernel");

@@ -150,7 +150,7 @@ class LayerCacheState:
 
     @classmethod
     def prefill_many(cls, items, cfg_k: QuantConfig, cfg_v: QuantConfig,
-                     check: bool = False, **kw) -> list:
+                     check: bool = True, **kw) -> list:
         """prefill() of several (k, v) pairs (the layers or sequences of one
         prompt), pipelined: pass A of item i+1 is launched before the host
         builds item i's codebooks, so the GPU runs it while the host works and
@@ -164,7 +164,10 @@ class LayerCacheState:
             cur = nxt
             nxt = (cls._prefill_begin(*items[i + 1], cfg_k, cfg_v, **kw)
                    if i + 1 < len(items) else None)
-            out.append(cls._prefill_finish(cur, check))
+            out.append(cls._prefill_finish(cur, False))
+        if check:  # one synchronisation for the whole batch, after every launch
+            for st in out:
+                st.check()
         return out
 
     @classmethod
@@ -179,9 +182,15 @@ class LayerCacheState:
             raise ConfigError("K and V tensors must share dimensions")
         if kv.shape[0] < 1:
             raise ConfigError("prefill requires at least one token")
-        src_dtype = np.dtype(str(kv.dtype).replace("torch.", "")) if isinstance(
-            kv, torch.Tensor) else np.dtype(kv.dtype)
         kt = as_device_tensor(kv, device)
+        # state dtype (its itemsize is the "original bytes" of collect_stats,
+        # bench.py:77-95): fp16 stays fp16; bf16 (no numpy dtype) is reported
+        # as a 2-byte original, everything else as f32 like the reference
+        if isinstance(kv, torch.Tensor):
+            src_dtype = np.dtype(np.float16) if kv.dtype in (torch.float16, torch.bfloat16) \
+                else np.dtype(np.float32)
+        else:
+            src_dtype = np.dtype(kv.dtype)
         vt = as_device_tensor(vv, kt.device)
         ctx, H, D = kt.shape
         bs = cfg_k.block_size
@@ -230,11 +239,10 @@ class LayerCacheState:
                                           else None, hist.data_ptr(), stream),
                        "kvc_store_hist")
         elif n_full and not fused:
-            if k_is_ch:
-                raise ConfigError("K_CHANNEL needs the single-pass store kernels (shape too big)")
             kcodes, kmetas = quantize_tokens(kt, n_chunks, H, D, bs, cfg_k.mode,
                                              cfg_k.rel_quant_scale,
-                                             hist[:256] if codebooks is None else None)
+                                             hist[:256] if codebooks is None else None,
+                                             k_ranges=ranges_dev)
             vcodes, vmetas = quantize_tokens(vt, n_chunks, H, D, bs, QuantMode.V_TOKEN,
                                              cfg_v.rel_quant_scale,
                                              hist[256:] if codebooks is None else None)
@@ -316,7 +324,7 @@ class LayerCacheState:
             else:
                 if kcodes is None:
                     kcodes, kmetas = quantize_tokens(kt, n_chunks, H, D, bs, cfg_k.mode,
-                                                     cfg_k.rel_quant_scale)
+                                                     cfg_k.rel_quant_scale, k_ranges=st._k_ranges)
                     vcodes, vmetas = quantize_tokens(vt, n_chunks, H, D, bs, QuantMode.V_TOKEN,
                                                      cfg_v.rel_quant_scale)
                 st._encode(kcodes, kmetas, vcodes, vmetas, n_chunks)
@@ -357,6 +365,8 @@ class LayerCacheState:
                 chunk_base, bs, D, n_units, cb.max_code_length, tab.data_ptr(), arena.buf_ptr,
                 arena.alloc_capacity, arena.offsets_ptr, arena.counters_ptr, ws.data_ptr(), stream)
             _lib.check(st, "kvc_encode_append")
+            if arena.capacity is not None:  # codec.py:313-318: a full arena raises here
+                arena.check("arena")
             arena.note_append(nb, worst)
         self.compressed_tokens += n_chunks * bs
 
@@ -393,6 +403,12 @@ class LayerCacheState:
             self.v_arena.alloc_capacity, self.v_arena.offsets_ptr, self.v_arena.counters_ptr,
             ws.data_ptr(), ws.numel(), torch.cuda.current_stream(self.device).cuda_stream)
         _lib.check(st, "kvc_store_append" if blk_hist is None else "kvc_store_prefill")
+        if self.k_arena.capacity is not None or self.v_arena.capacity is not None:
+            # fixed capacity: the device refuses blocks past it (sticky error);
+            # raise ArenaFullError now, as CompressedArena.append does
+            # (codec.py:313-318), before the host mirrors advance
+            self.k_arena.check("K arena")
+            self.v_arena.check("V arena")
         self.k_arena.note_append(nb, kw)
         self.v_arena.note_append(nb, vw)
         self.compressed_tokens += n_chunks * bs
@@ -405,7 +421,8 @@ class LayerCacheState:
             self._store(self._k_buffer, self._v_buffer, n_chunks)
             return
         kcodes, kmetas = quantize_tokens(self._k_buffer, n_chunks, self.head_num, self.head_dim,
-                                         bs, self.cfg_k.mode, self.cfg_k.rel_quant_scale)
+                                         bs, self.cfg_k.mode, self.cfg_k.rel_quant_scale,
+                                         k_ranges=self._k_ranges)
         vcodes, vmetas = quantize_tokens(self._v_buffer, n_chunks, self.head_num, self.head_dim,
                                          bs, QuantMode.V_TOKEN, self.cfg_v.rel_quant_scale)
         self._encode(kcodes, kmetas, vcodes, vmetas, n_chunks)

@@ -99,12 +99,18 @@ def dtype_code(t: torch.Tensor) -> int:
 
 
 def quantize_tokens(x: torch.Tensor, n_chunks: int, head_num: int, head_dim: int, bs: int,
-                    mode: QuantMode, rel: float, hist: Optional[torch.Tensor] = None):
+                    mode: QuantMode, rel: float, hist: Optional[torch.Tensor] = None,
+                    k_ranges: Optional[torch.Tensor] = None):
     """Device quantisation of x[t, h, :] for t < n_chunks*bs, blocks in
     chunk-major / head-minor order (kvcache.py:242-268).  Returns (codes
-    [nb, bs, D] u8, metas [nb, n_units, 2] f32)."""
+    [nb, bs, D] u8, metas [nb, n_units, 2] f32).  K_CHANNEL takes the
+    whole-context ranges as a device f32 tensor [2, H, D]."""
     if mode is QuantMode.K_CHANNEL:
-        raise ConfigError("K_CHANNEL quantisation is not implemented on the device yet")
+        if k_ranges is None:
+            raise ConfigError("K_CHANNEL quantization requires whole-context channel_ranges")
+        k_ranges = k_ranges.to(x.device, torch.float32).contiguous()
+        if tuple(k_ranges.shape) != (2, head_num, head_dim):
+            raise ConfigError("channel ranges must have shape (2, head_num, head_dim)")
     nb = n_chunks * head_num
     n_units = bs if mode is QuantMode.V_TOKEN else head_dim
     codes = torch.empty((nb, bs, head_dim), dtype=torch.uint8, device=x.device)
@@ -112,7 +118,8 @@ def quantize_tokens(x: torch.Tensor, n_chunks: int, head_num: int, head_dim: int
     if nb:
         st = _lib.lib().kvc_quantize(
             x.data_ptr(), dtype_code(x), head_num * head_dim, n_chunks, head_num, head_dim, bs,
-            mode.abi, float(rel), codes.data_ptr(), metas.data_ptr(),
+            mode.abi, float(rel), k_ranges.data_ptr() if mode is QuantMode.K_CHANNEL else None,
+            codes.data_ptr(), metas.data_ptr(),
             hist.data_ptr() if hist is not None else None,
             torch.cuda.current_stream(x.device).cuda_stream)
         _lib.check(st, "kvc_quantize")
@@ -134,8 +141,15 @@ def quantize_block(block, mode: QuantMode, cfg: QuantConfig, head_index: int, ct
     if mode is QuantMode.K_CHANNEL and channel_ranges is None:
         raise ConfigError("K_CHANNEL quantization requires whole-context channel_ranges")
     D = x.shape[1]
+    ranges = None
+    if mode is QuantMode.K_CHANNEL:  # quantizer.py:191-197: (mins, maxs) of length head_dim
+        ranges = torch.stack([torch.as_tensor(np.asarray(r, np.float32)) if not isinstance(
+            r, torch.Tensor) else r.to(torch.float32).cpu() for r in channel_ranges])
+        if tuple(ranges.shape) != (2, D):
+            raise ConfigError("channel_ranges must be two arrays of length head_dim")
+        ranges = ranges.reshape(2, 1, D).to(x.device)
     codes, metas = quantize_tokens(x.reshape(cfg.block_size, 1, D), 1, 1, D, cfg.block_size, mode,
-                                   cfg.rel_quant_scale)
+                                   cfg.rel_quant_scale, k_ranges=ranges)
     return QuantizedBlock(codes=codes[0], unit_mins=metas[0, :, 0].clone(),
                           unit_scales=metas[0, :, 1].clone(),
                           block_index=(ctx_start // cfg.block_size) * head_num + head_index,

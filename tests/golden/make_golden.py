@@ -308,7 +308,14 @@ def big_digests(do_cfg2=False):
         k = kv.generate_synthetic(spec).values.astype(np.float16)
         v = kv.generate_synthetic(replace(spec, seed=0 ^ 0x9E3779B9)).values.astype(np.float16)
         st = kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v), cfg_k, cfg_v)
-        res["cfg2_slice"] = _digest(st)
+        d = _digest(st)
+        # one reference attention_step on the slice (attention.py:176-188, ~40 s)
+        q = np.random.default_rng([0, 0x71726E67]).standard_normal((40, 128), dtype=np.float32)
+        r = kv.attention_step(st, q)
+        d["att_out"] = r.out.tolist()
+        d["att_scores_head0_first64"] = r.scores[0, :64].tolist()
+        d["att_scores_head39_last64"] = r.scores[39, -64:].tolist()
+        res["cfg2_slice"] = d
         print(f"cfg2 slice done {time.time()-t0:.1f}s")
     with open(path, "w") as fh:
         json.dump(res, fh, indent=1)
@@ -339,6 +346,16 @@ def main():
               rel_k=None, k_mode="kchannel")
     make_case("c_kchannel_f32_bs8", ctx=8 * 3 + 2, H=2, D=4, bs=8, buffer=16, dtype=np.float32,
               synthetic=False, seed=30, appended=20, rel_k=0.05, k_mode="kchannel")
+    # Fine quantisation scales on the hot shape (D 128, bs 64; BASELINE config 5
+    # sweep points): 7-12 bit codes and 21-256 symbol alphabets, 3 prefill
+    # blocks + > 128 appends (one growing-cache overflow event), so the
+    # 256-bin Store histograms, the look-back prefill and the single-symbol
+    # fused fetch are all pinned to the reference.
+    for nm, rk, rv, sd in (("c_fine_d128_255", 1 / 255, 1 / 255, 21),
+                           ("c_fine_d128_001", 0.01, 0.02, 22),
+                           ("c_fine_d128_002", 0.02, 0.05, 23)):
+        make_case(nm, ctx=64 * 3 + 20, H=2, D=128, bs=64, rel_k=rk, rel_v=rv, seed=sd,
+                  appended=150)
     if args.big or args.cfg2:
         big_digests(args.cfg2)
 

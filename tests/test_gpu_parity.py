@@ -549,3 +549,152 @@ def test_prefill_many_fixed_codebooks_and_kchannel(kv):
             ref = kv.LayerCacheState.prefill(k, v, cfg_k, cv, **extra)
             for a, b in ((st.k_arena, ref.k_arena), (st.v_arena, ref.v_arena)):
                 assert a.snapshot() == b.snapshot()
+
+
+def test_cfg2_slice_attention_matches_reference(kv):
+    """One config-2 (seq, layer) through the fused kernel vs the reference's own
+    attention_step on the same slice (big_digests.json, made by running kvpack)."""
+    dd = json.load(open(os.path.join(GOLDEN, "big_digests.json")))
+    if "att_out" not in dd.get("cfg2_slice", {}):
+        pytest.skip("cfg2 attention golden not generated")
+    d = dd["cfg2_slice"]
+    k = kv.generate_synthetic(kv.SyntheticSpec(32768, 40, 128, seed=0)).values.astype(np.float16)
+    v = kv.generate_synthetic(kv.SyntheticSpec(32768, 40, 128, seed=0 ^ 0x9E3779B9)).values.astype(
+        np.float16)
+    st = kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v),
+                                    kv.QuantConfig(kv.QuantMode.K_BLOCK),
+                                    kv.QuantConfig(kv.QuantMode.V_TOKEN))
+    q = np.random.default_rng([0, 0x71726E67]).standard_normal((40, 128), dtype=np.float32)
+    res = kv.attention_step(st, q)
+    assert max_relative_error(res.out.cpu().numpy(), np.array(d["att_out"])) <= TOL
+    sc = res.scores.cpu().numpy()
+    assert max_relative_error(sc[0, :64], np.array(d["att_scores_head0_first64"])) <= TOL
+    assert max_relative_error(sc[39, -64:], np.array(d["att_scores_head39_last64"])) <= TOL
+    # the decode-loop entry point (no scores, batched) on the same state
+    out = kv.attention_batched([st], torch.from_numpy(q[None]).cuda())[0]
+    assert max_relative_error(out[0].cpu().numpy(), np.array(d["att_out"])) <= TOL
+
+
+def test_cfg3_gqa_128k_matches_oracle(kv):
+    """Config-3 shape at full context: one Llama-3-8B KV head (group 4) over
+    131072 tokens + a ragged buffered tail, decode-once GQA kernel vs the C
+    oracle's attention_step, one call per group member."""
+    import oracle
+    H, G, ctx, extra = 1, 4, 131072, 45
+    k = oracle.generate_synthetic(ctx + extra, H, 128, seed=31).astype(np.float16)
+    v = oracle.generate_synthetic(ctx + extra, H, 128, seed=32).astype(np.float16)
+    st = kv.LayerCacheState.prefill(kv.CacheTensor(k[:ctx]), kv.CacheTensor(v[:ctx]),
+                                    kv.QuantConfig(kv.QuantMode.K_BLOCK),
+                                    kv.QuantConfig(kv.QuantMode.V_TOKEN))
+    ost = oracle.OracleState.prefill(k[:ctx], v[:ctx], n_threads=8)
+    for t in range(ctx, ctx + extra):
+        st.append_token(k[t].astype(np.float32), v[t].astype(np.float32))
+        ost.append_token(k[t].astype(np.float32), v[t].astype(np.float32))
+    assert st.k_arena.snapshot() == ost.arena_bytes("k")
+    assert st.v_arena.snapshot() == ost.arena_bytes("v")
+    q = np.random.default_rng(33).standard_normal((1, H * G, 128), dtype=np.float32)
+    out = kv.attention_gqa([st], torch.from_numpy(q).cuda(), G)
+    for j in range(G):
+        o_out, _ = ost.attention_step(q[0].reshape(H, G, 128)[:, j])
+        assert max_relative_error(out[0].view(H, G, 128)[:, j].cpu().numpy(), o_out) <= TOL
+
+
+@pytest.mark.parametrize("H,ctx", [(1, 65536), (2, 65536), (4, 131072)])
+def test_few_heads_long_context_split_plan(kv, H, ctx):
+    """Few (seq, head) units at long context ask for more uniform splits than
+    the plan parameter holds; the plan is clamped (advisor finding) and the
+    fused result still matches the per-state generic reference path."""
+    k = kv.generate_synthetic(kv.SyntheticSpec(ctx, H, 128, seed=80 + H)).values.astype(np.float16)
+    v = kv.generate_synthetic(kv.SyntheticSpec(ctx, H, 128, seed=90 + H)).values.astype(np.float16)
+    st = kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v),
+                                    kv.QuantConfig(kv.QuantMode.K_BLOCK),
+                                    kv.QuantConfig(kv.QuantMode.V_TOKEN))
+    q = np.random.default_rng(H).standard_normal((H, 128), dtype=np.float32)
+    out = kv.attention_batched([st], torch.from_numpy(q[None]).cuda())[0]
+    sc = kv.fused_k_scores(st, q)
+    w = torch.softmax(sc, dim=-1)
+    ref = kv.fused_v_output(st, w)
+    assert max_relative_error(out.cpu().numpy(), ref.cpu().numpy()) <= TOL
+
+
+def test_bf16_prefill_and_append(kv):
+    """bf16 KV (Llama checkpoints' dtype; numpy has no bf16): prefill and
+    appends accept it, quantise its exact f32 values, and report 2-byte
+    originals (advisor finding: the dtype lookup used to raise TypeError)."""
+    torch.manual_seed(3)
+    k = torch.randn(64 * 3 + 5, 2, 128, device="cuda").to(torch.bfloat16)
+    v = torch.randn(64 * 3 + 5, 2, 128, device="cuda").to(torch.bfloat16)
+    ck, cv = kv.QuantConfig(kv.QuantMode.K_BLOCK), kv.QuantConfig(kv.QuantMode.V_TOKEN)
+    st = kv.LayerCacheState.prefill(k, v, ck, cv)
+    ref = kv.LayerCacheState.prefill(k.float(), v.float(), ck, cv)
+    assert st.k_arena.snapshot() == ref.k_arena.snapshot()
+    assert st.v_arena.snapshot() == ref.v_arena.snapshot()
+    assert st.dtype.itemsize == 2
+    st.append_token(k[0], v[0])
+    ref.append_token(k[0].float(), v[0].float())
+    q = torch.randn(2, 128).numpy()
+    a, b = kv.attention_step(st, q), kv.attention_step(ref, q)
+    assert torch.equal(a.out, b.out)
+
+
+def test_batched_validation(kv):
+    """attention_batched / attention_gqa reject tensors the kernels would read
+    or write out of bounds (advisor finding)."""
+    g = load("c_fp16_d128")
+    st = _final_state(kv, g)
+    H = st.head_num
+    ok = torch.zeros((1, H, 128), device="cuda")
+    with pytest.raises(kv.CodecError):
+        kv.attention_batched([st], ok.half())
+    with pytest.raises(kv.CodecError):
+        kv.attention_batched([st], torch.zeros((1, H + 1, 128), device="cuda"))
+    with pytest.raises(kv.CodecError):
+        kv.attention_batched([st], ok, out=torch.zeros((1, H, 64), device="cuda"))
+    with pytest.raises(kv.CodecError):
+        kv.attention_gqa([st], torch.zeros((1, 3 * H, 128), device="cuda"), 2)
+    other = kv.LayerCacheState.prefill(kv.CacheTensor(g["k_in"][:, :1]),
+                                       kv.CacheTensor(g["v_in"][:, :1]),
+                                       kv.QuantConfig(kv.QuantMode.K_BLOCK),
+                                       kv.QuantConfig(kv.QuantMode.V_TOKEN))
+    with pytest.raises(kv.ConfigError):
+        kv.attention_batched([st, other], torch.zeros((2, H, 128), device="cuda"))
+
+
+def test_append_capacity_raises_arena_full(kv):
+    """A fixed-capacity arena raises ArenaFullError from append_token when an
+    overflow event does not fit (codec.py:313-318), not at a later fetch."""
+    g = load("c_fp16_d128")
+    ck, cv = _cfgs(kv, g)
+    st = kv.LayerCacheState.prefill(kv.CacheTensor(g["k_in"]), kv.CacheTensor(g["v_in"]), ck, cv)
+    cap = st.k_arena.size_bytes + 100
+    st2 = kv.LayerCacheState.prefill(kv.CacheTensor(g["k_in"]), kv.CacheTensor(g["v_in"]), ck, cv,
+                                     capacity=max(cap, st.v_arena.size_bytes + 100))
+    with pytest.raises(kv.ArenaFullError):
+        for t in range(int(g["cfg"][5])):
+            st2.append_token(g["k_app"][t], g["v_app"][t])
+
+
+def test_quantize_block_k_channel(kv):
+    """quantize_block in K_CHANNEL mode (quantizer.py:191-197): whole-context
+    ranges, codes clipped to max_code; equals the codes the Store wrote for
+    the reference's K_CHANNEL golden."""
+    g = load("c_kchannel")
+    ctx, H, D, bs, buffer, appended, rel_k, rel_v = unpack_cfg(g)
+    cfg = kv.QuantConfig(kv.QuantMode.K_CHANNEL, bs, rel_k, buffer)
+    rng = g["k_ranges"]
+    kin = g["k_in"].astype(np.float32)
+    for chunk in range(ctx // bs):
+        for h in range(H):
+            q = kv.quantize_block(kin[chunk * bs:(chunk + 1) * bs, h], kv.QuantMode.K_CHANNEL, cfg,
+                                  h, chunk * bs, H, channel_ranges=(rng[0][h], rng[1][h]))
+            x = kin[chunk * bs:(chunk + 1) * bs, h].astype(np.float64)
+            lo = rng[0][h].astype(np.float32).astype(np.float64)
+            sc = (np.float64(rel_k) * (rng[1][h].astype(np.float64) - lo)).astype(np.float32)
+            t = (x - lo) / np.where(sc > 0, sc.astype(np.float64), 1.0)
+            c = np.floor(t)
+            c += (t - c) >= 0.5
+            c = np.where(sc > 0, np.clip(c, 0, cfg.max_code), 0).astype(np.uint8)
+            assert np.array_equal(q.codes.cpu().numpy(), c)
+            assert np.array_equal(q.unit_scales.cpu().numpy(), sc)
+    with pytest.raises(kv.ConfigError):
+        kv.quantize_block(kin[:bs, 0], kv.QuantMode.K_CHANNEL, cfg, 0, 0, H)
