@@ -143,7 +143,57 @@ def cpu_fetch_sample(ctx, heads, seconds=15.0, threads=None):
     return eq_bytes / dt / 1e9, threads, n, dt
 
 
+UNIT = "GB/s (equivalent fp16 KV)"
+
+
+def kvpack_fetch_sample(ctx, heads, seconds=12.0):
+    """The UNMODIFIED reference (kvpack from baseline/_ref, pure Python +
+    numpy) through its own public API: LayerCacheState.prefill then
+    attention_step on one (seq, layer) slice of the workload shape, the
+    faster of n_threads 1 and all cores.  None when baseline/_ref
+    is not installed."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "kvpack")):
+        return None
+    sys.path.insert(0, ref)
+    try:
+        import kvpack
+    finally:
+        sys.path.remove(ref)
+    from dataclasses import replace
+    spec = kvpack.SyntheticSpec(ctx, heads, 128, seed=0)
+    k = kvpack.generate_synthetic(spec).values.astype(np.float16)
+    v = kvpack.generate_synthetic(replace(spec, seed=0 ^ 0x9E3779B9)).values.astype(np.float16)
+    st = kvpack.LayerCacheState.prefill(kvpack.CacheTensor(k), kvpack.CacheTensor(v),
+                                        kvpack.QuantConfig(kvpack.QuantMode.K_BLOCK),
+                                        kvpack.QuantConfig(kvpack.QuantMode.V_TOKEN))
+    q = np.random.default_rng([0, 0x71726E67]).standard_normal((heads, 128), dtype=np.float32)
+    best = None
+    for thr in sorted({1, os.cpu_count() or 1}):
+        n, t0 = 0, time.perf_counter()
+        while True:
+            kvpack.attention_step(st, q, n_threads=thr)
+            n += 1
+            if time.perf_counter() - t0 > seconds / 2:
+                break
+        dt = (time.perf_counter() - t0) / n
+        if best is None or dt < best[0]:
+            best = (dt, thr, n)
+    dt, thr, n = best
+    return {"value": round(2 * ctx * heads * 128 * 2 / dt / 1e9, 5), "unit": UNIT,
+            "cores": thr, "kind": "reference",
+            "sample": f"unmodified kvpack (baseline/_ref) attention_step x{n}, n_threads={thr}, "
+                      f"on one (seq, layer) slice {ctx} tok x {heads} heads x 128 fp16, "
+                      f"{dt:.2f} s each"}
+
+
 def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on the host cores, on a
+    bounded (seq, layer) slice of this config's shape, in this config's unit
+    (equivalent fp16 GB/s, so the driver's ratio compares like with like).
+    value = the C port of kvpack's algorithm (oracle/, all threads; the
+    faster CPU implementation, kind "port"); reference_python = the unmodified
+    kvpack package itself (kind "reference")."""
     if rank != 0:
         return
     ctx, heads = args.cpu_ctx, args.heads
@@ -165,18 +215,24 @@ def run_reference(args, rank, world):
     val = 2 * ctx * heads * 128 * 2 / dt / 1e9
     sample = (f"oracle attention_step (C port of kvpack, {threads} threads) on one (seq, layer) "
               f"slice: {ctx} tokens x {heads} heads x 128, fp16 synthetic, default scales")
-    print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": "GB/s",
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8 codes / f32 accumulate", "data": "synthetic",
-        "config": {"workload": "cfg2 Llama-2-13B KV fused fetch-attention (bounded CPU sample)",
+        "config": {"workload": PRESETS[args.config]["workload"] + " -- bounded CPU sample",
+                   "sample_slice": f"1 layer x 1 sequence x {ctx} tokens x {heads} KV heads x "
+                                   f"128 (the per-byte rate of the same workload shape)",
                    "layers": 1, "batch": 1, "ctx": ctx, "kv_heads": heads, "head_dim": 128},
-        "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
-        "e2e": {"value": round(val, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+        "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-    }), flush=True)
+    }
+    if not args.no_py_ref:
+        line["reference_python"] = kvpack_fetch_sample(min(ctx, 4096), heads,
+                                                        seconds=args.py_ref_seconds)
+    print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------
@@ -284,6 +340,11 @@ def main():
     ap.add_argument("--cpu-ctx", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-paper", action="store_true",
+                    help="skip the fused vs multistage vs matvec comparison")
+    ap.add_argument("--no-py-ref", action="store_true",
+                    help="skip the unmodified-kvpack CPU leg (baseline/_ref)")
+    ap.add_argument("--py-ref-seconds", type=float, default=12.0)
     args = ap.parse_args()
     for k, v in PRESETS[args.config].items():
         if getattr(args, k, None) is None:
@@ -410,12 +471,29 @@ def main():
     if world > 1:
         dist.barrier()
     stream = torch.cuda.current_stream()
+    # per-layer events inside the timed region (same stream as the launches):
+    # the fused kernel's (+ its combine's) average launch duration for the
+    # roofline, measured live over the timed steps rather than in isolation
+    lev = [[torch.cuda.Event(enable_timing=True) for _ in range(L + 1)]
+           for _ in range(args.steps)]
+
+    def timed_step(ev):
+        for layer in range(L):
+            ev[layer].record(stream)
+            layer_call(layer)
+        ev[L].record(stream)
+        if world > 1:
+            if share:
+                dist.all_gather(list(gathered.unbind(0)), outs)
+            else:
+                dist.all_gather_into_tensor(gathered, outs)
+
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(args.steps):
-            step()
+        for i in range(args.steps):
+            timed_step(lev[i])
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -425,20 +503,16 @@ def main():
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    # fused kernel alone (per layer launch) for the roofline: attention minus combine is
-    # dominated by the fused kernel; time one layer launch in isolation
-    lay_ms = []
-    for layer in range(min(L, 8)):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        layer_call(layer)
-        b.record(stream)
-        torch.cuda.synchronize()
-        lay_ms.append(a.elapsed_time(b))
-    lay_ms = float(np.mean(lay_ms))
+    lay_ms = float(np.mean([ev[l].elapsed_time(ev[l + 1]) for ev in lev for l in range(L)]))
     hbm_peak, peak_kind = _peaks()
-    ach = comp_bytes_layer[0] / (lay_ms * 1e-3) / 1e9
-
+    ach = float(np.mean(comp_bytes_layer)) / (lay_ms * 1e-3) / 1e9
+    # the paper's two kernel comparisons (reference
+    # bench.py:165-177, :297-321) on one (seq, layer) state of this workload:
+    # the fused pass vs the multistage pass (decode -> dequantise -> dense
+    # GEMVs) and vs the plain matvec on the materialised tensors
+    paper = None
+    if rank == 0 and not args.no_paper:
+        paper = paper_comparisons(kv, torch, states[0][0], stream)
     # e2e through the public API with host buffers
     qh = torch.empty((L, B, hl * G, 128), dtype=torch.float32).pin_memory()
     qh.copy_(q.cpu())
@@ -498,12 +572,15 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, thr, n, dt = cpu_fetch_sample(args.cpu_ctx, H, seconds=args.cpu_seconds)
-        cpu = {"value": round(v, 4), "unit": "GB/s", "cores": thr, "kind": "port",
+        cpu = {"value": round(v, 4), "unit": UNIT, "cores": thr, "kind": "port",
                "sample": f"oracle attention_step (C port of kvpack) x{n} on one (seq, layer) "
                          f"slice {args.cpu_ctx} tok x {H} heads x 128 fp16, {dt:.2f} s each"}
+        if not args.no_py_ref:
+            cpu["reference_python"] = kvpack_fetch_sample(min(args.cpu_ctx, 4096), H,
+                                                          seconds=args.py_ref_seconds)
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 2), "unit": "GB/s (equivalent fp16 KV)",
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u8 Huffman codes -> f32 accumulate",
@@ -541,9 +618,13 @@ def main():
                          "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
                          "traffic": _ncu_traffic(args.config), "peak_kind": peak_kind,
                          "binding": _ncu_binding(args.config),
+                         "launch_ms": round(lay_ms, 4),
+                         "ncu_launch_ms": _ncu_duration_ms(args.config),
                          "kernel": ("fused_attn_ws_kernel" if G == 1 else "fused_attn_gqa_kernel")
-                                   + " (+combine), one layer launch, compressed bytes"},
-            "e2e": {"value": round(e2e_val, 2), "unit": "GB/s (equivalent fp16 KV)",
+                                   + " (+combine) per layer launch, compressed bytes per launch "
+                                     "/ its average duration from CUDA events inside the timed "
+                                     "steps"},
+            "e2e": {"value": round(e2e_val, 2), "unit": UNIT,
                     "h2d_bytes_per_step": int(L * B * hl * G * 128 * 4),
                     "d2h_bytes_per_step": int(L * B * hl * G * 128 * 4)},
             "gpu_launches": int(args.steps * L * 2),  # fused kernel + combine per layer
@@ -551,6 +632,8 @@ def main():
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        if paper:
+            line["paper_comparisons"] = paper
         if args.config == 5:
             line["quant_sweep"] = quant_sweep(kv, torch, device, T, H, B)
         print(json.dumps(line), flush=True)
@@ -594,6 +677,61 @@ def quant_sweep(kv, torch, device, T, H, B):
                      "fetch_ms": round(ms, 4)})
         del states
     return rows
+
+
+def paper_comparisons(kv, torch, st, stream, reps=10):
+    """Fused vs multistage vs plain matvec on one (seq, layer) state, device
+    time per call (CUDA events on the launching stream), and the reference's
+    equivalent decompression throughput (bench.py:165-177)."""
+    H = st.head_num
+    q = torch.randn((H, 128), device=st.device)
+
+    def dev_ms(fn):
+        for _ in range(2):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    cache = kv.attention._BatchDesc()
+    qb = q.unsqueeze(0).contiguous()
+    t_fused = dev_ms(lambda: kv.attention_batched([st], qb, desc_cache=cache, want_err=False))
+    t_multi = dev_ms(lambda: kv.multistage_attention(st, q))
+    k_mat, v_mat = st.fetch_dequantized()
+    t_mv = dev_ms(lambda: kv.reference_output(v_mat, kv.softmax_rows(
+        kv.reference_scores(k_mat, q))))
+    del k_mat, v_mat
+    orig = kv.collect_stats(st).original_bytes
+    edt = kv.equivalent_decompression_throughput(orig, t_fused * 1e-3, t_mv * 1e-3)
+    return {"state": f"one (seq, layer): {st.context_len} tok x {H} heads x 128",
+            "fused_ms": round(t_fused, 4), "multistage_ms": round(t_multi, 4),
+            "matvec_dequantized_f32_ms": round(t_mv, 4),
+            "fused_vs_multistage_speedup": round(t_multi / t_fused, 2),
+            "fused_vs_matvec_speedup": round(t_mv / t_fused, 2),
+            "equivalent_decompression_throughput": edt if isinstance(edt, str)
+            else round(edt / 1e9, 2),
+            "equivalent_decompression_unit": "GB/s of fp16 original bytes (reference bench.py"
+                                             ":165-177), or 'fused-faster'",
+            "note": "multistage = kvc_dequantize (decode + f64 dequant to f32 [ctx,H,D] in HBM) "
+                    "then dense torch GEMVs; matvec = the dense passes alone on the "
+                    "materialised f32 tensors"}
+
+
+def _ncu_duration_ms(config):
+    """The fused kernel's duration in the committed ncu --set full capture
+    (cold cache, serialised) -- a cross-check of roofline.launch_ms."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"fused_ncu_cfg{config}.json")) as fh:
+            d = json.load(fh)
+        num, unit = d["Duration"].split()[:2]
+        return round(float(num) * {"us": 1e-3, "ms": 1.0, "ns": 1e-6}[unit], 4)
+    except Exception:
+        return None
 
 
 def _ncu_binding(config):

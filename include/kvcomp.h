@@ -50,7 +50,7 @@ typedef enum {
 /* Quantisation modes (quantizer.py:37-42). */
 enum { KVC_K_BLOCK = 0, KVC_V_TOKEN = 1, KVC_K_CHANNEL = 2 };
 /* Input dtypes of the dense K/V tensors (tensor_io.py:30-51). */
-enum { KVC_F16 = 0, KVC_F32 = 1 };
+enum { KVC_F16 = 0, KVC_F32 = 1, KVC_F64 = 2 /* kvc_quantize only */ };
 
 /* Device-resident per-arena counters (codec.py:279-326 running totals). */
 typedef struct {
@@ -259,6 +259,44 @@ size_t kvc_attention_workspace_bytes(int n_seqs, int H, int group, int D, int ma
  * [ctx, H, D] (compressed region only; buffered rows untouched). */
 int kvc_dequantize(const kvc_seq_desc *seq_dev, int H, int D, int bs, int which /*0=K,1=V*/,
                    int n_chunks, float *out_dev, int *err_dev, void *stream);
+
+/* ---------------------------------------------------------------- */
+/* Per-block codec surface — replaces codec.py:59-472 single-block API */
+/* ---------------------------------------------------------------- */
+
+/* decompress_block (codec.py:356-391) for n arena ordinals: codes_dev
+ * [n, bs, D] u8, metas_dev [n, n_units, 2] f32 (min, scale), block_index_dev
+ * [n] u32 from each header.  Corrupt extents / slices -> *err_dev CodecError.
+ * (compress_block / encode_slice: kvc_encode_append on a one-block arena.) */
+int kvc_decode_blocks(const uint8_t *arena_dev, const uint32_t *offsets_dev,
+                      const kvc_arena_counters *counters_dev, const int32_t *ordinals_dev, int n,
+                      int bs, int n_units, int D, const kvc_codebook_dev *cb_dev,
+                      uint8_t *codes_dev, float *metas_dev, uint32_t *block_index_dev,
+                      int *err_dev, void *stream);
+
+/* decode_slice / decode_slices (codec.py:141-226): the array-form tree walk,
+ * one thread per slice, over an unpacked 0/1 bit array (packed = 0) or packed
+ * MSB-first bytes (packed = 1) of n_bits bits.  out_dev [n_slices, out_len];
+ * *bad_dev (initialise to n_slices) receives the lowest corrupt slice index. */
+int kvc_decode_slices_tree(const uint8_t *bits_dev, int packed, uint64_t n_bits,
+                           const int64_t *offsets_dev, const int64_t *counts_dev, int n_slices,
+                           const int32_t *children_dev, const int32_t *is_symbol_dev,
+                           const uint8_t *symbols_dev, int n_nodes, int out_len,
+                           uint8_t *out_dev, int *bad_dev, void *stream);
+
+/* CompressedArena.append (codec.py:308-326): one serialised block image
+ * (nbytes, a multiple of 4) appended at the device cursor; capacity or
+ * 32-bit overflow sets counters->err = KVC_ERR_ARENA_FULL and writes nothing. */
+int kvc_arena_append(const uint8_t *image_dev, uint32_t nbytes, uint64_t payload_bits,
+                     uint64_t payload_bytes, uint8_t *arena_dev, uint64_t capacity,
+                     uint32_t *offsets_dev, kvc_arena_counters *counters_dev, void *stream);
+
+/* CompressedArena.restore (codec.py:329-341): counters of an arena holding
+ * `size` serialised bytes and n_blocks offsets, every extent validated as
+ * _parse_block (codec.py:247-268); *n_slices_dev = total slices. */
+int kvc_arena_restore(const uint8_t *arena_dev, uint64_t size, const uint32_t *offsets_dev,
+                      int n_blocks, int n_units, kvc_arena_counters *counters_dev,
+                      uint64_t *n_slices_dev, int *err_dev, void *stream);
 
 /* Uncompressed fp16 decode-attention comparator (the north-star baseline):
  * K/V [n_seqs, H, ctx, D] f16 head-major, q [n_seqs, H*group, D] f32. */

@@ -10,19 +10,21 @@ from .attention import (AttentionOutput, attention_batched, attention_gqa, atten
                         dense_attention_f16,
                         fused_k_scores, fused_v_output, multistage_attention, reference_output,
                         reference_scores, softmax_rows)
-from .codebook import (HuffmanCodebook, build_codebook, build_histogram, build_smoothed_codebook,
-                       codebook_from_lengths, deserialize_codebook, histogram_entropy,
-                       serialize_codebook, smooth_histogram)
-from .codec import DataMovement, DeviceArena, reserve_arena_pool
+from .codebook import (DecodeTree, HuffmanCodebook, build_codebook, build_histogram,
+                       build_smoothed_codebook, codebook_from_lengths, deserialize_codebook,
+                       histogram_entropy, serialize_codebook, smooth_histogram)
+from .codec import (CompressedArena, CompressedBlock, DataMovement, DeviceArena, compress_block, decode_slice,
+                    decode_slices, decompress_block, encode_slice, metadata_overhead,
+                    reserve_arena_pool, scan_offsets, units_per_block)
 from .container import load_state, read_header, save_state
 from .errors import (ArenaFullError, CodebookError, CodecError, ConfigError,
                      ContainerFormatError, KvpackError, TensorFormatError)
 from .kvcache import LayerCacheState
-from .metrics import (CompressionStats, collect_stats, equivalent_decompression_throughput,
-                      median_time)
+from .metrics import (BenchRow, CompressionStats, SimulationResult, SimulationSettings,
+                      collect_stats, config_label, equivalent_decompression_throughput,
+                      median_time, run_ratio_sweep, run_simulation, write_csv)
 from .quantizer import (DEFAULT_REL_SCALE, MIN_REL_SCALE, QuantConfig, QuantizedBlock, QuantMode,
-                        QuantUnitMeta, dequantize_block, quantize_block)
+                        QuantUnitMeta, dequantize_block, quantize_block, quantize_unit)
 from .tensor_io import CacheTensor, SyntheticSpec, generate_synthetic, generate_synthetic_device
 
-CompressedArena = DeviceArena
 __version__ = "0.1.0"

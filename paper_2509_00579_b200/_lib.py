@@ -21,7 +21,7 @@ CSRC = os.path.join(_HERE, "csrc")
 KVC_OK, KVC_ERR_CONFIG, KVC_ERR_TENSOR, KVC_ERR_CODEBOOK, KVC_ERR_CODEC, KVC_ERR_ARENA_FULL, \
     KVC_ERR_CUDA = range(7)
 KVC_K_BLOCK, KVC_V_TOKEN, KVC_K_CHANNEL = 0, 1, 2
-KVC_F16, KVC_F32 = 0, 1
+KVC_F16, KVC_F32, KVC_F64 = 0, 1, 2
 LUT_BITS = 12
 
 
@@ -105,6 +105,10 @@ SIGNATURES = {
     "kvc_dequantize": (I, [P, I, I, I, I, I, P, P, P]),
     "kvc_dense_attention_f16": (I, [P, P, I, I, I, I, L, P, P, P, SZ, P]),
     "kvc_dense_workspace_bytes": (SZ, [I, I, I, I, L]),
+    "kvc_decode_blocks": (I, [P, P, P, P, I, I, I, I, P, P, P, P, P, P]),
+    "kvc_decode_slices_tree": (I, [P, I, U64, P, P, I, P, P, P, I, I, P, P, P]),
+    "kvc_arena_append": (I, [P, U32, U64, U64, P, U64, P, P, P]),
+    "kvc_arena_restore": (I, [P, U64, P, I, I, P, P, P, P]),
 }
 
 _lib = None

@@ -58,6 +58,62 @@ def histogram_entropy(h) -> float:
     return float(-(p * np.log2(p)).sum())
 
 
+@dataclass(frozen=True, eq=False)
+class DecodeTree:
+    """Array-form Huffman tree (codebook.py:35-53): node 0 is the root,
+    ``children[n] = [child on 0, child on 1]``, leaves carry ``symbols[n]``
+    with ``is_symbol[n] == 1``.  Host arrays as in the reference; the device
+    copies (``device(dev)``) feed kvc_decode_slices_tree."""
+
+    children: np.ndarray   # (n_nodes, 2) int32
+    is_symbol: np.ndarray  # (n_nodes,) int32
+    symbols: np.ndarray    # (n_nodes,) uint8
+    _dev: Dict[str, tuple] = field(default_factory=dict, repr=False, compare=False)
+
+    @property
+    def n_nodes(self) -> int:
+        return int(self.children.shape[0])
+
+    def device(self, dev):
+        key = str(torch.device(dev))
+        t = self._dev.get(key)
+        if t is None:
+            t = tuple(torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+                      for a in (self.children.astype(np.int32).reshape(-1),
+                                self.is_symbol.astype(np.int32), self.symbols.astype(np.uint8)))
+            self._dev[key] = t
+        return t
+
+
+def decode_tree_from_words(lengths: np.ndarray, words: np.ndarray) -> DecodeTree:
+    """The reference's node numbering (codebook.py:144-176): symbols are
+    inserted in increasing symbol order, each walking its codeword MSB-first
+    and appending a fresh node wherever a child is missing; a one-symbol
+    alphabet gets a root whose two branches both reach the single leaf."""
+    present = np.flatnonzero(np.asarray(lengths) > 0)
+    n_max = 1 + int(np.asarray(lengths, np.int64)[present].sum()) + 1
+    children = np.zeros((n_max, 2), np.int32)
+    is_symbol = np.zeros(n_max, np.int32)
+    symbols = np.zeros(n_max, np.uint8)
+    n = 1
+    if present.size == 1:
+        children[0] = (1, 1)
+        is_symbol[1], symbols[1] = 1, present[0]
+        n = 2
+    else:
+        for sym in present:
+            ln, w, node = int(lengths[sym]), int(words[sym]), 0
+            for sh in range(ln - 1, -1, -1):
+                b = (w >> sh) & 1
+                if children[node, b] == 0:
+                    children[node, b] = n
+                    n += 1
+                node = int(children[node, b])
+            is_symbol[node], symbols[node] = 1, sym
+    return DecodeTree(children=children[:n].copy(), is_symbol=is_symbol[:n].copy(),
+                      symbols=symbols[:n].copy())
+
+
 @dataclass(eq=False)
 class HuffmanCodebook:
     """Canonical code + device decode tables; same fields as the reference."""
@@ -67,6 +123,15 @@ class HuffmanCodebook:
     max_code_length: int
     tables: _lib.CodebookTables = field(repr=False)
     _device: Dict[str, torch.Tensor] = field(default_factory=dict, repr=False)
+
+    @property
+    def decode_tree(self) -> DecodeTree:
+        """codebook.py:144-176 (built on first use; the device decoders use
+        the LUT tables instead)."""
+        t = self._device.get("tree")
+        if t is None:
+            t = self._device["tree"] = decode_tree_from_words(self.code_lengths, self.code_words)
+        return t
 
     @property
     def encode_table(self):

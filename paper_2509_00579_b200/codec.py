@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import weakref
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Optional, Tuple
 
 import numpy as np
@@ -417,3 +417,329 @@ class DeviceArena:
 
 def full_error(what="arena"):
     return ArenaFullError(f"{what}: capacity exhausted")
+
+
+# ---------------------------------------------------------------------------
+# Per-block codec surface (reference codec.py:59-226, :308-341, :351-472).
+# The Store/Fetch hot path never builds these objects; they are the
+# reference's single-block API, backed by the same device kernels
+# (kvc_encode_append for encoding, kvc_decode_blocks / kvc_decode_slices_tree
+# for decoding, kvc_arena_append / kvc_arena_restore for the arena).
+# ---------------------------------------------------------------------------
+
+MAX_SLICE_BITS = 0xFFFF
+
+
+def _dev(device=None) -> torch.device:
+    return torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+
+
+def _stream(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _to_dev(x, dtype, dev) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(dev, dtype).contiguous()
+    if isinstance(x, (bytes, bytearray, memoryview)):
+        x = np.frombuffer(bytes(x), dtype=np.uint8)
+    return torch.as_tensor(np.ascontiguousarray(x)).to(dev, dtype).contiguous()
+
+
+@dataclass(frozen=True)
+class CompressedBlock:
+    """One entropy-coded block (codec.py:59-74): per-slice bit counts, unit
+    metadata and the byte-padded payload, as device tensors.  Blocks made by
+    ``compress_block`` also carry their serialised image, so
+    ``DeviceArena.append`` is a device copy."""
+
+    block_index: int
+    slice_bit_counts: torch.Tensor  # (n_slices,) int32 (u16 values)
+    unit_mins: torch.Tensor         # (n_units,) float32
+    unit_scales: torch.Tensor       # (n_units,) float32
+    payload: torch.Tensor           # (ceil(bits/8),) uint8
+    _total_bits: Optional[int] = field(default=None, compare=False, repr=False)
+    _image: Optional[torch.Tensor] = field(default=None, compare=False, repr=False)
+
+    @property
+    def n_slices(self) -> int:
+        return int(self.slice_bit_counts.shape[0])
+
+    @property
+    def total_bits(self) -> int:
+        if self._total_bits is not None:
+            return self._total_bits
+        return int(self.slice_bit_counts.to(torch.int64).sum())
+
+
+def _encode_one_block(codes: torch.Tensor, metas: torch.Tensor, block_index: int, cb):
+    """kvc_encode_append on a private one-block arena: returns (image, bits).
+    Missing codes / 16-bit slice overflow raise CodecError (codec.py:85-102)."""
+    dev = codes.device
+    bs, D = codes.shape
+    n_units = metas.shape[0]
+    lib = _lib.lib()
+    arena = DeviceArena(dev, None, initial_bytes=worst_block_bytes(bs, n_units, D,
+                                                                   cb.max_code_length),
+                        initial_blocks=1)
+    ws = torch.empty(lib.kvc_encode_workspace_bytes(1, bs), dtype=torch.uint8, device=dev)
+    st = lib.kvc_encode_append(codes.data_ptr(), metas.data_ptr(), 1, 1, 1, 0, int(block_index),
+                               bs, D, n_units, cb.max_code_length,
+                               cb.device_tables(dev).data_ptr(), arena.buf_ptr,
+                               arena.alloc_capacity, arena.offsets_ptr, arena.counters_ptr,
+                               ws.data_ptr(), _stream(dev))
+    _lib.check(st, "compress_block")
+    c = arena.counters()
+    if c.err:
+        _lib.raise_device_error(c.err, "compress_block")
+    return arena.raw_tensor()[: int(c.cursor)].clone(), int(c.payload_bits)
+
+
+def _check_codes(codes: torch.Tensor, cb) -> torch.Tensor:
+    """codec.py:77-91: every code must be present in the codebook; returns
+    the per-code lengths (device)."""
+    lens = torch.as_tensor(cb.code_lengths.astype(np.int64)).to(codes.device)[codes.long()]
+    absent = lens == 0
+    if bool(absent.any()):
+        missing = int(codes[absent].reshape(-1)[0])
+        raise CodecError(f"code {missing} is absent from the codebook")
+    return lens
+
+
+def encode_slice(codes, cb) -> Tuple[torch.Tensor, int]:
+    """codec.py:94-103: one slice -> (its codeword bits as a 0/1 uint8 device
+    tensor, bit count)."""
+    dev = codes.device if isinstance(codes, torch.Tensor) and codes.is_cuda else _dev()
+    arr = _to_dev(codes, torch.uint8, dev).reshape(-1)
+    if arr.numel() == 0:
+        raise CodecError("cannot encode an empty slice")
+    total = int(_check_codes(arr, cb).sum())
+    if total > MAX_SLICE_BITS:
+        raise CodecError(f"slice bit count {total} overflows 16 bits")
+    image, bits = _encode_one_block(arr.reshape(1, -1),
+                                    torch.zeros((1, 2), dtype=torch.float32, device=dev), 0, cb)
+    hdr = 6 + 2 + 8
+    payload = image[hdr: hdr + (bits + 7) // 8]
+    shifts = torch.arange(7, -1, -1, device=dev, dtype=torch.uint8)
+    out = ((payload[:, None] >> shifts) & 1).reshape(-1)[:bits]
+    return out.contiguous(), bits
+
+
+def scan_offsets(bit_counts) -> Tuple[torch.Tensor, int]:
+    """codec.py:106-116: exclusive bit offsets from the inclusive scan, and
+    the total (CodecError past 32 bits)."""
+    c = bit_counts if isinstance(bit_counts, torch.Tensor) else torch.as_tensor(
+        np.asarray(bit_counts, dtype=np.int64))
+    c = c.to(torch.int64)
+    if c.is_cpu:
+        c = c.to(_dev())
+    if c.numel() == 0:
+        raise CodecError("scan over an empty bit-count array")
+    inclusive = torch.cumsum(c.reshape(-1), 0)
+    total = int(inclusive[-1])
+    if total > 0xFFFFFFFF:
+        raise CodecError("total bit count overflows 32 bits")
+    return inclusive - c.reshape(-1), total
+
+
+def compress_block(q, cb) -> CompressedBlock:
+    """codec.py:119-138 on the device (the Store's block encoder)."""
+    codes = q.codes
+    dev = codes.device if isinstance(codes, torch.Tensor) and codes.is_cuda else _dev()
+    codes = _to_dev(codes, torch.uint8, dev)
+    if codes.ndim != 2:
+        raise CodecError("block codes must be a (n_slices, head_dim) matrix")
+    _check_codes(codes, cb)
+    mins = _to_dev(q.unit_mins, torch.float32, dev).reshape(-1)
+    scales = _to_dev(q.unit_scales, torch.float32, dev).reshape(-1)
+    metas = torch.stack([mins, scales], dim=1).contiguous()
+    image, bits = _encode_one_block(codes, metas, q.block_index, cb)
+    bs = codes.shape[0]
+    counts = image[6: 6 + 2 * bs].view(torch.int16).to(torch.int32) & 0xFFFF
+    p0 = 6 + 2 * bs + 8 * metas.shape[0]
+    return CompressedBlock(block_index=int(q.block_index), slice_bit_counts=counts,
+                           unit_mins=mins, unit_scales=scales,
+                           payload=image[p0: p0 + (bits + 7) // 8].clone(), _total_bits=bits,
+                           _image=image)
+
+
+def _tree_decode(bits: torch.Tensor, packed: bool, n_bits: int, offs: torch.Tensor,
+                 counts: torch.Tensor, tree, out_len: int) -> torch.Tensor:
+    dev = bits.device
+    n = offs.numel()
+    children, is_symbol, symbols = tree.device(dev)
+    out = torch.zeros((n, out_len), dtype=torch.uint8, device=dev)
+    bad = torch.full((1,), n, dtype=torch.int32, device=dev)
+    st = _lib.lib().kvc_decode_slices_tree(bits.data_ptr(), int(packed), int(n_bits),
+                                           offs.data_ptr(), counts.data_ptr(), n,
+                                           children.data_ptr(), is_symbol.data_ptr(),
+                                           symbols.data_ptr(), tree.n_nodes, out_len,
+                                           out.data_ptr(), bad.data_ptr(), _stream(dev))
+    _lib.check(st, "decode_slices")
+    b = int(bad.item())
+    if b < n:
+        raise CodecError(f"corrupt slice {b}: the stream does not decode to {out_len} symbols "
+                         f"in {int(counts[b])} bits")
+    return out
+
+
+def decode_slice(payload, bit_offset: int, bit_count: int, tree, out_len: int) -> torch.Tensor:
+    """codec.py:141-173: one slice of a packed MSB-first payload, decoded
+    with the array-form tree on the device."""
+    dev = payload.device if isinstance(payload, torch.Tensor) and payload.is_cuda else _dev()
+    data = _to_dev(payload, torch.uint8, dev).reshape(-1)
+    if bit_offset < 0 or bit_offset + bit_count > data.numel() * 8:
+        raise CodecError("bit range outside payload")
+    offs = torch.tensor([bit_offset], dtype=torch.int64, device=dev)
+    cnt = torch.tensor([bit_count], dtype=torch.int64, device=dev)
+    return _tree_decode(data, True, data.numel() * 8, offs, cnt, tree, out_len)[0]
+
+
+def decode_slices(bits, bit_offsets, bit_counts, tree, out_len: int) -> torch.Tensor:
+    """codec.py:176-226: many slices of an unpacked 0/1 bit array, one device
+    thread per slice (the reference's lockstep loop)."""
+    dev = bits.device if isinstance(bits, torch.Tensor) and bits.is_cuda else _dev()
+    b = _to_dev(bits, torch.uint8, dev).reshape(-1)
+    offs = _to_dev(bit_offsets, torch.int64, dev).reshape(-1)
+    counts = _to_dev(bit_counts, torch.int64, dev).reshape(-1)
+    if offs.numel() == 0:
+        return torch.zeros((0, out_len), dtype=torch.uint8, device=dev)
+    if bool((offs < 0).any()) or bool((offs + counts > b.numel()).any()):
+        raise CodecError("bit range outside payload")
+    return _tree_decode(b, False, b.numel(), offs, counts, tree, out_len)
+
+
+def units_per_block(mode, head_dim: int, block_size: int) -> int:
+    """codec.py:344-346: one metadata unit per channel (K) or token (V)."""
+    from .quantizer import QuantMode
+    return block_size if mode is QuantMode.V_TOKEN else head_dim
+
+
+def decompress_block(arena: "DeviceArena", ordinal: int, cb, *, mode, head_num: int,
+                     head_dim: int, block_size: int):
+    """codec.py:351-391: the exact inverse of compress_block + append, on the
+    device (kvc_decode_blocks)."""
+    from .quantizer import QuantizedBlock
+    if not 0 <= ordinal < arena.n_blocks:
+        raise CodecError(f"block ordinal {ordinal} out of range")
+    dev = arena.device
+    n_units = units_per_block(mode, head_dim, block_size)
+    codes = torch.empty((1, block_size, head_dim), dtype=torch.uint8, device=dev)
+    metas = torch.empty((1, n_units, 2), dtype=torch.float32, device=dev)
+    bidx = torch.zeros(1, dtype=torch.int64, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    ords = torch.tensor([ordinal], dtype=torch.int32, device=dev)
+    st = _lib.lib().kvc_decode_blocks(arena.buf_ptr, arena.offsets_ptr, arena.counters_ptr,
+                                      ords.data_ptr(), 1, block_size, n_units, head_dim,
+                                      cb.device_tables(dev).data_ptr(), codes.data_ptr(),
+                                      metas.data_ptr(), bidx.data_ptr(), err.data_ptr(),
+                                      _stream(dev))
+    _lib.check(st, "decompress_block")
+    _lib.raise_device_error(int(err.item()), "decompress_block")
+    block_index = int(bidx.item()) & 0xFFFFFFFF
+    return QuantizedBlock(codes=codes[0], unit_mins=metas[0, :, 0].clone(),
+                          unit_scales=metas[0, :, 1].clone(), block_index=block_index,
+                          head_index=block_index % head_num,
+                          ctx_start=(block_index // head_num) * block_size)
+
+
+def metadata_overhead(cblocks, head_dim: int) -> Tuple[float, float]:
+    """codec.py:455-472: 16-bit slice counters as fractions of the payload and
+    of the original 16-bit values."""
+    if not cblocks:
+        raise CodecError("metadata_overhead needs at least one block")
+    n_slices = sum(b.n_slices for b in cblocks)
+    payload_bits = sum(b.total_bits for b in cblocks)
+    if payload_bits == 0:
+        raise CodecError("empty payloads have no meaningful overhead ratio")
+    counter_bits = 16 * n_slices
+    return counter_bits / payload_bits, counter_bits / (n_slices * head_dim * 16)
+
+
+def _block_image(cb: CompressedBlock) -> torch.Tensor:
+    """_serialize_block (codec.py:229-244) of a block built from its fields."""
+    if cb._image is not None:
+        return cb._image
+    dev = cb.payload.device if cb.payload.is_cuda else _dev()
+    hdr = np.zeros(6, np.uint8)
+    hdr[:4] = np.frombuffer(np.uint32(cb.block_index).tobytes(), np.uint8)
+    hdr[4:6] = np.frombuffer(np.uint16(cb.n_slices).tobytes(), np.uint8)
+    counts = _to_dev(cb.slice_bit_counts, torch.int32, dev).to(torch.int16).view(torch.uint8)
+    metas = torch.stack([_to_dev(cb.unit_mins, torch.float32, dev).reshape(-1),
+                         _to_dev(cb.unit_scales, torch.float32, dev).reshape(-1)], 1)
+    parts = [torch.from_numpy(hdr).to(dev), counts, metas.contiguous().view(torch.uint8),
+             _to_dev(cb.payload, torch.uint8, dev).reshape(-1)]
+    raw = sum(p.numel() for p in parts)
+    parts.append(torch.zeros((-raw) % 4, dtype=torch.uint8, device=dev))
+    return torch.cat(parts)
+
+
+def _arena_append(self: "DeviceArena", cblock: CompressedBlock) -> int:
+    """CompressedArena.append (codec.py:308-326): serialise and append one
+    block on the device; returns its arrival ordinal.  A full arena raises
+    ArenaFullError and is left unchanged."""
+    image = _block_image(cblock).to(self.device)
+    n = image.numel()
+    bits = cblock.total_bits
+    self.reserve(1, n)
+    st = _lib.lib().kvc_arena_append(image.data_ptr(), n, bits, (bits + 7) // 8, self.buf_ptr,
+                                     self.alloc_capacity, self.offsets_ptr, self.counters_ptr,
+                                     _stream(self.device))
+    _lib.check(st, "CompressedArena.append")
+    if self.capacity is not None or self._bound + n > 0xFFFFFFFF:
+        c = self.counters()
+        if c.err == _lib.KVC_ERR_ARENA_FULL:
+            self._counters[36:40].zero_()  # the refused append changed nothing
+            raise ArenaFullError(f"arena capacity {self.capacity} exhausted at offset "
+                                 f"{int(c.cursor)}")
+    ordinal = self.n_blocks
+    self.note_append(1, n)
+    return ordinal
+
+
+def _arena_restore(cls, data, offsets, n_units: int, device=None) -> "DeviceArena":
+    """CompressedArena.restore (codec.py:329-341): serialised bytes + offsets
+    -> a device arena whose counters are recomputed (and every extent
+    validated) on the device."""
+    dev = _dev(device)
+    raw = bytes(data) if not isinstance(data, torch.Tensor) else data.cpu().numpy().tobytes()
+    offs = np.asarray([int(o) for o in offsets], dtype=np.uint32)
+    arena = cls(device=dev, capacity=None, initial_bytes=max(len(raw), 1),
+                initial_blocks=max(len(offs), 1))
+    arena.load(raw, offs, bytes(ctypes.sizeof(_lib.ArenaCounters)))
+    nsl = torch.zeros(1, dtype=torch.int64, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = _lib.lib().kvc_arena_restore(arena.buf_ptr, len(raw), arena.offsets_ptr, len(offs),
+                                      int(n_units), arena.counters_ptr, nsl.data_ptr(),
+                                      err.data_ptr(), _stream(dev))
+    _lib.check(st, "CompressedArena.restore")
+    _lib.raise_device_error(int(err.item()), "CompressedArena.restore")
+    arena.counters()
+    return arena
+
+
+def _arena_n_slices(self: "DeviceArena") -> int:
+    """Running total of slices (codec.py:290): the n_slices header fields."""
+    if self.n_blocks == 0:
+        return 0
+    at = self._offsets[: self.n_blocks].to(torch.int64) & 0xFFFFFFFF
+    lo = self._buf[at + 4].to(torch.int64)
+    hi = self._buf[at + 5].to(torch.int64)
+    return int((lo | (hi << 8)).sum())
+
+
+DeviceArena.append = _arena_append
+DeviceArena.restore = classmethod(_arena_restore)
+DeviceArena.n_slices = property(_arena_n_slices)
+
+
+class CompressedArena(DeviceArena):
+    """The reference's constructor signature (codec.py:279-284:
+    ``CompressedArena(capacity=None)``) for a device arena on the current
+    (or given) CUDA device."""
+
+    def __init__(self, capacity: Optional[int] = None, device=None, initial_bytes: int = 1 << 16,
+                 initial_blocks: int = 256):
+        super().__init__(_dev(device), capacity, initial_bytes=initial_bytes,
+                         initial_blocks=initial_blocks)

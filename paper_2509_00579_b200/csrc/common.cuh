@@ -24,6 +24,10 @@ __host__ __device__ __forceinline__ int kvc_header_bytes(int bs, int n_units) {
 
 __device__ __forceinline__ float kvc_load(const __half *p) { return __half2float(*p); }
 __device__ __forceinline__ float kvc_load(const float *p) { return *p; }
+// exact widening loads (the quantiser's f64 arithmetic; f16/f32 -> f64 is exact)
+__device__ __forceinline__ double kvc_load_d(const __half *p) { return (double)__half2float(*p); }
+__device__ __forceinline__ double kvc_load_d(const float *p) { return (double)*p; }
+__device__ __forceinline__ double kvc_load_d(const double *p) { return *p; }
 
 __device__ __forceinline__ void kvc_set_err(int *err, int code) {
     if (err) atomicCAS(err, 0, code);

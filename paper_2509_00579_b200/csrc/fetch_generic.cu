@@ -299,6 +299,48 @@ dequant_kernel(const kvc_seq_desc *__restrict__ seq, int H, int D, int bs, int w
     }
 }
 
+// decompress_block (codec.py:356-391) for a list of arena ordinals: parse and
+// validate each extent, decode its slices with the codebook LUT (canonical
+// tail for long codes) into codes [bs, D] u8, copy the (min, scale) pairs and
+// the header's block_index.  One CTA per block.
+__global__ void __launch_bounds__(kThreads)
+decode_blocks_kernel(const uint8_t *__restrict__ arena, const uint32_t *__restrict__ offsets,
+                     const kvc_arena_counters *__restrict__ counters,
+                     const int32_t *__restrict__ ordinals, int bs, int n_units, int D,
+                     const kvc_codebook_dev *__restrict__ cb, uint8_t *__restrict__ codes,
+                     float *__restrict__ metas, uint32_t *__restrict__ block_index, int *err) {
+    __shared__ uint32_t sh_off[1024], sh_cnt[1024], sh_tot;
+    const long i = blockIdx.x;
+    const long nb = (long)counters->n_blocks;
+    const long ord = ordinals[i];
+    if (ord < 0 || ord >= nb) {
+        if (threadIdx.x == 0) kvc_set_err(err, KVC_ERR_CODEC);
+        return;
+    }
+    uint64_t start, end;
+    kvc_extent(offsets, counters, ord, nb, start, end);
+    int ok = parse_block(arena, start, end, bs, n_units, sh_off, sh_cnt, &sh_tot);
+    ok = __syncthreads_and(ok);
+    if (!ok) {
+        if (threadIdx.x == 0) kvc_set_err(err, KVC_ERR_CODEC);
+        return;
+    }
+    const uint8_t *blk = arena + start;
+    if (threadIdx.x == 0)
+        block_index[i] = blk[0] | (blk[1] << 8) | (blk[2] << 16) | ((uint32_t)blk[3] << 24);
+    const uint8_t *meta = blk + 6 + 2 * bs;
+    for (int u = threadIdx.x; u < 2 * n_units; u += blockDim.x)
+        metas[i * 2 * n_units + u] = ld_f32(meta + 4 * u);
+    const uint8_t *payload = meta + 8 * n_units;
+    uint8_t *out = codes + i * (long)bs * D;
+    for (int r = threadIdx.x; r < bs; r += blockDim.x) {
+        uint8_t *row = out + (long)r * D;
+        bool good = decode_slice(cb, payload, arena + end, sh_off[r], sh_cnt[r], D,
+                                 [&](int c, int sym) { row[c] = (uint8_t)sym; });
+        if (!good) kvc_set_err(err, KVC_ERR_CODEC);
+    }
+}
+
 int max_chunks_of(const kvc_seq_desc *seqs_host, int n) { return 0; }
 
 }  // namespace
@@ -354,4 +396,19 @@ extern "C" int kvc_dequantize(const kvc_seq_desc *seq_dev, int H, int D, int bs,
     dequant_kernel<<<n_chunks * H, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         seq_dev, H, D, bs, which, out_dev, err_dev);
     return kvc_check_launch("dequant_kernel");
+}
+
+extern "C" int kvc_decode_blocks(const uint8_t *arena_dev, const uint32_t *offsets_dev,
+                                 const kvc_arena_counters *counters_dev,
+                                 const int32_t *ordinals_dev, int n, int bs, int n_units, int D,
+                                 const kvc_codebook_dev *cb_dev, uint8_t *codes_dev,
+                                 float *metas_dev, uint32_t *block_index_dev, int *err_dev,
+                                 void *stream) {
+    if (n < 0 || bs < 1 || D < 1 || n_units < 1) return kvc_fail(KVC_ERR_CONFIG, "bad shape");
+    if (bs > 1024) return kvc_fail(KVC_ERR_CONFIG, "block_size > 1024 unsupported");
+    if (n == 0) return KVC_OK;
+    decode_blocks_kernel<<<n, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        arena_dev, offsets_dev, counters_dev, ordinals_dev, bs, n_units, D, cb_dev, codes_dev,
+        metas_dev, block_index_dev, err_dev);
+    return kvc_check_launch("decode_blocks_kernel");
 }

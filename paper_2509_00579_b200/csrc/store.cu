@@ -27,9 +27,9 @@ constexpr int kEncThreads = 256;
 // half-integer (the only decision boundaries of round-half-up) recompute with
 // the correctly rounded division.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint8_t quant_code(float x, float vmin, double s64, double r64) {
+__device__ __forceinline__ uint8_t quant_code(double x, float vmin, double s64, double r64) {
     if (!(s64 > 0.0)) return 0;
-    double d = __dsub_rn((double)x, (double)vmin);
+    double d = __dsub_rn(x, (double)vmin);
     double t = __dmul_rn(d, r64);
     double f = floor(t);
     double frac = __dsub_rn(t, f);
@@ -55,7 +55,7 @@ __device__ __forceinline__ void hist_add(uint32_t *sh_hist, uint32_t code, bool 
 
 // K_CHANNEL (quantizer.py:191-197): whole-context ranges, codes clipped to
 // [0, clamp_max] (values outside the ranges appear after they were fixed).
-__device__ __forceinline__ uint8_t quant_code_clip(float x, float vmin, double s64, double r64,
+__device__ __forceinline__ uint8_t quant_code_clip(double x, float vmin, double s64, double r64,
                                                    int clamp_max) {
     if (!(s64 > 0.0)) return 0;
     double d = __dsub_rn((double)x, (double)vmin);
@@ -96,7 +96,7 @@ quantize_kernel(const T *__restrict__ x, long row_stride, int H, int D, int bs, 
             const T *row = blk + (long)r * row_stride;
             float lo = 3.4e38f, hi = -3.4e38f;
             for (int c = lane; c < D; c += 32) {
-                float v = kvc_load(row + c);
+                float v = (float)kvc_load_d(row + c);
                 lo = fminf(lo, v);
                 hi = fmaxf(hi, v);
             }
@@ -108,7 +108,7 @@ quantize_kernel(const T *__restrict__ x, long row_stride, int H, int D, int bs, 
             for (int c0 = 0; c0 < D; c0 += 32) {
                 int c = c0 + lane;
                 bool ok = c < D;
-                uint8_t code = ok ? quant_code(kvc_load(row + c), lo, s64, r64) : 0;
+                uint8_t code = ok ? quant_code(kvc_load_d(row + c), lo, s64, r64) : 0;
                 if (ok) out[(long)r * D + c] = code;
                 if (do_hist) hist_add(sh_hist, code, ok);
             }
@@ -129,7 +129,7 @@ quantize_kernel(const T *__restrict__ x, long row_stride, int H, int D, int bs, 
                 hi = ranges[(long)(H + head) * D + c];
             } else if (ok) {
                 for (int r = 0; r < bs; ++r) {
-                    float v = kvc_load(blk + (long)r * row_stride + c);
+                    float v = (float)kvc_load_d(blk + (long)r * row_stride + c);
                     lo = fminf(lo, v);
                     hi = fmaxf(hi, v);
                 }
@@ -138,7 +138,7 @@ quantize_kernel(const T *__restrict__ x, long row_stride, int H, int D, int bs, 
             double s64 = (double)scale;
             double r64 = s64 > 0.0 ? __drcp_rn(s64) : 0.0;
             for (int r = 0; r < bs; ++r) {
-                const float xv = ok ? kvc_load(blk + (long)r * row_stride + c) : 0.f;
+                const double xv = ok ? kvc_load_d(blk + (long)r * row_stride + c) : 0.0;
                 uint8_t code = !ok ? 0
                                : ranges ? quant_code_clip(xv, lo, s64, r64, clamp_max)
                                         : quant_code(xv, lo, s64, r64);
@@ -397,6 +397,10 @@ extern "C" int kvc_quantize(const void *x_dev, int x_dtype, long row_stride, int
     else if (x_dtype == KVC_F32)
         quantize_kernel<float><<<(unsigned)nb, kQuantThreads, 0, s>>>(
             static_cast<const float *>(x_dev), row_stride, H, D, bs, mode, rel, k_ranges_dev,
+            clamp_max, codes_dev, metas_dev, hist);
+    else if (x_dtype == KVC_F64)  // quantize_unit on float64 values (quantizer.py:144-160)
+        quantize_kernel<double><<<(unsigned)nb, kQuantThreads, 0, s>>>(
+            static_cast<const double *>(x_dev), row_stride, H, D, bs, mode, rel, k_ranges_dev,
             clamp_max, codes_dev, metas_dev, hist);
     else
         return kvc_fail(KVC_ERR_TENSOR, "unsupported dtype");

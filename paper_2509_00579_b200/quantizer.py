@@ -126,6 +126,38 @@ def quantize_tokens(x: torch.Tensor, n_chunks: int, head_num: int, head_dim: int
     return codes, metas
 
 
+def quantize_unit(values, rel_quant_scale: float, device=None):
+    """quantizer.py:144-160 on the device: one unit (a flat group of values
+    sharing min/scale), binary64 arithmetic on the float64 values ->
+    (codes uint8 device tensor, QuantUnitMeta(min, scale))."""
+    if isinstance(values, torch.Tensor):
+        v = values.detach().reshape(-1)
+        dev = torch.device(device) if device is not None else (
+            v.device if v.is_cuda else torch.device("cuda", torch.cuda.current_device()))
+        v = v.to(dev, torch.float64).contiguous()
+    else:
+        a = np.asarray(values, dtype=np.float64).reshape(-1)
+        dev = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        v = torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    if v.numel() == 0:
+        raise CodecError("cannot quantize an empty unit")
+    if not bool(torch.isfinite(v).all()):
+        raise CodecError("non-finite values in quantization unit")
+    if not MIN_REL_SCALE <= rel_quant_scale <= 1.0:
+        raise ConfigError(f"rel_quant_scale {rel_quant_scale} outside [1/255, 1]")
+    n = v.numel()
+    codes = torch.empty(n, dtype=torch.uint8, device=dev)
+    meta = torch.empty(2, dtype=torch.float32, device=dev)
+    # the unit as one V_TOKEN row: min/max over the row, one (min, scale)
+    st = _lib.lib().kvc_quantize(v.data_ptr(), _lib.KVC_F64, n, 1, 1, n, 1, _lib.KVC_V_TOKEN,
+                                 float(rel_quant_scale), None, codes.data_ptr(), meta.data_ptr(),
+                                 None, torch.cuda.current_stream(dev).cuda_stream)
+    _lib.check(st, "quantize_unit")
+    m = meta.cpu().numpy()
+    return codes, QuantUnitMeta(float(m[0]), float(m[1]))
+
+
 def quantize_block(block, mode: QuantMode, cfg: QuantConfig, head_index: int, ctx_start: int,
                    head_num: int, channel_ranges=None, device=None) -> QuantizedBlock:
     """quantizer.py:162-209 on the device."""

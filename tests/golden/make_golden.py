@@ -248,6 +248,118 @@ def kat_cases():
     print("kats: written")
 
 
+def blockapi_cases():
+    """The per-block codec surface (codec.py:59-472, quantizer.py:144-160,
+    codebook.py:35-66/:144-176, CompressedArena.append/.restore) run on the
+    reference, for the device-backed drop-ins (tests/test_gpu_blockapi.py)."""
+    from kvpack import codec as rcodec
+
+    out = {}
+    H, D, bs = 2, 128, 64
+    spec = kv.SyntheticSpec(bs * 3 + 9, H, D, seed=41)
+    k = kv.generate_synthetic(spec).values.astype(np.float16)
+    v = kv.generate_synthetic(replace(spec, seed=41 ^ 0x9E3779B9)).values.astype(np.float16)
+    cfg_k, cfg_v = kv.QuantConfig(kv.QuantMode.K_BLOCK), kv.QuantConfig(kv.QuantMode.V_TOKEN)
+    st = kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v), cfg_k, cfg_v)
+    out["k_in"], out["v_in"] = k, v
+    kf, vf = k.astype(np.float32), v.astype(np.float32)
+    # quantize_block + compress_block of block (chunk 1, head 1) for K and V
+    qk = kv.quantize_block(kf[bs:2 * bs, 1], kv.QuantMode.K_BLOCK, cfg_k, 1, bs, H)
+    qv = kv.quantize_block(vf[bs:2 * bs, 1], kv.QuantMode.V_TOKEN, cfg_v, 1, bs, H)
+    blocks = []
+    for nm, q, cb in (("k", qk, st.k_codebook), ("v", qv, st.v_codebook)):
+        c = kv.compress_block(q, cb)
+        blocks.append(c)
+        out[nm + "_codes"] = q.codes
+        out[nm + "_mins"], out[nm + "_scales"] = q.unit_mins, q.unit_scales
+        out[nm + "_block_index"] = np.int64(c.block_index)
+        out[nm + "_counts"] = c.slice_bit_counts.astype(np.uint16)
+        out[nm + "_payload"] = np.frombuffer(c.payload, np.uint8).copy()
+        out[nm + "_total_bits"] = np.int64(c.total_bits)
+        out[nm + "_image"] = np.frombuffer(rcodec._serialize_block(c), np.uint8).copy()
+        offs, tot = kv.scan_offsets(c.slice_bit_counts)
+        out[nm + "_scan"], out[nm + "_scan_total"] = offs.astype(np.uint32), np.int64(tot)
+        out[nm + "_dec_slice5"] = kv.decode_slice(c.payload, int(offs[5]),
+                                                  int(c.slice_bit_counts[5]), cb.decode_tree, D)
+        out[nm + "_dec_slices"] = kv.decode_slices(np.unpackbits(np.frombuffer(c.payload, np.uint8)),
+                                                   offs, c.slice_bit_counts, cb.decode_tree, D)
+        t = cb.decode_tree
+        out[nm + "_tree_children"], out[nm + "_tree_is_symbol"] = t.children, t.is_symbol
+        out[nm + "_tree_symbols"] = t.symbols
+        bits, cnt = kv.encode_slice(q.codes[3], cb)
+        out[nm + "_enc_slice3_bits"], out[nm + "_enc_slice3_count"] = bits.astype(np.uint8), np.int64(cnt)
+    out["meta_overhead"] = np.array(kv.metadata_overhead(blocks, D), np.float64)
+    # decompress_block of arena ordinals of the prefilled state
+    ords = [0, 3, 5]
+    out["dec_ords"] = np.array(ords, np.int64)
+    for nm, ar, cb, mode in (("k", st.k_arena, st.k_codebook, kv.QuantMode.K_BLOCK),
+                             ("v", st.v_arena, st.v_codebook, kv.QuantMode.V_TOKEN)):
+        res = [kv.decompress_block(ar, o, cb, mode=mode, head_num=H, head_dim=D, block_size=bs)
+               for o in ords]
+        out[nm + "_dec_codes"] = np.stack([r.codes for r in res])
+        out[nm + "_dec_mins"] = np.stack([r.unit_mins for r in res])
+        out[nm + "_dec_scales"] = np.stack([r.unit_scales for r in res])
+        out[nm + "_dec_idx"] = np.array([[r.block_index, r.head_index, r.ctx_start] for r in res],
+                                        np.int64)
+        out[nm + "_arena"] = np.frombuffer(ar.snapshot(), np.uint8).copy()
+        out[nm + "_offsets"] = ar.block_offsets.astype(np.uint32)
+        r = kv.CompressedArena.restore(ar.snapshot(), ar.block_offsets,
+                                       rcodec.units_per_block(mode, D, bs))
+        out[nm + "_restore_counters"] = np.array([r.payload_bits, r.payload_bytes, r.n_slices,
+                                                  r.size_bytes, len(r)], np.int64)
+    # CompressedArena.append: K block, V block, K block again, then a capacity refusal
+    a = kv.CompressedArena()
+    ords_app = [a.append(blocks[0]), a.append(blocks[1]), a.append(blocks[0])]
+    out["append_ordinals"] = np.array(ords_app, np.int64)
+    out["append_arena"] = np.frombuffer(a.snapshot(), np.uint8).copy()
+    out["append_offsets"] = a.block_offsets.astype(np.uint32)
+    out["append_counters"] = np.array([a.payload_bits, a.payload_bytes, a.n_slices], np.int64)
+    cap = len(rcodec._serialize_block(blocks[0])) + 8
+    a2 = kv.CompressedArena(capacity=cap)
+    a2.append(blocks[0])
+    try:
+        a2.append(blocks[1])
+        raise SystemExit("reference did not refuse the append")
+    except kv.ArenaFullError:
+        pass
+    out["append_capacity"] = np.int64(cap)
+    # quantize_unit on float64 units: KAT, values off the f32 grid, ties, constant
+    rng = np.random.default_rng(77)
+    units = [np.array([0, 1, 2, 3], np.float64), rng.standard_normal(97) * 1e3,
+             np.linspace(-1.0, 1.0, 41), np.full(9, 2.5), rng.standard_normal(300)]
+    rels = [0.5, 0.05, 0.05, 0.15, 1 / 255]
+    uc, um = [], []
+    for u, rel in zip(units, rels):
+        c, m = kv.quantize_unit(u, rel)
+        uc.append(c.astype(np.uint8))
+        um.append([m.min_value, m.scale])
+    out["unit_values"] = np.concatenate(units)
+    out["unit_sizes"] = np.array([len(u) for u in units], np.int64)
+    out["unit_rels"] = np.array(rels, np.float64)
+    out["unit_codes"] = np.concatenate(uc)
+    out["unit_metas"] = np.array(um, np.float64)
+    # single-symbol codebook tree (codebook.py:149-154) and its decode
+    h = np.zeros(256, np.uint64)
+    h[7] = 5
+    cb1 = kv.build_codebook(h)
+    t1 = cb1.decode_tree
+    out["single_tree_children"], out["single_tree_is_symbol"] = t1.children, t1.is_symbol
+    out["single_tree_symbols"] = t1.symbols
+    # run_ratio_sweep / run_simulation rows (ratio fields only; times differ)
+    rows = kv.run_ratio_sweep([64, 200], [0.05, 0.2], head_num=2, head_dim=64, seed=3)
+    out["sweep_rows"] = np.array([[r.context_len, r.original_bytes, r.compressed_bytes,
+                                   r.metadata_bytes] for r in rows], np.int64)
+    out["sweep_labels"] = np.array([r.config for r in rows])
+    sim = kv.run_simulation(kv.SimulationSettings(prompt_len=100, gen_len=40, head_num=2,
+                                                  head_dim=128, seed=5, warmup=1, reps=2),
+                            cfg_k, cfg_v)
+    out["sim_rows"] = np.array([[r.context_len, r.original_bytes, r.compressed_bytes,
+                                 r.metadata_bytes] for r in sim.rows], np.int64)
+    out["sim_label"] = np.array(sim.summary.config)
+    np.savez_compressed(os.path.join(HERE, "blockapi.npz"), **out)
+    print("blockapi: written")
+
+
 def _digest(st):
     h = {}
     for nm, a in (("k", st.k_arena), ("v", st.v_arena)):
@@ -325,8 +437,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--cfg2", action="store_true")
+    ap.add_argument("--only", default=None, help="run one generator, e.g. blockapi_cases")
     args = ap.parse_args()
+    if args.only:
+        globals()[args.only]()
+        return
     kat_cases()
+    blockapi_cases()
     make_case("c_fp16_d128", ctx=64 * 3 + 37, H=2, D=128, bs=64, seed=3, appended=100)
     make_case("c_f32_d32_bs16", ctx=16 * 5 + 3, H=4, D=32, bs=16, dtype=np.float32,
               synthetic=False, seed=7, appended=40)

@@ -95,3 +95,15 @@ def test_decode_lut_covers_every_window():
     for i in range(0, 4096, 37):
         s, l = int(syms[i]), int(lens[i])
         assert (i >> (12 - l)) == int(cb.code_words[s]) and cb.code_lengths[s] == l
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_decode_tree_matches_reference(case):
+    """HuffmanCodebook.decode_tree (codebook.py:144-176): the reference's node
+    numbering, host-side, from the reference-built codebooks' lengths."""
+    from paper_2509_00579_b200 import codebook_from_lengths
+    g = load(case)
+    for w in ("k", "v"):
+        t = codebook_from_lengths(g[f"fin_{w}_lengths"]).decode_tree
+        assert np.array_equal(t.children, g[f"fin_{w}_tree_children"])
+        assert t.n_nodes == len(g[f"fin_{w}_tree_children"])
