@@ -340,6 +340,9 @@ def main():
     ap.add_argument("--cpu-ctx", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--stream-steps", type=int, default=None,
+                    help="streaming-decode steps with appends (default: one overflow cycle, "
+                         "buffer_size = 128; 0 disables)")
     ap.add_argument("--no-paper", action="store_true",
                     help="skip the fused vs multistage vs matvec comparison")
     ap.add_argument("--no-py-ref", action="store_true",
@@ -349,6 +352,8 @@ def main():
     for k, v in PRESETS[args.config].items():
         if getattr(args, k, None) is None:
             setattr(args, k, v)
+    if args.stream_steps is None:
+        args.stream_steps = 128
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -560,6 +565,16 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # Streaming decode (BASELINE config 4 as a stream, reference bench.py:207-330):
+    # every step appends one token per (seq, layer) through the growing-cache
+    # Store, then runs the fused fetch; one full overflow cycle (buffer_size
+    # steps) so the amortised event cost is inside the timed region.  Eager
+    # (~2 launches per layer from Python) and as a CUDA graph (replayed between
+    # events, re-captured after each event).
+    streaming = None
+    if args.stream_steps > 0:
+        streaming = streaming_block(kv, torch, dist, states, G, q, outs, stream, args.stream_steps,
+                                    world, device, ms)
 
     world_f = world
     value = eq_bytes_step * world_f / (ms * 1e-3) / 1e9
@@ -634,6 +649,8 @@ def main():
             line["cpu_baseline"] = cpu
         if paper:
             line["paper_comparisons"] = paper
+        if streaming:
+            line["streaming"] = streaming
         if args.config == 5:
             line["quant_sweep"] = quant_sweep(kv, torch, device, T, H, B)
         print(json.dumps(line), flush=True)
@@ -677,6 +694,51 @@ def quant_sweep(kv, torch, device, T, H, B):
                      "fetch_ms": round(ms, 4)})
         del states
     return rows
+
+
+def streaming_block(kv, torch, dist, states, G, q, outs, stream, n_steps, world, device,
+                    no_append_ms):
+    """Timed decode steps that append a token per (seq, layer) and attend, via
+    DecodeLoop: eager and CUDA-graph.  Device time (CUDA events on the
+    launching stream) per step, max over ranks."""
+    L, B = len(states), len(states[0])
+    H, D = states[0][0].head_num, states[0][0].head_dim
+    kn = torch.randn((L, B, H, D), device=device, dtype=torch.float16)
+    vn = torch.randn_like(kn)
+    res = {"steps": n_steps, "appended_tokens_per_step": L * B,
+           "no_append_ms_per_step": round(no_append_ms, 4)}
+    for name, use_graph in (("eager", False), ("graph", True)):
+        loop = kv.DecodeLoop(states, group=G, use_graph=use_graph)
+        for _ in range(3):  # warm (and capture)
+            loop.step(kn, vn, q, outs)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ev0 = loop.events
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        a.record(stream)
+        for _ in range(n_steps):
+            loop.step(kn, vn, q, outs)
+        b.record(stream)
+        host_s = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / n_steps
+        if world > 1:
+            t = torch.tensor([ms], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        res[name] = {"ms_per_step": round(ms, 4),
+                     "vs_no_append": round(ms / no_append_ms, 4),
+                     "event_steps": loop.events - ev0, "graph_captures": loop.captures,
+                     "host_ms_per_step": round(host_s * 1e3 / n_steps, 4)}
+    for row in states:
+        for s in row:
+            s.check()  # sticky device errors of the appends (none expected)
+    res["note"] = ("each step: kvc_buffer_append per layer batch (+ Store launches on the "
+                   "overflow step), then the fused fetch; the context grows by one token per "
+                   "step; vs_no_append compares with the headline's no-append step")
+    return res
 
 
 def paper_comparisons(kv, torch, st, stream, reps=10):

@@ -106,6 +106,11 @@ typedef struct {
     int32_t stage_bytes_v;
     int32_t k_max_len;              /* longest K / V code length (host copy)   */
     int32_t v_max_len;
+    /* optional device int32[2] {n_chunks, buffered}: when non-NULL the kernels
+     * read these two counts from it (kvc_buffer_append / kvc_set_live keep it
+     * current), so a decode loop reuses one descriptor array across steps;
+     * the host array passed beside it must carry the same values. */
+    const int32_t *live;
 } kvc_seq_desc;
 
 /* ---------------------------------------------------------------- */
@@ -259,6 +264,28 @@ size_t kvc_attention_workspace_bytes(int n_seqs, int H, int group, int D, int ma
  * [ctx, H, D] (compressed region only; buffered rows untouched). */
 int kvc_dequantize(const kvc_seq_desc *seq_dev, int H, int D, int bs, int which /*0=K,1=V*/,
                    int n_chunks, float *out_dev, int *err_dev, void *stream);
+
+/* ---------------------------------------------------------------- */
+/* Growing cache, device side — kvcache.py:150-177 without host syncs */
+/* ---------------------------------------------------------------- */
+
+/* append_token's buffer write for n_seqs states in one launch: row
+ * buffered (read from seqs_dev[s].live[1], < cap_rows) of each state's K/V
+ * f32 buffers <- k/v_rows_dev[s] ([n_seqs][H*D], f16 or f32, seq_stride
+ * elements apart), then live[1] += 1.  Non-finite values -> *err_dev (NULL:
+ * the state's K arena counters' sticky err, raised by the next check). */
+int kvc_buffer_append(const kvc_seq_desc *seqs_dev, int n_seqs, int H, int D, int cap_rows,
+                      const void *k_rows_dev, const void *v_rows_dev, int x_dtype,
+                      long seq_stride, int *err_dev, void *stream);
+
+/* After an overflow event compressed buffer rows [0, n_rows): move rows
+ * [n_rows, n_rows + rem) to the front (rem < n_rows) and set live =
+ * {n_chunks, rem} (kvcache.py:168-177), for n_seqs states at once. */
+int kvc_buffer_shift(const kvc_seq_desc *seqs_dev, int n_seqs, int H, int D, int n_rows,
+                     int rem, int n_chunks, void *stream);
+
+/* live = {n_chunks, buffered} (state creation, prefill, restore). */
+int kvc_set_live(int32_t *live_dev, int n_chunks, int buffered, void *stream);
 
 /* ---------------------------------------------------------------- */
 /* Per-block codec surface — replaces codec.py:59-472 single-block API */

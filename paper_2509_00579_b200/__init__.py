@@ -19,7 +19,8 @@ from .codec import (CompressedArena, CompressedBlock, DataMovement, DeviceArena,
 from .container import load_state, read_header, save_state
 from .errors import (ArenaFullError, CodebookError, CodecError, ConfigError,
                      ContainerFormatError, KvpackError, TensorFormatError)
-from .kvcache import LayerCacheState
+from .decode_loop import DecodeLoop
+from .kvcache import LayerCacheState, append_batched
 from .metrics import (BenchRow, CompressionStats, SimulationResult, SimulationSettings,
                       collect_stats, config_label, equivalent_decompression_throughput,
                       median_time, run_ratio_sweep, run_simulation, write_csv)

@@ -65,7 +65,8 @@ class SeqDesc(ctypes.Structure):
                 ("k_buffer", ctypes.c_void_p), ("v_buffer", ctypes.c_void_p),
                 ("n_chunks", ctypes.c_int32), ("buffered", ctypes.c_int32),
                 ("stage_bytes_k", ctypes.c_int32), ("stage_bytes_v", ctypes.c_int32),
-                ("k_max_len", ctypes.c_int32), ("v_max_len", ctypes.c_int32)]
+                ("k_max_len", ctypes.c_int32), ("v_max_len", ctypes.c_int32),
+                ("live", ctypes.c_void_p)]
 
 
 P = ctypes.c_void_p
@@ -109,6 +110,9 @@ SIGNATURES = {
     "kvc_decode_slices_tree": (I, [P, I, U64, P, P, I, P, P, P, I, I, P, P, P]),
     "kvc_arena_append": (I, [P, U32, U64, U64, P, U64, P, P, P]),
     "kvc_arena_restore": (I, [P, U64, P, I, I, P, P, P, P]),
+    "kvc_buffer_append": (I, [P, I, I, I, I, P, P, I, L, P, P]),
+    "kvc_buffer_shift": (I, [P, I, I, I, I, I, I, P]),
+    "kvc_set_live": (I, [P, I, I, P]),
 }
 
 _lib = None

@@ -21,7 +21,7 @@ import torch
 from . import _lib
 from .codec import DataMovement
 from .errors import CodecError, ConfigError
-from .kvcache import LayerCacheState
+from .kvcache import LayerCacheState, _BatchDesc, append_batched  # noqa: F401
 from .tensor_io import CacheTensor
 
 
@@ -120,32 +120,6 @@ def _fused_supported(states: Sequence[LayerCacheState]) -> bool:
         return False
     return all(max(s.k_codebook.max_code_length, s.v_codebook.max_code_length) <= 12
                for s in states)
-
-
-class _BatchDesc:
-    """Device array of kvc_seq_desc for a fixed list of states (rebuilt on change)."""
-
-    def __init__(self):
-        self.key = None
-        self.dev = None
-        self.host = None
-
-    def get(self, states: Sequence[LayerCacheState]):
-        descs = [s.desc() for s in states]
-        # desc() returns the same object while a state is unchanged: an identity
-        # check skips the byte comparison on the decode loop's steady path
-        ids = tuple(map(id, descs))
-        if ids == getattr(self, "ids", None) and self.dev is not None:
-            return self.dev, self.host
-        raw = b"".join(bytes(d) for d in descs)
-        self.ids = ids
-        self.descs = descs  # keep them alive so the ids stay unique
-        if raw != self.key:
-            arr = (_lib.SeqDesc * len(descs))(*descs)
-            self.host = arr
-            self.dev = torch.from_numpy(np.frombuffer(raw, np.uint8).copy()).to(states[0].device)
-            self.key = raw
-        return self.dev, self.host
 
 
 _default_desc_cache = _BatchDesc()

@@ -228,6 +228,13 @@ class DeviceArena:
                                                      torch.uint8, zero=True)
         self.n_blocks = 0          # host mirror (deterministic)
         self._bound = 0            # host upper bound on the cursor
+        # host mirror of counters.max_extent (the fused fetch sizes its
+        # shared-memory stages from it): exact after a counters() read; after
+        # appends it is refreshed by an asynchronous readback, and until that
+        # lands stage sizes use the appended blocks' worst case
+        self._ext_host = 0
+        self._ext_worst = 0        # worst extent of blocks appended since the last read
+        self._ext_pending = None   # (pinned slot, event) of an in-flight readback
 
     def _pooled(self, nbytes: int, dtype, zero: bool = False):
         """A device tensor of nbytes (as dtype) from the slab pool, released
@@ -310,10 +317,31 @@ class DeviceArena:
         self._counters = torch.frombuffer(bytearray(counters), dtype=torch.uint8).to(self.device)
         self.n_blocks = nb
         self._bound = n
+        self._ext_pending = None
+        self._ext_host = _lib.ArenaCounters.from_buffer_copy(bytes(counters)).max_extent
+        self._ext_worst = 0
 
-    def note_append(self, n_blocks: int, worst_bytes: int) -> None:
+    def note_append(self, n_blocks: int, worst_bytes: int, block_worst: int = 0) -> None:
+        """Host mirrors after an append of n_blocks (worst_bytes in total,
+        block_worst per block); starts the asynchronous max-extent readback."""
         self.n_blocks += n_blocks
         self._bound += worst_bytes
+        if n_blocks:
+            self._ext_worst = max(self._ext_worst, block_worst or worst_bytes)
+            if self.device.type == "cuda":
+                self._ext_pending = _counters_readback(self._counters)
+
+    def max_extent_bound(self) -> int:
+        """An upper bound of every block extent, without synchronising: the
+        exact device value once known, else the worst case of the blocks
+        appended since it was last read."""
+        if self._ext_pending is not None:
+            buf, ev = self._ext_pending
+            if ev.query():
+                c = _lib.ArenaCounters.from_buffer_copy(buf.numpy().tobytes())
+                self._ext_pending = None
+                self._ext_host, self._ext_worst = int(c.max_extent), 0
+        return max(self._ext_host, self._ext_worst)
 
     @property
     def alloc_capacity(self) -> int:
@@ -363,6 +391,7 @@ class DeviceArena:
         raw = self._counters.cpu().numpy().tobytes()
         c = _lib.ArenaCounters.from_buffer_copy(raw)
         self._bound = int(c.cursor)
+        self._ext_host, self._ext_worst, self._ext_pending = int(c.max_extent), 0, None
         return c
 
     def check(self, what: str = "arena") -> None:
@@ -413,6 +442,36 @@ class DeviceArena:
 
     def offsets_tensor(self) -> torch.Tensor:
         return self._offsets
+
+
+class _PinnedRing:
+    """Pinned host slots for asynchronous counter readbacks; a slot is
+    rewritten only after the event of its previous copy has completed."""
+
+    def __init__(self, slot_bytes: int, slots: int = 1024):
+        self.buf = torch.empty((slots, slot_bytes), dtype=torch.uint8, pin_memory=True)
+        self.events = [None] * slots
+        self.i = 0
+
+
+_CNT_RING = None
+
+
+def _counters_readback(counters: torch.Tensor):
+    global _CNT_RING
+    if _CNT_RING is None:
+        _CNT_RING = _PinnedRing(ctypes.sizeof(_lib.ArenaCounters))
+    r = _CNT_RING
+    i = r.i
+    r.i = (i + 1) % len(r.events)
+    if r.events[i] is not None:
+        r.events[i].synchronize()
+    slot = r.buf[i]
+    slot.copy_(counters, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(counters.device))
+    r.events[i] = ev
+    return slot, ev
 
 
 def full_error(what="arena"):
@@ -668,7 +727,7 @@ def _block_image(cb: CompressedBlock) -> torch.Tensor:
     counts = _to_dev(cb.slice_bit_counts, torch.int32, dev).to(torch.int16).view(torch.uint8)
     metas = torch.stack([_to_dev(cb.unit_mins, torch.float32, dev).reshape(-1),
                          _to_dev(cb.unit_scales, torch.float32, dev).reshape(-1)], 1)
-    parts = [torch.from_numpy(hdr).to(dev), counts, metas.contiguous().view(torch.uint8),
+    parts = [torch.from_numpy(hdr).to(dev), counts, metas.contiguous().view(torch.uint8).reshape(-1),
              _to_dev(cb.payload, torch.uint8, dev).reshape(-1)]
     raw = sum(p.numel() for p in parts)
     parts.append(torch.zeros((-raw) % 4, dtype=torch.uint8, device=dev))

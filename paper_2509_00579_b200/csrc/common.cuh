@@ -29,6 +29,18 @@ __device__ __forceinline__ double kvc_load_d(const __half *p) { return (double)_
 __device__ __forceinline__ double kvc_load_d(const float *p) { return (double)*p; }
 __device__ __forceinline__ double kvc_load_d(const double *p) { return *p; }
 
+// A sequence descriptor with the live (n_chunks, buffered) pair: when
+// `live` is set the growing-cache Store keeps those two counts in device
+// memory, so the descriptor itself stays unchanged across decode steps.
+__device__ __forceinline__ kvc_seq_desc kvc_load_desc(const kvc_seq_desc *seqs, long i) {
+    kvc_seq_desc sd = seqs[i];
+    if (sd.live) {
+        sd.n_chunks = sd.live[0];
+        sd.buffered = sd.live[1];
+    }
+    return sd;
+}
+
 __device__ __forceinline__ void kvc_set_err(int *err, int code) {
     if (err) atomicCAS(err, 0, code);
 }

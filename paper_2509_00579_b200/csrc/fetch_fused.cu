@@ -210,7 +210,7 @@ fused_attn_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__r
     const uint32_t laneK_s = lutK_s + 4 * lane, laneV_s = lutV_s + 4 * lane;
 
     const int split = blockIdx.x, h = blockIdx.y, sidx = blockIdx.z;
-    const kvc_seq_desc sd = seqs[sidx];
+    const kvc_seq_desc sd = kvc_load_desc(seqs, sidx);
     if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) mbar_init(&bar[k], 1);
@@ -707,7 +707,7 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
     const int n_splits = plan.n;
     int split, h, sidx;
     plan_decode(plan, H, split, h, sidx);
-    const kvc_seq_desc sd = seqs[sidx];
+    const kvc_seq_desc sd = kvc_load_desc(seqs, sidx);
     if (!is_v && lane == 0) {
         mbar_init(&kfull[0], 1);
         mbar_init(&kfull[1], 1);
@@ -1052,7 +1052,7 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     const int n_splits = plan.n;
     int split, h, sidx;
     plan_decode(plan, H, split, h, sidx);
-    const kvc_seq_desc sd = seqs[sidx];
+    const kvc_seq_desc sd = kvc_load_desc(seqs, sidx);
     if (!is_v && lane == 0) {
         mbar_init(&kfull[0], 1);
         mbar_init(&kfull[1], 1);
@@ -1383,7 +1383,7 @@ combine_kernel(const kvc_seq_desc *__restrict__ seqs, int H, int bs, const float
     __shared__ float sh_red[8];
     __shared__ float sh_m, sh_l;
     const int hq = blockIdx.y, sidx = blockIdx.z, h = hq / group, HQ = H * group;
-    const kvc_seq_desc sd = seqs[sidx];
+    const kvc_seq_desc sd = kvc_load_desc(seqs, sidx);
     const float *qh = q + ((long)sidx * HQ + hq) * D;
     const float sm_scale = kLog2e / sqrtf((float)D), inv_sqrt = 1.0f / sqrtf((float)D);
     const int nbuf = sd.buffered;

@@ -85,7 +85,7 @@ k_scores_kernel(const kvc_seq_desc *__restrict__ seqs, int H, int D, int bs,
     __shared__ uint32_t sh_off[1024], sh_cnt[1024], sh_tot;
     __shared__ float sh_base;
     const int h = blockIdx.y, sidx = blockIdx.z;
-    const kvc_seq_desc sd = seqs[sidx];
+    const kvc_seq_desc sd = kvc_load_desc(seqs, sidx);
     const float *qh = q + ((long)sidx * H + h) * D;
     float *out = scores + ((long)sidx * H + h) * ctx_stride;
     const float inv = (float)(1.0 / sqrt((double)D));
@@ -145,7 +145,7 @@ v_output_kernel(const kvc_seq_desc *__restrict__ seqs, int H, int D, int bs,
     __shared__ float sh_a[1024];
     __shared__ float sh_wm;
     const int h = blockIdx.y, sidx = blockIdx.z;
-    const kvc_seq_desc sd = seqs[sidx];
+    const kvc_seq_desc sd = kvc_load_desc(seqs, sidx);
     const float *wh = w + ((long)sidx * H + h) * ctx_stride;
     float acc[kMaxDPerThread];
 #pragma unroll
@@ -213,7 +213,7 @@ __global__ void v_combine_kernel(const kvc_seq_desc *__restrict__ seqs, int H, i
                                  const float *__restrict__ partial, const float *__restrict__ w,
                                  long ctx_stride, int bs, float *__restrict__ out) {
     const int h = blockIdx.y, sidx = blockIdx.z;
-    const kvc_seq_desc sd = seqs[sidx];
+    const kvc_seq_desc sd = kvc_load_desc(seqs, sidx);
     const float *wh = w + ((long)sidx * H + h) * ctx_stride;
     const long t0 = (long)sd.n_chunks * bs;
     for (int c = threadIdx.x; c < D; c += blockDim.x) {

@@ -88,11 +88,13 @@ class KVCompLayer(CacheLayerMixin):
             return key_states, value_states
         if len(self.states) != B:
             raise ValueError("batch size changed after prefill")
-        for b, st in enumerate(self.states):
-            for t in range(T):
-                st.append_token(key_states[b, :, t], value_states[b, :, t], validate=False)
+        from .kvcache import _BatchDesc, append_batched
+        if self._desc is None:
+            self._desc = _BatchDesc()
+        for t in range(T):  # the batch rows' token t in one device append
+            append_batched(self.states, key_states[:, :, t], value_states[:, :, t],
+                           desc_cache=self._desc)
         self.cumulative_length += T
-        self._desc = None if T > 1 else self._desc
         if T == 1:
             self.decode_pending = True
             _LAST_DECODE = self

@@ -124,6 +124,15 @@ class LayerCacheState:
         self._k_tab = k_codebook.device_tables(self.device)
         self._v_tab = v_codebook.device_tables(self.device)
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+        # live {n_chunks, buffered} on the device (kvc_seq_desc.live): the
+        # growing-cache kernels update it, the fetch kernels read it, so the
+        # descriptor stays the same across decode steps; the host keeps
+        # deterministic mirrors (compressed_tokens, buffered)
+        if self.device.type == "cuda":
+            self._live, ext = pooled_zeros((2,), torch.int32, self.device)
+            weakref.finalize(self, ext.release)
+        else:
+            self._live = torch.zeros(2, dtype=torch.int32, device=self.device)
         self.context_len = 0
         self.compressed_tokens = 0
         self.buffered = 0
@@ -337,6 +346,7 @@ class LayerCacheState:
             st._v_buffer[:r] = vt[n_full:].to(torch.float32)
         st.buffered = r
         st.context_len = ctx
+        st._publish_live()
         if check:
             st.check()
         return st
@@ -367,7 +377,7 @@ class LayerCacheState:
             _lib.check(st, "kvc_encode_append")
             if arena.capacity is not None:  # codec.py:313-318: a full arena raises here
                 arena.check("arena")
-            arena.note_append(nb, worst)
+            arena.note_append(nb, worst, worst_block_bytes(bs, n_units, D, cb.max_code_length))
         self.compressed_tokens += n_chunks * bs
 
     def _store(self, k_src: torch.Tensor, v_src: torch.Tensor, n_chunks: int,
@@ -409,8 +419,8 @@ class LayerCacheState:
             # (codec.py:313-318), before the host mirrors advance
             self.k_arena.check("K arena")
             self.v_arena.check("V arena")
-        self.k_arena.note_append(nb, kw)
-        self.v_arena.note_append(nb, vw)
+        self.k_arena.note_append(nb, kw, worst_block_bytes(bs, D, D, self.k_codebook.max_code_length))
+        self.v_arena.note_append(nb, vw, worst_block_bytes(bs, bs, D, self.v_codebook.max_code_length))
         self.compressed_tokens += n_chunks * bs
 
     def _compress_buffer(self, n: int) -> None:
@@ -427,16 +437,53 @@ class LayerCacheState:
                                          bs, QuantMode.V_TOKEN, self.cfg_v.rel_quant_scale)
         self._encode(kcodes, kmetas, vcodes, vmetas, n_chunks)
 
-    # ------------------------------------------------------------------
+    def _publish_live(self) -> None:
+        """Device live pair <- host mirrors (after prefill / restore)."""
+        if self.device.type != "cuda":
+            self._live.copy_(torch.tensor([self.n_chunks, self.buffered], dtype=torch.int32))
+            return
+        _lib.check(_lib.lib().kvc_set_live(self._live.data_ptr(), self.n_chunks, self.buffered,
+                                           torch.cuda.current_stream(self.device).cuda_stream),
+                   "kvc_set_live")
+
+    def _after_append(self) -> Optional[int]:
+        """Host mirrors after one appended token; returns the rows to compress
+        when the buffer overflows (kvcache.py:168-177), else None."""
+        self.buffered += 1
+        self.context_len += 1
+        if self.buffered > self.cfg_k.buffer_size:
+            bs = self.cfg_k.block_size
+            return (self.buffered // bs) * bs
+        return None
+
+    def _overflow(self, n: int, desc_dev: Optional[torch.Tensor] = None) -> None:
+        """Overflow event: compress buffer rows [0, n), move the remainder to
+        the front and publish the new live pair, all on the device."""
+        self._compress_buffer(n)
+        rem = self.buffered - n
+        if desc_dev is None:
+            desc_dev = self.desc_device()
+        _lib.check(_lib.lib().kvc_buffer_shift(desc_dev.data_ptr(), 1, self.head_num,
+                                               self.head_dim, n, rem, self.n_chunks,
+                                               torch.cuda.current_stream(self.device).cuda_stream),
+                   "kvc_buffer_shift")
+        self.buffered = rem
+
     def append_token(self, k_vec, v_vec, validate: bool = True) -> None:
         """kvcache.py:150-177.  Host arrays are validated on the host; device
-        tensors are validated with one device reduction when validate=True."""
+        tensors with one device reduction when validate=True (validate=False:
+        non-finite values set the state's sticky error, raised by check()).
+        The buffer write and the live counts are device work (kvc_buffer_append):
+        no synchronisation on the decode path."""
         expected = (self.head_num, self.head_dim)
         if isinstance(k_vec, torch.Tensor) and isinstance(v_vec, torch.Tensor):
             if tuple(k_vec.shape) != expected or tuple(v_vec.shape) != expected:
                 raise CodecError(f"token vectors must have shape {expected}")
-            kd = k_vec.to(self.device, torch.float32)
-            vd = v_vec.to(self.device, torch.float32)
+            kd, vd = k_vec, v_vec
+            if kd.dtype not in (torch.float16, torch.float32) or kd.dtype != vd.dtype:
+                kd, vd = kd.to(torch.float32), vd.to(torch.float32)
+            kd = kd.to(self.device).contiguous()
+            vd = vd.to(self.device).contiguous()
             if validate and not bool(torch.isfinite(kd).all() & torch.isfinite(vd).all()):
                 raise CodecError("non-finite token vectors rejected")
         else:
@@ -448,19 +495,27 @@ class LayerCacheState:
                 raise CodecError("non-finite token vectors rejected")
             kd = torch.from_numpy(kn).to(self.device, non_blocking=False)
             vd = torch.from_numpy(vn).to(self.device, non_blocking=False)
-        self._k_buffer[self.buffered] = kd
-        self._v_buffer[self.buffered] = vd
-        self.buffered += 1
-        self.context_len += 1
-        if self.buffered > self.cfg_k.buffer_size:
-            bs = self.cfg_k.block_size
-            n = (self.buffered // bs) * bs
-            self._compress_buffer(n)
-            rem = self.buffered - n
-            if rem:
-                self._k_buffer[:rem] = self._k_buffer[n: self.buffered].clone()
-                self._v_buffer[:rem] = self._v_buffer[n: self.buffered].clone()
-            self.buffered = rem
+        if self.device.type != "cuda":
+            self._k_buffer[self.buffered] = kd
+            self._v_buffer[self.buffered] = vd
+            n = self._after_append()
+            if n is not None:
+                self._compress_buffer(n)
+                rem = self.buffered - n
+                if rem:
+                    self._k_buffer[:rem] = self._k_buffer[n: self.buffered].clone()
+                    self._v_buffer[:rem] = self._v_buffer[n: self.buffered].clone()
+                self.buffered = rem
+            self._live.copy_(torch.tensor([self.n_chunks, self.buffered], dtype=torch.int32))
+            return
+        dd = self.desc_device()
+        _lib.check(_lib.lib().kvc_buffer_append(
+            dd.data_ptr(), 1, self.head_num, self.head_dim, self.cfg_k.buffer_size + 1,
+            kd.data_ptr(), vd.data_ptr(), dtype_code(kd), 0, None,
+            torch.cuda.current_stream(self.device).cuda_stream), "kvc_buffer_append")
+        n = self._after_append()
+        if n is not None:
+            self._overflow(n, dd)
 
     def append_tokens(self, k_tokens: torch.Tensor, v_tokens: torch.Tensor) -> None:
         """Append many tokens (device tensors [n, H, D]); identical arenas to
@@ -475,6 +530,14 @@ class LayerCacheState:
         self.k_arena.check("K arena")
         self.v_arena.check("V arena")
 
+    def settle(self) -> None:
+        """Wait for the arenas' in-flight max-extent readbacks (after appends)
+        so stage_bytes() is exact again; waits on those copies only."""
+        for a in (self.k_arena, self.v_arena):
+            if a._ext_pending is not None:
+                a._ext_pending[1].synchronize()
+                a.max_extent_bound()
+
     def compact(self, headroom: int = 0) -> None:
         """Trim arena allocations to their contents (pointers change)."""
         self.k_arena.compact(headroom)
@@ -486,39 +549,46 @@ class LayerCacheState:
         return self.compressed_tokens // self.cfg_k.block_size
 
     def stage_bytes(self) -> Tuple[int, int]:
-        """Shared-memory staging size per K / V extent for the fused fetch."""
-        bs, D = self.cfg_k.block_size, self.head_dim
+        """Shared-memory staging size per K / V extent for the fused fetch,
+        from the arenas' host max-extent bounds (no synchronisation)."""
         out = []
-        for arena, cb, n_units in ((self.k_arena, self.k_codebook, D),
-                                   (self.v_arena, self.v_codebook, bs)):
-            ext = arena.max_extent if arena.n_blocks else 16
+        for arena in (self.k_arena, self.v_arena):
+            ext = arena.max_extent_bound() if arena.n_blocks else 16
             out.append(((ext + 15) // 16) * 16 + 48)
         return out[0], out[1]
 
     def desc(self) -> _lib.SeqDesc:
-        key = (self.compressed_tokens, self.buffered, self.k_arena.buf_ptr, self.v_arena.buf_ptr,
-               self.k_arena.offsets_ptr, self.v_arena.offsets_ptr)
-        if self._desc_key == key and getattr(self, "_desc_host", None) is not None:
-            return self._desc_host
+        """The kernels' view of this state.  Stable across decode steps: the
+        token counts travel through the device live pair, so only an arena
+        reallocation or a new stage size makes a new descriptor; the host
+        copy's n_chunks / buffered are refreshed on every call."""
         sk, sv = self.stage_bytes()
-        d = _lib.SeqDesc(
-            k_arena=self.k_arena.buf_ptr, k_offsets=self.k_arena.offsets_ptr,
-            k_counters=self.k_arena.counters_ptr, k_cb=self._k_tab.data_ptr(),
-            v_arena=self.v_arena.buf_ptr, v_offsets=self.v_arena.offsets_ptr,
-            v_counters=self.v_arena.counters_ptr, v_cb=self._v_tab.data_ptr(),
-            k_buffer=self._k_buffer.data_ptr(), v_buffer=self._v_buffer.data_ptr(),
-            n_chunks=self.n_chunks, buffered=self.buffered, stage_bytes_k=sk, stage_bytes_v=sv,
-            k_max_len=self.k_codebook.max_code_length, v_max_len=self.v_codebook.max_code_length)
-        self._desc_host = d
-        self._desc_key = key
-        self._desc_dev = None
+        key = (self.k_arena.buf_ptr, self.v_arena.buf_ptr, self.k_arena.offsets_ptr,
+               self.v_arena.offsets_ptr, self.k_arena.counters_ptr, self.v_arena.counters_ptr,
+               sk, sv)
+        d = getattr(self, "_desc_host", None)
+        if self._desc_key != key or d is None:
+            d = _lib.SeqDesc(
+                k_arena=self.k_arena.buf_ptr, k_offsets=self.k_arena.offsets_ptr,
+                k_counters=self.k_arena.counters_ptr, k_cb=self._k_tab.data_ptr(),
+                v_arena=self.v_arena.buf_ptr, v_offsets=self.v_arena.offsets_ptr,
+                v_counters=self.v_arena.counters_ptr, v_cb=self._v_tab.data_ptr(),
+                k_buffer=self._k_buffer.data_ptr(), v_buffer=self._v_buffer.data_ptr(),
+                n_chunks=self.n_chunks, buffered=self.buffered, stage_bytes_k=sk,
+                stage_bytes_v=sv, k_max_len=self.k_codebook.max_code_length,
+                v_max_len=self.v_codebook.max_code_length, live=self._live.data_ptr())
+            self._desc_host = d
+            self._desc_key = key
+            self._desc_dev = None
+        else:
+            d.n_chunks = self.n_chunks
+            d.buffered = self.buffered
         return d
 
     def desc_device(self) -> torch.Tensor:
         d = self.desc()
         if self._desc_dev is None:
-            raw = np.frombuffer(bytes(d), dtype=np.uint8).copy()
-            self._desc_dev = torch.from_numpy(raw).to(self.device)
+            self._desc_dev = upload_bytes(bytes(d), self.device)
         return self._desc_dev
 
     # ------------------------------------------------------------------
@@ -546,3 +616,110 @@ def _prefill_call(fn, blk_hist_ptr, codes_ptr, *args):
     """kvc_store_prefill takes kvc_store_append's arguments plus the per-block
     histograms and pass A's codes before the workspace."""
     return fn(*args[:-3], blk_hist_ptr, codes_ptr, *args[-3:])
+
+
+class _PinnedUpload:
+    """Pinned staging ring for small asynchronous H2D uploads (descriptor
+    arrays): a pageable .to(device) would synchronise the stream.  A slot is
+    rewritten only after the event of its previous copy has completed."""
+
+    def __init__(self, slot_bytes: int = 1 << 16, slots: int = 64):
+        self.slot_bytes = slot_bytes
+        self.buf = torch.empty((slots, slot_bytes), dtype=torch.uint8, pin_memory=True)
+        self.events = [None] * slots
+        self.i = 0
+
+
+_UPLOAD = None
+
+
+def upload_bytes(raw: bytes, device) -> torch.Tensor:
+    """bytes -> a new device uint8 tensor, stream-ordered, without a sync."""
+    global _UPLOAD
+    dev = torch.device(device)
+    n = len(raw)
+    if dev.type != "cuda":
+        return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev)
+    if _UPLOAD is None:
+        _UPLOAD = _PinnedUpload()
+    r = _UPLOAD
+    if n > r.slot_bytes:
+        return torch.from_numpy(np.frombuffer(raw, np.uint8).copy()).pin_memory().to(
+            dev, non_blocking=True)
+    i = r.i
+    r.i = (i + 1) % len(r.events)
+    if r.events[i] is not None:
+        r.events[i].synchronize()
+    slot = r.buf[i, :n]
+    slot.numpy()[:] = np.frombuffer(raw, np.uint8)
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    out.copy_(slot, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(dev))
+    r.events[i] = ev
+    return out
+
+
+class _BatchDesc:
+    """Device array of kvc_seq_desc for a fixed list of states, re-uploaded
+    only when a state's descriptor changes (arena reallocation, stage size);
+    the token counts travel through each state's live pair.  The host copy
+    (kvc_attention plans its splits from it) gets the current counts on
+    every call."""
+
+    def __init__(self):
+        self.key = None
+        self.dev = None
+        self.host = None
+        self.ids = None
+
+    def get(self, states):
+        descs = [s.desc() for s in states]
+        # desc() returns the same object while a state's descriptor is
+        # unchanged: an identity check skips the byte comparison
+        ids = tuple(map(id, descs))
+        if ids != self.ids or self.dev is None:
+            raw = b"".join(bytes(d) for d in descs)
+            self.ids = ids
+            self.descs = descs  # keep them alive so the ids stay unique
+            self.host = (_lib.SeqDesc * len(descs))(*descs)
+            if raw != self.key:
+                self.dev = upload_bytes(raw, states[0].device)
+                self.key = raw
+        else:
+            h = self.host
+            for i, s in enumerate(states):
+                h[i].n_chunks = s.n_chunks
+                h[i].buffered = s.buffered
+        return self.dev, self.host
+
+
+def append_batched(states, k_rows: torch.Tensor, v_rows: torch.Tensor,
+                   desc_cache: Optional[_BatchDesc] = None) -> None:
+    """append_token for a batch of same-shape states in one launch
+    (kvc_buffer_append): k_rows / v_rows [B, H, D] f16|f32 on the device.
+    Overflow events (kvcache.py:168-177) then run per state.  No host sync;
+    non-finite values set the states' sticky error (raised by check())."""
+    s0 = states[0]
+    B, H, D = len(states), s0.head_num, s0.head_dim
+    if tuple(k_rows.shape) != (B, H, D) or tuple(v_rows.shape) != (B, H, D):
+        raise CodecError(f"token rows must have shape {(B, H, D)}")
+    for s in states[1:]:
+        if (s.head_num, s.head_dim, s.cfg_k.buffer_size, s.device) != (
+                H, D, s0.cfg_k.buffer_size, s0.device):
+            raise ConfigError("batched states must share head_num, head_dim, buffer and device")
+    kd, vd = k_rows, v_rows
+    if kd.dtype not in (torch.float16, torch.float32) or kd.dtype != vd.dtype:
+        kd, vd = kd.to(torch.float32), vd.to(torch.float32)
+    kd = kd.to(s0.device).contiguous()
+    vd = vd.to(s0.device).contiguous()
+    cache = desc_cache if desc_cache is not None else _BatchDesc()
+    ddev, _ = cache.get(states)
+    _lib.check(_lib.lib().kvc_buffer_append(
+        ddev.data_ptr(), B, H, D, s0.cfg_k.buffer_size + 1, kd.data_ptr(), vd.data_ptr(),
+        dtype_code(kd), H * D, None, torch.cuda.current_stream(s0.device).cuda_stream),
+        "kvc_buffer_append")
+    for s in states:
+        n = s._after_append()
+        if n is not None:
+            s._overflow(n)
