@@ -277,7 +277,11 @@ class DeviceArena:
             return  # fixed capacity: the device reports ArenaFullError
         need = self._bound + worst_bytes
         if need > self._buf.numel() - TMA_SLACK:
-            new_cap = max(need, 2 * (self._buf.numel() - TMA_SLACK))
+            # 1.25x growth: a compacted config-2 arena is ~90 MB and a decode
+            # step's overflow event adds ~0.3 MB, so doubling would map (and
+            # copy) gigabytes per event across a batch of states
+            cur = self._buf.numel() - TMA_SLACK
+            new_cap = max(need, cur + cur // 4, 1 << 16)
             self._set_buf(new_cap + TMA_SLACK, keep=self._buf.numel())
 
     def compact(self, headroom: int = 0) -> None:

@@ -1773,11 +1773,9 @@ extern "C" size_t kvc_attention_workspace_bytes(int n_seqs, int H, int group, in
     // partials: n_seqs * H * group * max_splits; max splits bounded by chunks / (4*NW)
     long splits = (max_chunks + 4 * NW - 1) / (4 * NW) + 1;
     long nh = (long)n_seqs * H * (group > 0 ? group : 1);
-    size_t part = sizeof(Partial) * (size_t)nh * (size_t)splits;
-    // generic fallback: scores/weights [n_seqs, H*group, ctx] + v partials
-    size_t gen = sizeof(float) * (size_t)nh * ((size_t)max_chunks * 1024 + 256) + 0;
+    // (the shape-generic fallback sizes its own scratch: kvc_v_output_workspace_bytes)
     (void)D_;
-    return part > gen ? part : gen;
+    return sizeof(Partial) * (size_t)nh * (size_t)splits;
 }
 
 extern "C" int kvc_v_output(const kvc_seq_desc *, int, int, int, int, const float *, long, float *,

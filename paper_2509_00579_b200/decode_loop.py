@@ -39,6 +39,7 @@ class DecodeLoop:
         self.captures = 0
         s0 = self.states[0][0]
         self._ws = torch.empty(0, dtype=torch.uint8, device=s0.device)
+        self._stream = torch.cuda.Stream(s0.device) if self.use_graph else None
 
     # ------------------------------------------------------------------
     def _attend(self, layer: int, q: torch.Tensor, out: torch.Tensor) -> None:
@@ -79,13 +80,21 @@ class DecodeLoop:
         for layer, row in enumerate(self.states):
             self.caches[layer].get(row)
         saved = [(s.buffered, s.context_len) for r in self.states for s in r]
+        # capture_begin/end directly: the torch.cuda.graph context manager
+        # also synchronises, runs gc.collect() and empties the allocator cache
+        # (~1 s with a large resident cache), on every re-capture
+        dev = self.states[0][0].device
         g = torch.cuda.CUDAGraph()
-        stream = torch.cuda.Stream(self.states[0][0].device)
-        stream.wait_stream(torch.cuda.current_stream())
+        self.graph = None  # its private memory pool goes with it
+        stream = self._stream
+        stream.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(stream):
-            with torch.cuda.graph(g, stream=stream):
+            g.capture_begin()
+            try:
                 self._eager(k_new, v_new, q, out)
-        torch.cuda.current_stream().wait_stream(stream)
+            finally:
+                g.capture_end()
+        torch.cuda.current_stream(dev).wait_stream(stream)
         it = iter(saved)
         for r in self.states:
             for s in r:
@@ -108,6 +117,12 @@ class DecodeLoop:
             return out
         io = (k_new.data_ptr(), v_new.data_ptr(), q.data_ptr(), out.data_ptr())
         if self.graph is None or io != self.graph_io:
+            # after an event, stay eager until the arenas' max-extent readbacks
+            # have landed (exact stage sizes without draining the stream)
+            if not all(s.extents_ready() for r in self.states for s in r):
+                self._reserve_workspace()
+                self._eager(k_new, v_new, q, out)
+                return out
             self._capture(k_new, v_new, q, out)
         self.graph.replay()
         for r in self.states:

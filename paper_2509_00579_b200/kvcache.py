@@ -530,6 +530,15 @@ class LayerCacheState:
         self.k_arena.check("K arena")
         self.v_arena.check("V arena")
 
+    def extents_ready(self) -> bool:
+        """True when no max-extent readback is in flight (non-blocking)."""
+        for a in (self.k_arena, self.v_arena):
+            if a._ext_pending is not None:
+                a.max_extent_bound()
+                if a._ext_pending is not None:
+                    return False
+        return True
+
     def settle(self) -> None:
         """Wait for the arenas' in-flight max-extent readbacks (after appends)
         so stage_bytes() is exact again; waits on those copies only."""
