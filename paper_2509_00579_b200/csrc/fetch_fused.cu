@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "mma.cuh"
 
 namespace {
 
@@ -1373,6 +1374,528 @@ fused_attn_gqa_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float 
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Decode-once GQA fused fetch on tensor cores (default for groups 2 and 4).
+// Same warp specialisation, TMA rings and score ring as fused_attn_gqa_kernel,
+// but both dot products run on mma.sync m16n8k16 (f16 in, f32 accumulate):
+//   K warp: the decoded codes of a 16-channel slab x 64 tokens go to a 1 KB u8
+//     tile (one STS.128 per slice and slab), ldmatrix brings 4 codes per lane,
+//     two PRMT + HSUB2 make them exact f16 A fragments (channel order
+//     permuted within the slab; B follows), and S[tok][n] += codes . B with B
+//     = q' in two f16 pieces (n = g: f16(q' 2^e), n = G+g: the f16
+//     remainder; 2^e a per-chunk power of two): 8 slabs x 4 token m-tiles;
+//   V warp: the same u8 slab tile, ldmatrix.trans, is V^T (rows = channel
+//     pairs) and O^T[ch][n] += V^T . W with W = p_t scale_t in two f16 pieces
+//     (per-chunk power-of-two scale): 8 channel m-tiles x 4 token k-steps.
+// The FFMA dot products of the CUDA-core kernel (4 FFMA2 + 2 LDS.128 per
+// pair step on the K side, a per-channel GEMV on the V side) become ~1
+// instruction per pair step plus the MMAs.
+// ---------------------------------------------------------------------------
+constexpr int kMmRow = 16;          // u8 code tile row: one 16-channel slab
+constexpr int kQbRow = 272;         // q' pieces [8][128 + 8] f16
+constexpr int kWbRow = 144;         // w pieces [8][64 + 8] f16
+constexpr int kRegKm = 120, kRegVm = 136;
+__host__ __device__ constexpr int gqa_mma_per_pair(int stage_k, int stage_v, int G, int vslots) {
+    return 2 * stage_k + vslots * stage_v + 8 * kQbRow + 8 * kWbRow + 2 * G * BS * 4 +
+           2 * BS * kMmRow + 64;
+}
+
+// f16x2 of two u8 codes picked from x by a PRMT selector ([b, 0x64, b', 0x64]):
+// f16(1024 + c) has the code in its low mantissa bits, minus 1024 is exact
+template <uint32_t SEL>
+__device__ __forceinline__ uint32_t u8x2_f16x2(uint32_t x) {
+    const uint32_t y = __byte_perm(x, 0x6464u, SEL);
+    uint32_t r;
+    asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(y), "r"(0x64006400u));
+    return r;
+}
+// k position of channel c (0..15) of a slab in the K MMA: ldmatrix hands lane
+// (g, t) the codes 4t..4t+3, used as k = 2t, 2t+1, 2t+8, 2t+9
+__host__ __device__ constexpr int slab_kpos(int c) {
+    return 2 * (c >> 2) + (c & 1) + 8 * ((c >> 1) & 1);
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+                 "r"(d));
+}
+__device__ __forceinline__ void sts16(uint32_t addr, __half v) {
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(addr), "h"(__half_as_ushort(v)));
+}
+__device__ __forceinline__ uint32_t lds32m(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+// power of two p with amax * p in [2^13, 2^14) (p = 1 for amax == 0)
+__device__ __forceinline__ int pow2_exp(float amax) { return amax > 0.f ? 13 - ilogbf(amax) : 0; }
+
+template <int G, int NP, int VS>
+__global__ void __launch_bounds__(NP * 64, 1)
+fused_attn_gqa_mma_kernel(const kvc_seq_desc *__restrict__ seqs, int H,
+                          const float *__restrict__ q, Partial *__restrict__ partial,
+                          const SplitPlan plan, int stage_k, int stage_v, int *err) {
+    static_assert(G == 2 || G == 4, "GQA group");
+    __shared__ __align__(128) uint32_t s_lutK[1 << KVC_LUT_BITS];
+    __shared__ __align__(128) uint32_t s_lutV[1 << KVC_LUT_BITS];
+    __shared__ uint64_t s_lbar[1];
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const bool is_v = warp >= NP;
+    const int pair = is_v ? warp - NP : warp;
+    const int per_pair = gqa_mma_per_pair(stage_k, stage_v, G, VS);
+    uint8_t *pb = smem + pair * per_pair;
+    uint8_t *kring = pb, *vring = pb + 2 * stage_k;
+    uint8_t *qb = vring + VS * stage_v;                       // [8][kQbRow]
+    uint8_t *wb = qb + 8 * kQbRow;                            // [8][kWbRow]
+    float *sring = reinterpret_cast<float *>(wb + 8 * kWbRow);  // [2][G][64]
+    uint8_t *kbuf = reinterpret_cast<uint8_t *>(sring + 2 * G * BS);  // [64][kMmRow]
+    uint8_t *vbuf = kbuf + BS * kMmRow;                                 // [64][kMmRow]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(vbuf + BS * kMmRow);
+    uint64_t *kfull = bar, *vfull = bar + 2, *sfull = bar + 4, *sempty = bar + 6;
+
+    const int n_splits = plan.n;
+    int split, h, sidx;
+    plan_decode(plan, H, split, h, sidx);
+    const kvc_seq_desc sd = kvc_load_desc(seqs, sidx);
+    if (!is_v && lane == 0) {
+        mbar_init(&kfull[0], 1);
+        mbar_init(&kfull[1], 1);
+        mbar_init(&vfull[0], 1);
+        mbar_init(&vfull[1], 1);
+        mbar_init(&sfull[0], 32);
+        mbar_init(&sfull[1], 32);
+        mbar_init(&sempty[0], 32);
+        mbar_init(&sempty[1], 32);
+    }
+    if (threadIdx.x == 0) mbar_init(s_lbar, 1);
+    fence_mbar_init();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(s_lbar, 2u * (4u << KVC_LUT_BITS));
+        tma_load_1d(s_lutK, sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+        tma_load_1d(s_lutV, sd.v_cb->fetch_lut_x, 4u << KVC_LUT_BITS, s_lbar);  // bank-swizzled
+    }
+    const int c_begin = plan.begin[split];
+    const int c_end = min(sd.n_chunks, plan.begin[split + 1]);
+    const int first = c_begin + pair;
+    const int n = first < c_end ? (c_end - first + NP - 1) / NP : 0;
+    const float sm_scale = kLog2e / sqrtf((float)D);
+    const long nb_k = (long)sd.k_counters->n_blocks, nb_v = (long)sd.v_counters->n_blocks;
+    const uint64_t cur_k = sd.k_counters->cursor, cur_v = sd.v_counters->cursor;
+    auto issue = [&](bool v, int j) {
+        const long ord = (long)(first + NP * j) * H + h;
+        const uint32_t *offs = v ? sd.v_offsets : sd.k_offsets;
+        const long nb = v ? nb_v : nb_k;
+        const uint64_t s0 = offs[ord];
+        const uint64_t e0 = (ord + 1 < nb) ? (uint64_t)offs[ord + 1] : (v ? cur_v : cur_k);
+        const uint64_t a = s0 & ~15ull;
+        uint32_t bytes = (uint32_t)(((e0 + 15) & ~15ull) - a);
+        if (bytes > (uint32_t)(v ? stage_v : stage_k)) {
+            kvc_set_err(err, KVC_ERR_CODEC);
+            bytes = 16;
+        }
+        const int vsl = VS == 2 ? (j & 1) : 0;
+        uint64_t *b = v ? &vfull[vsl] : &kfull[j & 1];
+        uint8_t *dst = v ? vring + vsl * stage_v : kring + (j & 1) * stage_k;
+        mbar_expect_tx(b, bytes);
+        tma_load_1d(dst, (v ? sd.v_arena : sd.k_arena) + a, bytes, b);
+    };
+    bool bad = false;
+    // this lane's rows of a 64-token code tile: token lane (slice A), lane+32 (B)
+    const uint32_t rowA_k = smem_u32(kbuf) + lane * kMmRow, rowB_k = rowA_k + 32 * kMmRow;
+    const uint32_t rowA_v = smem_u32(vbuf) + lane * kMmRow, rowB_v = rowA_v + 32 * kMmRow;
+
+    if (!is_v) {
+        // ======== K warp: codes tile -> S = codes . q' on tensor cores ========
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegKm));
+        if (lane == 0) {
+            if (n > 0) issue(false, 0);
+            if (n > 1) issue(false, 1);
+        }
+        float qreg[G][4];
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                qreg[g][k] = q[((long)sidx * H * G + (long)h * G + g) * D + lane + 32 * k];
+        const uint32_t lut_s = smem_u32(s_lutK), qb_s = smem_u32(qb);
+        // ldmatrix x4 over tokens 0-31 / 32-63 of the slab tile: lane t's row = token t
+        const uint32_t a_ld = smem_u32(kbuf) + lane * kMmRow;
+        mbar_wait(s_lbar, 0);
+        uint32_t kofs_next = n > 0 ? sd.k_offsets[(long)first * H + h] & 15u : 0u;
+        for (int j = 0; j < n; ++j) {
+            const int u = j >> 1, sl = j & 1;
+            const uint32_t kofs = kofs_next;
+            if (j + 1 < n) kofs_next = sd.k_offsets[(long)(first + NP * (j + 1)) * H + h] & 15u;
+            mbar_wait(&kfull[sl], u & 1);
+            const uint8_t *ks = kring + sl * stage_k + kofs;
+            const uint32_t cA = lds_u16(ks + 6 + 2 * lane), cB = lds_u16(ks + 6 + 2 * (lane + 32));
+            const uint32_t iA = kvc_warp_incl_scan(cA, lane);
+            const uint32_t totA = __shfl_sync(0xffffffffu, iA, 31);
+            const uint32_t iB = kvc_warp_incl_scan(cB, lane);
+            // q' = scale_c q_c per member, its power-of-two scale, the f16 pieces
+            float base[G], qp[G][4], amax = 0.f;
+#pragma unroll
+            for (int g = 0; g < G; ++g) base[g] = 0.f;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int c = lane + 32 * k;
+                const float sc = lds_f32_a2(ks + 6 + 2 * BS + 8 * c + 4);
+                const float mn = lds_f32_a2(ks + 6 + 2 * BS + 8 * c);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    qp[g][k] = sc * qreg[g][k];
+                    amax = fmaxf(amax, fabsf(qp[g][k]));
+                    base[g] = fmaf(mn, qreg[g][k], base[g]);
+                }
+            }
+            const int e = pow2_exp(kvc_warp_max(amax));
+            const float qs = ldexpf(1.f, e);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int c = lane + 32 * k;
+                const uint32_t col = 2 * ((c & ~15) + slab_kpos(c & 15));
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    __half hi, lo;
+                    split_f16(qp[g][k] * qs, hi, lo);
+                    sts16(qb_s + g * kQbRow + col, hi);
+                    sts16(qb_s + (G + g) * kQbRow + col, lo);
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) base[g] = kvc_warp_sum(base[g]);
+            __syncwarp();
+            const uint32_t bit0 = (kofs + K_HDR) * 8, slot = smem_u32(kring + sl * stage_k);
+            Cursor2 cc[2];
+            cursor2_init(cc[0], slot, bit0 + iA - cA);
+            cursor2_init(cc[1], slot, bit0 + totA + iB - cB);
+            const uint32_t p0A = cc[0].p, p0B = cc[1].p;
+            float d[4][4];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) d[mt][0] = d[mt][1] = d[mt][2] = d[mt][3] = 0.f;
+            // 8 slabs of 16 channels: decode 8 pair steps of both slices (codes
+            // packed 4 per register, one STS.128 per slice), then 4 MMAs over the
+            // 64 tokens with f16 A fragments made from the u8 tile
+            auto kstep = [&](auto ksc) {
+                constexpr int kst = decltype(ksc)::value;
+                uint32_t ra[4], rb[4], ta = 0, tb = 0;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    if ((8 * kst + t) % 5 == 0) {
+                        cursor2_reload(cc[0]);
+                        cursor2_reload(cc[1]);
+                    }
+                    uint32_t eA = lds32(lut_s + ((cc[0].hi >> 20) << 2));
+                    cc[0].hi = __funnelshift_l(cc[0].lo, cc[0].hi, eA);
+                    cc[0].lo = __funnelshift_l(0u, cc[0].lo, eA);
+                    cc[0].p += eA;
+                    uint32_t eB = lds32(lut_s + ((cc[1].hi >> 20) << 2));
+                    cc[1].hi = __funnelshift_l(cc[1].lo, cc[1].hi, eB);
+                    cc[1].lo = __funnelshift_l(0u, cc[1].lo, eB);
+                    cc[1].p += eB;
+                    if (t & 1) {
+                        ra[t >> 1] = __byte_perm(ta, eA, 0x7632);
+                        rb[t >> 1] = __byte_perm(tb, eB, 0x7632);
+                    } else {
+                        ta = eA;
+                        tb = eB;
+                    }
+                }
+                sts128(rowA_k, ra[0], ra[1], ra[2], ra[3]);
+                sts128(rowB_k, rb[0], rb[1], rb[2], rb[3]);
+                __syncwarp();
+                uint32_t b0 = 0, b1 = 0;
+                if (gid < 2 * G) {
+                    const uint32_t ba = qb_s + gid * kQbRow + (16 * kst + 2 * tig) * 2;
+                    b0 = lds32m(ba);
+                    b1 = lds32m(ba + 16);
+                }
+#pragma unroll
+                for (int hlf = 0; hlf < 2; ++hlf) {
+                    uint32_t x0, x1, x2, x3;  // tokens 32hlf + 8i + g: codes 4t..4t+3
+                    ldsm_x4(a_ld + hlf * 32 * kMmRow, x0, x1, x2, x3);
+                    {
+                        const uint32_t a[4] = {u8x2_f16x2<0x5140>(x0), u8x2_f16x2<0x5140>(x1),
+                                               u8x2_f16x2<0x5342>(x0), u8x2_f16x2<0x5342>(x1)};
+                        mma_f16_16816(d[2 * hlf], a, b0, b1);
+                    }
+                    {
+                        const uint32_t a[4] = {u8x2_f16x2<0x5140>(x2), u8x2_f16x2<0x5140>(x3),
+                                               u8x2_f16x2<0x5342>(x2), u8x2_f16x2<0x5342>(x3)};
+                        mma_f16_16816(d[2 * hlf + 1], a, b0, b1);
+                    }
+                }
+                __syncwarp();
+            };
+            kstep(std::integral_constant<int, 0>());
+            kstep(std::integral_constant<int, 1>());
+            kstep(std::integral_constant<int, 2>());
+            kstep(std::integral_constant<int, 3>());
+            kstep(std::integral_constant<int, 4>());
+            kstep(std::integral_constant<int, 5>());
+            kstep(std::integral_constant<int, 6>());
+            kstep(std::integral_constant<int, 7>());
+            bad |= (((cc[0].p - p0A) & 0xFFFFu) != cA) | (((cc[1].p - p0B) & 0xFFFFu) != cB);
+            // S[tok][n]: hi column g + lo column G + g (xor G/2 lanes away)
+            const float inv_qs = ldexpf(1.f, -e);
+            float sv[4][4];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    sv[mt][r] = d[mt][r] + __shfl_xor_sync(0xffffffffu, d[mt][r], G / 2);
+            mbar_wait(&sempty[sl], (u & 1) ^ 1);
+            if (tig < G / 2) {
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int g = 2 * tig + c;
+                    float bg = base[0];
+#pragma unroll
+                    for (int gg = 1; gg < G; ++gg) bg = g == gg ? base[gg] : bg;
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) {
+                        sring[(sl * G + g) * BS + 16 * mt + gid] = (sv[mt][c] * inv_qs + bg) * sm_scale;
+                        sring[(sl * G + g) * BS + 16 * mt + gid + 8] =
+                            (sv[mt][2 + c] * inv_qs + bg) * sm_scale;
+                    }
+                }
+            }
+            mbar_arrive(&sfull[sl]);
+            __syncwarp();
+            if (lane == 0 && j + 2 < n) issue(false, j + 2);
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) kvc_set_err(err, KVC_ERR_CODEC);
+        __syncthreads();
+        __syncthreads();
+        return;
+    }
+
+    // ======== V warp: softmax, codes tile -> O^T += V^T . W on tensor cores ========
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegVm));
+    if (lane == 0) {
+        if (n > 0) issue(true, 0);
+        if (VS == 2 && n > 1) issue(true, 1);
+    }
+    float m[G], lsum[G], wm[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        m[g] = -INFINITY;
+        lsum[g] = wm[g] = 0.f;
+    }
+    // acc[s]: O^T rows (channels 16s + 2gid, 16s + 2gid + 1) x columns n = 2tig, 2tig+1
+    float acc[8][4];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) acc[s][0] = acc[s][1] = acc[s][2] = acc[s][3] = 0.f;
+    const uint32_t lut_s = smem_u32(s_lutV), wb_s = smem_u32(wb);
+    // ldmatrix x4 .trans over tokens 0-31 / 32-63 of the slab tile (row = token)
+    const uint32_t a_ldv = smem_u32(vbuf) + lane * kMmRow;
+    mbar_wait(s_lbar, 0);
+    uint32_t vofs_next = n > 0 ? sd.v_offsets[(long)first * H + h] & 15u : 0u;
+    for (int j = 0; j < n; ++j) {
+        const int u = j >> 1, sl = j & 1;
+        const uint32_t vofs_cur = vofs_next;
+        if (j + 1 < n) vofs_next = sd.v_offsets[(long)(first + NP * (j + 1)) * H + h] & 15u;
+        mbar_wait(&sfull[sl], u & 1);
+        float pA[G], pB[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            pA[g] = sring[(sl * G + g) * BS + lane];
+            pB[g] = sring[(sl * G + g) * BS + lane + 32];
+        }
+        mbar_arrive(&sempty[sl]);
+        float alpha[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const float bm = kvc_warp_max(fmaxf(pA[g], pB[g]));
+            alpha[g] = 1.f;
+            if (bm > m[g]) {
+                alpha[g] = exp2f(m[g] - bm);
+                lsum[g] *= alpha[g];
+                wm[g] *= alpha[g];
+                m[g] = bm;
+            }
+            pA[g] = exp2f(pA[g] - m[g]);
+            pB[g] = exp2f(pB[g] - m[g]);
+            lsum[g] += pA[g] + pB[g];
+        }
+        {   // rescale the accumulators: column n = 2tig + c belongs to member n % G
+            float a0 = alpha[0], a1 = alpha[1 % G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                a0 = (2 * tig) % G == g ? alpha[g] : a0;
+                a1 = (2 * tig + 1) % G == g ? alpha[g] : a1;
+            }
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                acc[s][0] *= a0; acc[s][1] *= a1; acc[s][2] *= a0; acc[s][3] *= a1;
+            }
+        }
+        const int vsl = VS == 2 ? sl : 0;
+        mbar_wait(&vfull[vsl], VS == 2 ? (u & 1) : (j & 1));
+        const uint32_t vofs = vofs_cur;
+        const uint8_t *vs = vring + vsl * stage_v + vofs;
+        const uint32_t cA = lds_u16(vs + 6 + 2 * lane), cB = lds_u16(vs + 6 + 2 * (lane + 32));
+        const uint32_t iA = kvc_warp_incl_scan(cA, lane);
+        const uint32_t totA = __shfl_sync(0xffffffffu, iA, 31);
+        const uint32_t iB = kvc_warp_incl_scan(cB, lane);
+        const float scA = lds_f32_a2(vs + 6 + 2 * BS + 8 * lane + 4);
+        const float scB = lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32) + 4);
+        const float mnA = lds_f32_a2(vs + 6 + 2 * BS + 8 * lane);
+        const float mnB = lds_f32_a2(vs + 6 + 2 * BS + 8 * (lane + 32));
+        // W = p scale per token and member, power-of-two scaled, f16 hi / lo rows
+        float amax = 0.f;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            wm[g] = fmaf(pA[g], mnA, fmaf(pB[g], mnB, wm[g]));
+            pA[g] *= scA;
+            pB[g] *= scB;
+            amax = fmaxf(amax, fmaxf(fabsf(pA[g]), fabsf(pB[g])));
+        }
+        const int e = pow2_exp(kvc_warp_max(amax));
+        const float ws = ldexpf(1.f, e), inv_ws = ldexpf(1.f, -e);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            __half hi, lo;
+            split_f16(pA[g] * ws, hi, lo);
+            sts16(wb_s + g * kWbRow + 2 * lane, hi);
+            sts16(wb_s + (G + g) * kWbRow + 2 * lane, lo);
+            split_f16(pB[g] * ws, hi, lo);
+            sts16(wb_s + g * kWbRow + 2 * (lane + 32), hi);
+            sts16(wb_s + (G + g) * kWbRow + 2 * (lane + 32), lo);
+        }
+        __syncwarp();
+        uint32_t bw0[4], bw1[4];  // B fragments of W for the 4 token k-steps
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            bw0[k] = bw1[k] = 0;
+            if (gid < 2 * G) {
+                const uint32_t ba = wb_s + gid * kWbRow + (16 * k + 2 * tig) * 2;
+                bw0[k] = lds32m(ba);
+                bw1[k] = lds32m(ba + 16);
+            }
+        }
+        const uint32_t bit0 = (vofs + V_HDR) * 8, slot = smem_u32(vring + vsl * stage_v);
+        Cursor2 cc[2];
+        cursor2_init(cc[0], slot, bit0 + iA - cA);
+        cursor2_init(cc[1], slot, bit0 + totA + iB - cB);
+        const uint32_t p0A = cc[0].p, p0B = cc[1].p;
+        auto slab = [&](auto ssc) {
+            constexpr int s = decltype(ssc)::value;
+            uint32_t ra[4], rb[4], ta = 0, tb = 0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                if ((8 * s + t) % 5 == 0) {
+                    cursor2_reload(cc[0]);
+                    cursor2_reload(cc[1]);
+                }
+                const uint32_t eA = lds32(lut_s + (((cc[0].hi >> 18) ^ (cc[0].hi >> 25)) & 0x3FFCu));
+                cc[0].hi = __funnelshift_l(cc[0].lo, cc[0].hi, eA);
+                cc[0].lo = __funnelshift_l(0u, cc[0].lo, eA);
+                cc[0].p += eA;
+                const uint32_t eB = lds32(lut_s + (((cc[1].hi >> 18) ^ (cc[1].hi >> 25)) & 0x3FFCu));
+                cc[1].hi = __funnelshift_l(cc[1].lo, cc[1].hi, eB);
+                cc[1].lo = __funnelshift_l(0u, cc[1].lo, eB);
+                cc[1].p += eB;
+                if (t & 1) {
+                    ra[t >> 1] = __byte_perm(ta, eA, 0x7632);
+                    rb[t >> 1] = __byte_perm(tb, eB, 0x7632);
+                } else {
+                    ta = eA;
+                    tb = eB;
+                }
+            }
+            sts128(rowA_v, ra[0], ra[1], ra[2], ra[3]);
+            sts128(rowB_v, rb[0], rb[1], rb[2], rb[3]);
+            __syncwarp();
+            // V^T A fragments: lane (g, t) holds codes (tok 2t, 2t+1) x (ch 2g, 2g+1)
+            // per 8-token matrix; rows g / g+8 of the m-tile = channels 2g / 2g+1
+            float dd[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int hlf = 0; hlf < 2; ++hlf) {
+                uint32_t x0, x1, x2, x3;
+                ldsm_x4_t(a_ldv + hlf * 32 * kMmRow, x0, x1, x2, x3);
+                {
+                    const uint32_t a[4] = {u8x2_f16x2<0x5240>(x0), u8x2_f16x2<0x5341>(x0),
+                                           u8x2_f16x2<0x5240>(x1), u8x2_f16x2<0x5341>(x1)};
+                    mma_f16_16816(dd, a, bw0[2 * hlf], bw1[2 * hlf]);
+                }
+                {
+                    const uint32_t a[4] = {u8x2_f16x2<0x5240>(x2), u8x2_f16x2<0x5341>(x2),
+                                           u8x2_f16x2<0x5240>(x3), u8x2_f16x2<0x5341>(x3)};
+                    mma_f16_16816(dd, a, bw0[2 * hlf + 1], bw1[2 * hlf + 1]);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[s][r] = fmaf(dd[r], inv_ws, acc[s][r]);
+            __syncwarp();
+        };
+        slab(std::integral_constant<int, 0>());
+        slab(std::integral_constant<int, 1>());
+        slab(std::integral_constant<int, 2>());
+        slab(std::integral_constant<int, 3>());
+        slab(std::integral_constant<int, 4>());
+        slab(std::integral_constant<int, 5>());
+        slab(std::integral_constant<int, 6>());
+        slab(std::integral_constant<int, 7>());
+        bad |= (((cc[0].p - p0A) & 0xFFFFu) != cA) | (((cc[1].p - p0B) & 0xFFFFu) != cB);
+        __syncwarp();
+        if (VS == 1 && lane == 0 && j + 1 < n) issue(true, j + 1);  // slot consumed
+        if (VS == 2 && lane == 0 && j + 2 < n) issue(true, j + 2);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) kvc_set_err(err, KVC_ERR_CODEC);
+    __syncthreads();  // K warps done: their region is scratch
+    Partial *wp = reinterpret_cast<Partial *>(smem + pair * per_pair);  // G partials per pair
+    // columns: hi n = g (lanes tig < G/2), lo n = G + g (xor G/2 lanes away)
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[s][r] += __shfl_xor_sync(0xffffffffu, acc[s][r], G / 2);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const float l = kvc_warp_sum(lsum[g]), w2 = kvc_warp_sum(wm[g]);
+        if (tig == g / 2) {
+            const int c = g & 1;
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                wp[g].o[16 * s + 2 * gid] = acc[s][c] + w2;
+                wp[g].o[16 * s + 2 * gid + 1] = acc[s][2 + c] + w2;
+            }
+        }
+        if (lane == 0) {
+            wp[g].m = m[g];
+            wp[g].l = l;
+        }
+    }
+    __syncthreads();
+    if (pair == 0) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float M = -INFINITY;
+            for (int w = 0; w < NP; ++w)
+                M = fmaxf(M, reinterpret_cast<const Partial *>(smem + w * per_pair)[g].m);
+            float L = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int w = 0; w < NP; ++w) {
+                const Partial *pw = reinterpret_cast<const Partial *>(smem + w * per_pair) + g;
+                const float sc = (pw->m == -INFINITY) ? 0.f : exp2f(pw->m - M);
+                L += pw->l * sc;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) o[k] += pw->o[lane + 32 * k] * sc;
+            }
+            Partial *dst = partial + ((long)sidx * H * G + (long)h * G + g) * n_splits + split;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst->o[lane + 32 * k] = o[k];
+            if (lane == 0) {
+                dst->m = M;
+                dst->l = L;
+            }
+        }
+    }
+}
+
 // Merge split partials + the f32 buffered tokens (attention.py:103-107,
 // :160-164) into out = O / L; also writes buffered scores when requested.
 __global__ void __launch_bounds__(128)
@@ -1562,6 +2085,222 @@ dense_attn_kernel(const __half *__restrict__ K, const __half *__restrict__ V, in
                 dst->m = M;
                 dst->l = L;
             }
+        }
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Uncompressed fp16 GQA decode attention on tensor cores (comparator, G > 1):
+// flash-decoding with mma.sync m16n8k16.  Per warp, 32-token tiles of K and V
+// stream HBM -> shared memory with cp.async (3 stages, rows padded to 272 B
+// so ldmatrix is conflict-free).  S = Q.K^T with Q as the A operand: rows
+// 0..G-1 hold f16(q'), rows G..2G-1 the f16 remainder q' - f16(q') (q'
+// scaled by a power of two into f16 range), so one MMA computes both halves
+// of a 22-bit-accurate product; O = P.V with P split the same way (P as A,
+// from the S accumulators; V^T fragments by ldmatrix.trans).  Online softmax
+// in the log2 domain; split partials -> dense_combine_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kDmNW = 4, kDmTile = 32, kDmStages = 3, kDmRow = 272;
+constexpr int kDmTileBytes = kDmTile * kDmRow;
+constexpr size_t kDmSmem = (size_t)kDmNW * kDmStages * 2 * kDmTileBytes;
+
+template <int G>
+__global__ void __launch_bounds__(kDmNW * 32, 1)
+dense_attn_mma_kernel(const __half *__restrict__ K, const __half *__restrict__ V, int H, long ctx,
+                      const float *__restrict__ q, Partial *__restrict__ partial,
+                      long tok_per_split, int n_splits) {
+    static_assert(G == 2 || G == 4 || G == 8, "GQA group");
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int split = blockIdx.x, h = blockIdx.y, sidx = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const long base = ((long)sidx * H + h) * ctx * D;
+    const __half *Kh = K + base, *Vh = V + base;
+    const uint32_t wbuf = smem_u32(smem) + warp * kDmStages * 2 * kDmTileBytes;
+    const long t_begin = (long)split * tok_per_split;
+    const long t_end = min(ctx, t_begin + tok_per_split);
+    const long first = t_begin + (long)warp * kDmTile, stride = (long)kDmNW * kDmTile;
+    const int n_tiles = first < t_end ? (int)((t_end - first + stride - 1) / stride) : 0;
+
+    // q' = q * log2e / sqrt(D), scaled by qs = 2^e so max |q' qs| < 2^14
+    const float *qg = q + ((long)sidx * H * G + (long)h * G) * D;
+    const float sm_scale = kLog2e / sqrtf((float)D);
+    float amax = 0.f;
+    for (int i = lane; i < G * D; i += 32) amax = fmaxf(amax, fabsf(qg[i]) * sm_scale);
+    amax = kvc_warp_max(amax);
+    const int e = amax > 0.f ? 14 - ilogbf(amax) - 1 : 0;
+    const float qs = ldexpf(1.f, e), inv_qs = ldexpf(1.f, -e);
+    // A fragments of Q for the 8 k-steps: row r -> member r % G, hi if r < G
+    uint32_t aq[8][4];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int row = gid + ((r & 1) ? 8 : 0);
+            const int col = 16 * ks + 2 * tig + ((r & 2) ? 8 : 0);
+            uint32_t v = 0;
+            if (row < 2 * G) {
+                const float *qm = qg + (row % G) * D + col;
+                __half h0, l0, h1, l1;
+                split_f16(qm[0] * sm_scale * qs, h0, l0);
+                split_f16(qm[1] * sm_scale * qs, h1, l1);
+                v = row < G ? pack_half2(h0, h1) : pack_half2(l0, l1);
+            }
+            aq[ks][r] = v;
+        }
+    }
+    auto load_tile = [&](int i) {
+        if (i < n_tiles) {
+            const long t0 = first + (long)i * stride;
+            const uint32_t slot = wbuf + (i % kDmStages) * 2 * kDmTileBytes;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int c = lane + 32 * j, row = c >> 4, c16 = c & 15;
+                const long t = t0 + row;
+                const bool ok = t < t_end;
+                const long tt = ok ? t : t_begin;
+                cp_async16(slot + row * kDmRow + c16 * 16, Kh + tt * D + c16 * 8, ok ? 16u : 0u);
+                cp_async16(slot + kDmTileBytes + row * kDmRow + c16 * 16, Vh + tt * D + c16 * 8,
+                           ok ? 16u : 0u);
+            }
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int i = 0; i < kDmStages - 1; ++i) load_tile(i);
+
+    float m_run = -INFINITY, l_run = 0.f;
+    float o[16][4];
+#pragma unroll
+    for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    const bool row_live = gid < 2 * G;
+    for (int i = 0; i < n_tiles; ++i) {
+        cp_async_wait<kDmStages - 2>();
+        __syncwarp();
+        const long t0 = first + (long)i * stride;
+        const uint32_t sk = wbuf + (i % kDmStages) * 2 * kDmTileBytes, sv = sk + kDmTileBytes;
+        // ---- S = Q K^T: 4 n-tiles of 8 tokens
+        float sc[4][4];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+#pragma unroll
+            for (int np = 0; np < 2; ++np) {
+                const int mi = lane >> 3;
+                const int tok = 16 * np + (mi >> 1) * 8 + (lane & 7);
+                const int ch = 16 * ks + (mi & 1) * 8;
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(sk + tok * kDmRow + ch * 2, b0, b1, b2, b3);
+                mma_f16_16816(sc[2 * np], aq[ks], b0, b1);
+                mma_f16_16816(sc[2 * np + 1], aq[ks], b2, b3);
+            }
+        }
+        // ---- full scores of this thread's member: hi rows + lo rows
+        float s[4][2];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                float v = sc[n][c];
+                if (G == 8) v += sc[n][2 + c];
+                else v += __shfl_xor_sync(0xffffffffu, v, 4 * G);
+                const long t = t0 + 8 * n + 2 * tig + c;
+                s[n][c] = (t < t_end && row_live) ? v * inv_qs : -INFINITY;
+            }
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int n = 0; n < 4; ++n) mx = fmaxf(mx, fmaxf(s[n][0], s[n][1]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_run, mx);
+        if (m_new > m_run) {
+            const float alpha = exp2f(m_run - m_new);
+            l_run *= alpha;
+#pragma unroll
+            for (int n = 0; n < 16; ++n) {
+                o[n][0] *= alpha; o[n][1] *= alpha; o[n][2] *= alpha; o[n][3] *= alpha;
+            }
+            m_run = m_new;
+        }
+        // ---- P as the A operand (x 2^12, hi rows / lo rows)
+        uint32_t ap[2][4];
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                const int n = 2 * kk + hf;
+                __half h0, l0, h1, l1;
+                float p0 = row_live ? exp2f(s[n][0] - m_run) : 0.f;
+                float p1 = row_live ? exp2f(s[n][1] - m_run) : 0.f;
+                l_run += p0 + p1;
+                split_f16(p0 * 4096.f, h0, l0);
+                split_f16(p1 * 4096.f, h1, l1);
+                const uint32_t hv = pack_half2(h0, h1), lv = pack_half2(l0, l1);
+                ap[kk][2 * hf] = gid < G ? hv : (row_live ? lv : 0u);
+                ap[kk][2 * hf + 1] = G == 8 ? lv : 0u;  // rows gid+8: lo rows when G = 8
+            }
+        }
+        // ---- O += P V: 16 n-tiles of 8 channels, 2 k-steps of 16 tokens
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+            const uint32_t a[4] = {ap[kk][0], ap[kk][1], ap[kk][2], ap[kk][3]};
+#pragma unroll
+            for (int np = 0; np < 8; ++np) {
+                const int mi = lane >> 3;
+                const int tok = 16 * kk + (mi & 1) * 8 + (lane & 7);
+                const int ch = 16 * np + (mi >> 1) * 8;
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(sv + tok * kDmRow + ch * 2, b0, b1, b2, b3);
+                mma_f16_16816(o[2 * np], a, b0, b1);
+                mma_f16_16816(o[2 * np + 1], a, b2, b3);
+            }
+        }
+        __syncwarp();
+        load_tile(i + kDmStages - 1);
+    }
+    cp_async_wait<0>();
+    // ---- per-warp result of member gid (< G): hi + lo rows, x 2^-12
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    __syncthreads();  // all warps done with their tile buffers: reuse as scratch
+    float *sh_o = reinterpret_cast<float *>(smem);               // [NW][G][D]
+    float *sh_ml = sh_o + kDmNW * G * D;                          // [NW][G][2]
+#pragma unroll
+    for (int n = 0; n < 16; ++n) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            float v = o[n][c];
+            if (G == 8) v += o[n][2 + c];
+            else v += __shfl_xor_sync(0xffffffffu, v, 4 * G);
+            if (gid < G) sh_o[(warp * G + gid) * D + 8 * n + 2 * tig + c] = v * (1.f / 4096.f);
+        }
+    }
+    if (gid < G && tig == 0) {
+        sh_ml[(warp * G + gid) * 2] = m_run;
+        sh_ml[(warp * G + gid) * 2 + 1] = l_run;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < G * D; idx += blockDim.x) {
+        const int g = idx / D, c = idx % D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kDmNW; ++w) M = fmaxf(M, sh_ml[(w * G + g) * 2]);
+        float L = 0.f, O = 0.f;
+#pragma unroll
+        for (int w = 0; w < kDmNW; ++w) {
+            const float mw = sh_ml[(w * G + g) * 2];
+            const float sc = mw == -INFINITY ? 0.f : exp2f(mw - M);
+            L += sh_ml[(w * G + g) * 2 + 1] * sc;
+            O += sh_o[(w * G + g) * D + c] * sc;
+        }
+        Partial *dst = partial + ((long)sidx * H * G + (long)h * G + g) * n_splits + split;
+        dst->o[c] = O;
+        if (c == 0) {
+            dst->m = M;
+            dst->l = L;
         }
     }
 }
@@ -1853,6 +2592,45 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         if (sizeof(Partial) * (size_t)n_seqs * H * group * g_splits > workspace_bytes)
             return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
         dim3 g3((unsigned)(g_splits * H * n_seqs));
+        // tensor-core decode-once kernel (default); KVC_GQA_IMPL=ffma selects the
+        // CUDA-core one
+        const char *gimpl = getenv("KVC_GQA_IMPL");
+        if (!(gimpl && gimpl[0] == 'f')) {
+            int mnp = 8, mvs = 1;
+            const char *mnpenv = getenv("KVC_GQA_PAIRS");
+            if (mnpenv && (mnpenv[0] == '4' || mnpenv[0] == '6')) mnp = mnpenv[0] - '0';
+            while (mnp > 4 && (size_t)mnp * gqa_mma_per_pair(stage_k, stage_v, group, mvs) > lim) mnp -= 2;
+            const size_t m_smem = (size_t)mnp * gqa_mma_per_pair(stage_k, stage_v, group, mvs);
+            if (m_smem + 2 * 16384 + 256 > 227 * 1024)
+                return kvc_fail(KVC_ERR_CONFIG, "block extents too large for GQA staging");
+            int m_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H, 1, mnp);
+            const long m_max_sp =
+                (long)(workspace_bytes / (sizeof(Partial) * (size_t)n_seqs * H * group));
+            const SplitPlan m_plan = pick_split_plan(max_chunks, (long)n_seqs * H, 1, mnp,
+                                                     (int)std::min(m_max_sp, 1L << 20), m_cps, 0.5);
+            if (sizeof(Partial) * (size_t)n_seqs * H * group * m_plan.n > workspace_bytes)
+                return kvc_fail(KVC_ERR_CONFIG, "attention workspace too small");
+            dim3 gm((unsigned)(m_plan.n * H * n_seqs));
+#define KVC_LAUNCH_GQAM(GG, NPP)                                                                   \
+    do {                                                                                           \
+        KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_gqa_mma_kernel<GG, NPP, 1>,                     \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m_smem)); \
+        fused_attn_gqa_mma_kernel<GG, NPP, 1><<<gm, NPP * 64, m_smem, s>>>(                          \
+            seqs_dev, H, q_dev, part, m_plan, stage_k, stage_v, err_dev);                          \
+    } while (0)
+            if (group == 2) {
+                if (mnp >= 8) KVC_LAUNCH_GQAM(2, 8); else if (mnp >= 6) KVC_LAUNCH_GQAM(2, 6); else KVC_LAUNCH_GQAM(2, 4);
+            } else {
+                if (mnp >= 8) KVC_LAUNCH_GQAM(4, 8); else if (mnp >= 6) KVC_LAUNCH_GQAM(4, 6); else KVC_LAUNCH_GQAM(4, 4);
+            }
+#undef KVC_LAUNCH_GQAM
+            int st = kvc_check_launch("fused_attn_gqa_mma_kernel");
+            if (st) return st;
+            combine_kernel<<<dim3(1, H * group, n_seqs), 128, 0, s>>>(seqs_dev, H, bs, q_dev, part,
+                                                                      m_plan.n, out_dev, nullptr, 0,
+                                                                      group);
+            return kvc_check_launch("combine_kernel");
+        }
 #define KVC_LAUNCH_GQA(GG, NPP, VSS)                                                                   \
     do {                                                                                            \
         KVC_CUDA_TRY(cudaFuncSetAttribute(fused_attn_gqa_kernel<GG, NPP, VSS>,                         \
@@ -1950,7 +2728,7 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
 
 extern "C" size_t kvc_dense_workspace_bytes(int n_seqs, int H, int group, int D_, long ctx) {
     (void)D_;
-    long splits = (ctx + 255) / 256;
+    long splits = (ctx + 127) / 128 + 1;  // >= either kernel's split count
     return sizeof(Partial) * (size_t)n_seqs * H * (size_t)(group > 0 ? group : 1) * (size_t)splits;
 }
 
@@ -1964,6 +2742,37 @@ extern "C" int kvc_dense_attention_f16(const void *k_dev, const void *v_dev, int
     if (ctx < 1) return kvc_fail(KVC_ERR_CONFIG, "empty context");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     long nh = (long)n_seqs * H;
+    const char *ffma_env = getenv("KVC_DENSE_FFMA");  // the older FFMA kernel for G > 1
+    if (group > 1 && !(ffma_env && ffma_env[0] == '1')) {
+        // tensor-core kernel: one 4-warp CTA per SM (204 KB of cp.async stages);
+        // ~4 waves of splits, tokens per split a multiple of 4 warps x 32
+        long splits = (4L * num_sms() + nh - 1) / nh;
+        long tps = (ctx + splits - 1) / splits;
+        tps = (tps + kDmNW * kDmTile - 1) / (kDmNW * kDmTile) * (kDmNW * kDmTile);
+        splits = (ctx + tps - 1) / tps;
+        if (sizeof(Partial) * (size_t)nh * group * splits > workspace_bytes)
+            return kvc_fail(KVC_ERR_CONFIG, "dense workspace too small");
+        Partial *part = static_cast<Partial *>(workspace_dev);
+        const __half *k = static_cast<const __half *>(k_dev), *v = static_cast<const __half *>(v_dev);
+        dim3 grid((unsigned)splits, H, n_seqs);
+#define KVC_LAUNCH_DM(GG)                                                                        \
+    do {                                                                                         \
+        KVC_CUDA_TRY(cudaFuncSetAttribute(dense_attn_mma_kernel<GG>,                              \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,           \
+                                          (int)kDmSmem));                                        \
+        dense_attn_mma_kernel<GG><<<grid, kDmNW * 32, kDmSmem, s>>>(k, v, H, ctx, q_dev, part,   \
+                                                                    tps, (int)splits);           \
+    } while (0)
+        if (group == 2) KVC_LAUNCH_DM(2);
+        else if (group == 4) KVC_LAUNCH_DM(4);
+        else KVC_LAUNCH_DM(8);
+#undef KVC_LAUNCH_DM
+        int st = kvc_check_launch("dense_attn_mma_kernel");
+        if (st) return st;
+        dense_combine_kernel<<<dim3(1, H * group, n_seqs), 128, 0, s>>>(H * group, part, (int)splits,
+                                                                         out_dev);
+        return kvc_check_launch("dense_combine_kernel");
+    }
     long target = (long)num_sms() * 8 * 2;
     long splits = (target + nh - 1) / nh;
     long tps = (ctx + splits - 1) / splits;
