@@ -276,10 +276,10 @@ def _flash_attn_reference(B, T, H, G, dev):
 
 
 def build_cache(kv, torch, layers, batch, ctx, heads_total, head_base, heads_local, device,
-                group=None):
+                group=None, rel_k=None, rel_v=None):
     """Prefill layers x batch compressed states (this rank's head shard)."""
-    cfg_k = kv.QuantConfig(kv.QuantMode.K_BLOCK)
-    cfg_v = kv.QuantConfig(kv.QuantMode.V_TOKEN)
+    cfg_k = kv.QuantConfig(kv.QuantMode.K_BLOCK, rel_quant_scale=rel_k)
+    cfg_v = kv.QuantConfig(kv.QuantMode.V_TOKEN, rel_quant_scale=rel_v)
     kbuf = torch.empty((batch, ctx, heads_total, 128), dtype=torch.float16, device=device)
     vbuf = torch.empty_like(kbuf)
     states = []

@@ -78,6 +78,10 @@ typedef struct {
      * i ^ ((i >> 7) & 31), so the bank of a lookup is window bits 7-11 XOR
      * bits 0-4 (fewer shared-memory bank conflicts for short V pairs). */
     uint32_t fetch_lut_x[1 << KVC_LUT_BITS];
+    /* Single-symbol fused-fetch LUT over 13-bit windows for books whose
+     * longest code is <= 13 bits (used when it is 13): entry = float bits of
+     * the symbol | length (low 4 bits); zero when max_len > 13. */
+    uint32_t lut13[1 << 13];
     uint32_t first_code[33];        /* canonical decode (lengths > 12)         */
     uint32_t count[33];
     uint32_t first_index[33];

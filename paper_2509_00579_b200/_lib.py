@@ -50,6 +50,7 @@ class CodebookTables(ctypes.Structure):
                 ("lut", ctypes.c_uint32 * (1 << LUT_BITS)),
                 ("fetch_lut", ctypes.c_uint32 * (1 << LUT_BITS)),
                 ("fetch_lut_x", ctypes.c_uint32 * (1 << LUT_BITS)),
+                ("lut13", ctypes.c_uint32 * (1 << 13)),
                 ("first_code", ctypes.c_uint32 * 33),
                 ("count", ctypes.c_uint32 * 33), ("first_index", ctypes.c_uint32 * 33),
                 ("sorted_symbols", ctypes.c_uint8 * 256), ("fetch_syms", ctypes.c_int32),

@@ -3,7 +3,7 @@
 ``attention_step`` runs the single-pass fused sm_100a kernel (Huffman decode
 -> dequantise -> q.K^T -> online softmax -> .V per context split, then a
 combine that also folds in the f32 buffered tokens) whenever the shape is
-covered (head_dim 128, block_size 64, codes <= 12 bits); other shapes run the
+covered (head_dim 128, block_size 64, codes <= 13 bits); other shapes run the
 shape-generic decode-in-the-dot-product kernels (kvc_k_scores ->
 kvc_softmax_rows -> kvc_v_output).  Both are CUDA; there is no CPU path.
 ``attention_batched`` is the batch entry point (many sequences, one launch).
@@ -114,12 +114,18 @@ def softmax_rows(logits) -> torch.Tensor:
     return x
 
 
+FUSED_MAX_CODE_LENGTH = 13  # pair LUT (<= 6), 12-bit and 13-bit single-symbol LUTs
+
+
+def _state_fused_ok(s: LayerCacheState) -> bool:
+    return max(s.k_codebook.max_code_length, s.v_codebook.max_code_length) <= FUSED_MAX_CODE_LENGTH
+
+
 def _fused_supported(states: Sequence[LayerCacheState]) -> bool:
     s0 = states[0]
     if s0.head_dim != 128 or s0.cfg_k.block_size != 64 or s0.cfg_k.buffer_size >= 1024:
         return False
-    return all(max(s.k_codebook.max_code_length, s.v_codebook.max_code_length) <= 12
-               for s in states)
+    return all(_state_fused_ok(s) for s in states)
 
 
 _default_desc_cache = _BatchDesc()
@@ -165,6 +171,33 @@ def attention_batched(states: Sequence[LayerCacheState], q: torch.Tensor,
     _check_batch(states, q, 1, out)
     B = len(states)
     s0 = states[0]
+    # a batch mixing books the fused kernel covers (codes <= 13 bits) with
+    # longer ones (very fine scales): fused launch for the former, the generic
+    # kernels for the rest, instead of the whole batch on the generic path
+    ok = [_state_fused_ok(s) for s in states]
+    shape_ok = s0.head_dim == 128 and s0.cfg_k.block_size == 64 and s0.cfg_k.buffer_size < 1024
+    if shape_ok and any(ok) and not all(ok):
+        cache = desc_cache if desc_cache is not None else _BatchDesc()
+        if getattr(cache, "split", None) is None:
+            cache.split = (_BatchDesc(), _BatchDesc())
+        if out is None:
+            out = torch.empty((B, s0.head_num, s0.head_dim), dtype=torch.float32, device=s0.device)
+        max_ctx = max(s.context_len for s in states)
+        scores = (torch.zeros((B, s0.head_num, max_ctx), dtype=torch.float32, device=s0.device)
+                  if want_scores else None)
+        errs = []
+        for sub_ok, sub_cache in ((True, cache.split[0]), (False, cache.split[1])):
+            idx = [i for i in range(B) if ok[i] == sub_ok]
+            it = torch.tensor(idx, device=s0.device)
+            o, sc, e = attention_batched([states[i] for i in idx], q.index_select(0, it).contiguous(),
+                                         want_scores=want_scores, desc_cache=sub_cache,
+                                         want_err=True)
+            out.index_copy_(0, it, o)
+            if want_scores:
+                scores[it, :, : sc.shape[-1]] = sc
+            errs.append(e)
+        err = torch.maximum(errs[0], errs[1])
+        return out, scores, (err if want_err else None)
     H, D, bs = s0.head_num, s0.head_dim, s0.cfg_k.block_size
     dev = s0.device
     lib = _lib.lib()

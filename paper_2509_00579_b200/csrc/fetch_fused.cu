@@ -152,7 +152,10 @@ __device__ __forceinline__ float sym_hi_byte(uint32_t e, uint32_t sel) {
 // ---------------------------------------------------------------------------
 template <int MODE>
 struct Dec {
-    static constexpr int kLutWords = MODE == 0 ? 64 * 32 : (1 << KVC_LUT_BITS);
+    // MODE 5: single-symbol LUT over 13-bit windows (books with 13-bit codes)
+    static constexpr int kLutWords = MODE == 0 ? 64 * 32 : (MODE == 5 ? 8192 : (1 << KVC_LUT_BITS));
+    static constexpr int kSymBits = MODE == 5 ? 13 : 12;   // single-symbol window
+    static constexpr int kReload = MODE == 5 ? 4 : 5;      // symbols per 64-bit window
     static constexpr bool kPair = MODE == 1 || MODE == 3 || MODE == 4;  // the 4096-entry pair LUT (TMA-loaded)
     // symbols decodable from one 32-bit window; MODE 0 uses 4 (not 5) so the
     // reload cadence divides the unrolled loop (24 of 32 bits)
@@ -512,6 +515,16 @@ __device__ __forceinline__ uint32_t cursor2_sym(Cursor2 &c, uint32_t lane_s) {
     c.p += e;
     return e;
 }
+// single-symbol step on the 4096- / 8192-entry LUT (MODE 2 / 5: entry =
+// float(sym) bits | len, codes <= 12 / 13 bits): 5 / 4 steps per 64-bit window
+template <int BITS = 12>
+__device__ __forceinline__ float cursor2_sym12(Cursor2 &c, uint32_t lut_s) {
+    const uint32_t e = lds32(lut_s + ((c.hi >> (32 - BITS)) << 2));
+    c.hi = __funnelshift_l(c.lo, c.hi, e);
+    c.lo = __funnelshift_l(0u, c.lo, e);
+    c.p += e;
+    return __uint_as_float(e & ~15u);
+}
 __device__ __forceinline__ float2 cursor2_pair(Cursor2 &c, uint32_t lut_s) {
     const uint32_t e = lds32(lut_s + ((c.hi >> 20) << 2));
     c.hi = __funnelshift_l(c.lo, c.hi, e);
@@ -689,8 +702,10 @@ __global__ void __launch_bounds__(kThreadsWS, 2)
 fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *__restrict__ q,
                      float *__restrict__ scores, long ctx_stride, Partial *__restrict__ partial,
                      const SplitPlan plan, int stage_k, int stage_v, int *err) {
-    __shared__ __align__(128) uint32_t s_lutK[Dec<MODE>::kLutWords];
-    __shared__ __align__(128) uint32_t s_lutV[Dec<VMODE>::kLutWords];
+    // the 13-bit LUTs (MODE 5, 2 x 32 KB) exceed the static shared-memory
+    // limit: they live in the dynamic region, after the pairs' staging
+    __shared__ __align__(128) uint32_t s_lutK_st[MODE == 5 ? 1 : Dec<MODE>::kLutWords];
+    __shared__ __align__(128) uint32_t s_lutV_st[VMODE == 5 ? 1 : Dec<VMODE>::kLutWords];
     __shared__ uint64_t s_lbar[1];
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
@@ -698,6 +713,10 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
     const bool is_v = warp >= WS_PAIRS;
     const int pair = warp & (WS_PAIRS - 1);
     const int per_pair = 2 * (stage_k + stage_v) + 1024 + 64;
+    uint32_t *s_lutK = MODE == 5 ? reinterpret_cast<uint32_t *>(smem + WS_PAIRS * per_pair) : s_lutK_st;
+    uint32_t *s_lutV = VMODE == 5 ? reinterpret_cast<uint32_t *>(smem + WS_PAIRS * per_pair) +
+                                        (MODE == 5 ? 8192 : 0)
+                                  : s_lutV_st;
     uint8_t *pb = smem + pair * per_pair;
     uint8_t *kring = pb, *vring = pb + 2 * stage_k;
     float *qf = reinterpret_cast<float *>(pb + 2 * (stage_k + stage_v));
@@ -719,15 +738,21 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
         mbar_init(&sempty[0], 32);
         mbar_init(&sempty[1], 32);
     }
-    constexpr bool kPK = Dec<MODE>::kPair, kPV = Dec<VMODE>::kPair;
+    // pair LUTs and the 13-bit LUTs come by TMA from the codebook tables
+    constexpr bool kPK = Dec<MODE>::kPair || MODE == 5, kPV = Dec<VMODE>::kPair || VMODE == 5;
     constexpr bool kTma = kPK || kPV;
     if (kTma && threadIdx.x == 0) mbar_init(s_lbar, 1);
     fence_mbar_init();
     __syncthreads();
     if (kTma && threadIdx.x == 0) {
-        mbar_expect_tx(s_lbar, ((int)kPK + (int)kPV) * (4u << KVC_LUT_BITS));
-        if (kPK) tma_load_1d(s_lutK, sd.k_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
-        if (kPV) tma_load_1d(s_lutV, VMODE == 1 ? sd.v_cb->fetch_lut_x : sd.v_cb->fetch_lut, 4u << KVC_LUT_BITS, s_lbar);
+        mbar_expect_tx(s_lbar, (kPK ? 4u * Dec<MODE>::kLutWords : 0u) +
+                                   (kPV ? 4u * Dec<VMODE>::kLutWords : 0u));
+        if (kPK)
+            tma_load_1d(s_lutK, MODE == 5 ? sd.k_cb->lut13 : sd.k_cb->fetch_lut,
+                        4u * Dec<MODE>::kLutWords, s_lbar);
+        if (kPV)
+            tma_load_1d(s_lutV, VMODE == 5 ? sd.v_cb->lut13 : (VMODE == 1 ? sd.v_cb->fetch_lut_x : sd.v_cb->fetch_lut),
+                        4u * Dec<VMODE>::kLutWords, s_lbar);
     }
     if (!kPK) build_lut<MODE>(s_lutK, sd.k_cb);
     if (!kPV) build_lut<VMODE>(s_lutV, sd.v_cb);
@@ -838,6 +863,43 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
                 steps(60, std::integral_constant<int, 4>());
                 cur[0].p = c2c[0].p;
                 cur[1].p = c2c[1].p;
+            } else if (MODE == 2 || MODE == 5) {
+                // codes <= 12 (13) bits: single-symbol lookups on 64-bit windows, one
+                // reload per 5 (4) symbols (was a 32-bit window reloaded every 2)
+                constexpr int R = Dec<MODE>::kReload, SB = Dec<MODE>::kSymBits;
+                Cursor2 c2c[2];
+                cursor2_init(c2c[0], slot, bit0 + iA - cA);
+                cursor2_init(c2c[1], slot, bit0 + totA + iB - cB);
+                auto grp = [&](int c2base, auto np) {
+                    float fa = 0.f, fb = 0.f;
+#pragma unroll
+                    for (int t = 0; t < 2 * decltype(np)::value; ++t) {
+                        if (t % R == 0) {
+                            cursor2_reload(c2c[0]);
+                            cursor2_reload(c2c[1]);
+                        }
+                        const float xa = cursor2_sym12<SB>(c2c[0], lut_s);
+                        const float xb = cursor2_sym12<SB>(c2c[1], lut_s);
+                        if (t & 1) {
+                            const float2 q2 = lds64f(qf_s + 8 * (c2base + t / 2));
+                            sA2 = __ffma2_rn(make_float2(fa, xa), q2, sA2);
+                            sB2 = __ffma2_rn(make_float2(fb, xb), q2, sB2);
+                        } else {
+                            fa = xa;
+                            fb = xb;
+                        }
+                    }
+                };
+                if (R == 5) {  // groups of 10 symbols (2 reloads), a tail of 8
+#pragma unroll 1
+                    for (int g = 0; g < 12; ++g) grp(5 * g, std::integral_constant<int, 5>());
+                    grp(60, std::integral_constant<int, 4>());
+                } else {       // groups of 8 symbols (2 reloads)
+#pragma unroll 1
+                    for (int g = 0; g < 16; ++g) grp(4 * g, std::integral_constant<int, 4>());
+                }
+                cur[0].p = c2c[0].p;
+                cur[1].p = c2c[1].p;
             } else {
                 decode_two<MODE, false>(cur, lut_s, lane_s, [&](int c2, float2 fA, float2 fB) {
                     const float2 q2 = lds64f(qf_s + 8 * c2);
@@ -943,6 +1005,32 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
                                          aA2, acc[c2]);
                     acc[c2] = __ffma2_rn(make_float2(__uint_as_float(b0 & ~15u), __uint_as_float(b1 & ~15u)),
                                          aB2, acc[c2]);
+                }
+            }
+            cur[0].p = c2c[0].p;
+            cur[1].p = c2c[1].p;
+        } else if (VMODE == 2 || VMODE == 5) {
+            // codes <= 12 (13) bits: single-symbol lookups, 64-bit windows, a
+            // reload per 5 (4) symbols
+            constexpr int R = Dec<VMODE>::kReload, SB = Dec<VMODE>::kSymBits;
+            Cursor2 c2c[2];
+            cursor2_init(c2c[0], slot, bit0 + iA - cA);
+            cursor2_init(c2c[1], slot, bit0 + totA + iB - cB);
+            float fa = 0.f, fb = 0.f;
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                if (t % R == 0) {
+                    cursor2_reload(c2c[0]);
+                    cursor2_reload(c2c[1]);
+                }
+                const float xa = cursor2_sym12<SB>(c2c[0], lut_s);
+                const float xb = cursor2_sym12<SB>(c2c[1], lut_s);
+                if (t & 1) {
+                    acc[t / 2] = __ffma2_rn(make_float2(fa, xa), aA2, acc[t / 2]);
+                    acc[t / 2] = __ffma2_rn(make_float2(fb, xb), aB2, acc[t / 2]);
+                } else {
+                    fa = xa;
+                    fb = xb;
                 }
             }
             cur[0].p = c2c[0].p;
@@ -2539,7 +2627,7 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         stage_k = seqs_host[i].stage_bytes_k > stage_k ? seqs_host[i].stage_bytes_k : stage_k;
         stage_v = seqs_host[i].stage_bytes_v > stage_v ? seqs_host[i].stage_bytes_v : stage_v;
     }
-    const bool fused_ok = D_ == D && bs == BS && max_len <= 12 && max_len >= 1;
+    const bool fused_ok = D_ == D && bs == BS && max_len <= 13 && max_len >= 1;
     if (!fused_ok) return kvc_fail(KVC_ERR_CONFIG, "shape not covered by the fused kernel");
     stage_k = (stage_k + 15) & ~15;
     stage_v = (stage_v + 15) & ~15;
@@ -2550,7 +2638,7 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
     Partial *part = static_cast<Partial *>(workspace_dev);
     // decoder: pair LUT12 when every code is <= 6 bits (measured fastest, see
     // profiles/), else single-symbol LUT12; env KVC_FUSED_MODE=0|1 overrides.
-    int mode = max_len <= 6 ? 1 : 2;
+    int mode = max_len <= 6 ? 1 : (max_len <= 12 ? 2 : 5);
     if (max_len <= 6) {
         const char *env = getenv("KVC_FUSED_MODE");
         if (env && (env[0] == '0' || env[0] == '1')) mode = env[0] - '0';
@@ -2558,7 +2646,7 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
     const size_t per_warp = 2 * (size_t)(stage_k + stage_v) + D * 4 + 64;
     size_t smem = NW * per_warp;  // dynamic part (LUTs are static)
     if (smem < NW * sizeof(Partial)) smem = NW * sizeof(Partial);
-    const size_t lut_bytes = mode == 0 ? 2 * 8192 : 2 * 16384;
+    const size_t lut_bytes = mode == 0 ? 2 * 8192 : (mode == 5 ? 2 * 32768 : 2 * 16384);
     if (smem + lut_bytes + 256 > 227 * 1024)
         return kvc_fail(KVC_ERR_CONFIG, "block extents too large for staging");
     dim3 grid(n_splits, H, n_seqs);
@@ -2653,8 +2741,9 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
     }
     const char *impl = getenv("KVC_FUSED_IMPL");
     const bool use_ws = !(impl && impl[0] == 'i');
-    const size_t ws_smem = WS_PAIRS * (2 * (size_t)(stage_k + stage_v) + 1024 + 64);
-    if (use_ws && max_chunks > 0 && ws_smem + lut_bytes + 256 <= 227 * 1024) {
+    const size_t ws_smem = WS_PAIRS * (2 * (size_t)(stage_k + stage_v) + 1024 + 64) +
+                           (mode == 5 ? lut_bytes : 0);  // the 13-bit LUTs are dynamic
+    if (use_ws && max_chunks > 0 && ws_smem + (mode == 5 ? 0 : lut_bytes) + 256 <= 227 * 1024) {
         int ws_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H);
         if (const char *cenv = getenv("KVC_FUSED_CPS")) {  // experiments: chunks per split
             const int v = atoi(cenv);
@@ -2689,7 +2778,8 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
             seqs_dev, H, q_dev, scores_dev, ctx_stride, part, ws_plan, stage_k, stage_v,     \
             err_dev);                                                                        \
     } while (0)
-        if (mode == 2) KVC_LAUNCH_WS(2, 2);
+        if (mode == 5) KVC_LAUNCH_WS(5, 5);
+        else if (mode == 2) KVC_LAUNCH_WS(2, 2);
         else if (mode == 0) KVC_LAUNCH_WS(0, 0);
         else if (kmode == 3 && vmode == 3) KVC_LAUNCH_WS(3, 3);
         else if (vmode == 0) KVC_LAUNCH_WS(1, 0);
@@ -2703,6 +2793,7 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
                                                           out_dev, scores_dev, ctx_stride);
         return kvc_check_launch("combine_kernel");
     }
+    if (mode == 5) return kvc_fail(KVC_ERR_CONFIG, "13-bit codes: block extents too large for staging");
     if (max_chunks > 0) {
 #define KVC_LAUNCH_FUSED(M)                                                                   \
     do {                                                                                      \

@@ -142,6 +142,10 @@ extern "C" int kvc_codebook_build_tables(const uint8_t *lengths, kvc_codebook_de
         t->sorted_symbols[0] = (uint8_t)only;
         t->sorted_symbols[1] = (uint8_t)only;
         build_fetch_lut(t);
+        float f = (float)only;
+        uint32_t fb;
+        std::memcpy(&fb, &f, 4);
+        for (int i = 0; i < (1 << 13); ++i) t->lut13[i] = fb | 1u;
         return KVC_OK;
     }
     uint64_t kraft = 0;
@@ -175,5 +179,16 @@ extern "C" int kvc_codebook_build_tables(const uint8_t *lengths, kvc_codebook_de
         for (uint32_t i = lo; i < hi; ++i) t->lut[i] = (uint32_t)s | ((uint32_t)l << 8);
     }
     build_fetch_lut(t);
+    if (max_len <= 13) {  // the fused single-symbol fetch over 13-bit windows (fine scales)
+        for (int s = 0; s < 256; ++s) {
+            const int l = lengths[s];
+            if (!l) continue;
+            float f = (float)s;
+            uint32_t fb;
+            std::memcpy(&fb, &f, 4);
+            const uint32_t lo = t->words[s] << (13 - l), hi = (t->words[s] + 1) << (13 - l);
+            for (uint32_t i = lo; i < hi; ++i) t->lut13[i] = fb | (uint32_t)l;
+        }
+    }
     return KVC_OK;
 }

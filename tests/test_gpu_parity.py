@@ -700,3 +700,63 @@ def test_quantize_block_k_channel(kv):
             assert np.array_equal(q.unit_scales.cpu().numpy(), sc)
     with pytest.raises(kv.ConfigError):
         kv.quantize_block(kin[:bs, 0], kv.QuantMode.K_CHANNEL, cfg, 0, 0, H)
+
+
+def _lengths_with_max(n_symbols, target, hk_fn):
+    """Code lengths (reference Huffman, host builder) of a decaying histogram over
+    n_symbols whose longest code is exactly `target` bits."""
+    from paper_2509_00579_b200 import CodebookError, build_codebook
+    for r in np.linspace(0.95, 0.3, 600):
+        h = np.zeros(256, np.uint64)
+        h[:n_symbols] = np.maximum(1, (1e9 * r ** np.arange(n_symbols))).astype(np.uint64)
+        h = hk_fn(h)
+        try:
+            ln = build_codebook(h).code_lengths
+        except CodebookError:
+            continue
+        if int(ln.max()) == target:
+            return ln
+    raise AssertionError("no histogram found")
+
+
+@pytest.mark.parametrize("target", [12, 13])
+def test_fused_single_symbol_long_codes_match_oracle(kv, target):
+    """Codes of 12 and 13 bits on the hot shape (D 128, bs 64): the fused
+    fetch's single-symbol decoders (12-bit LUT, MODE 2; 13-bit LUT, MODE 5)
+    against the oracle with the same injected codebooks, ragged tail
+    included; and a batch mixing 13-bit books with a 14-bit one (the latter on
+    the generic kernels) equals per-state attention_step."""
+    import oracle
+    from paper_2509_00579_b200 import codebook_from_lengths
+    H, ctx = 2, 64 * 9 + 23
+    rel_k, rel_v = 0.05, 0.02        # K codes 0..20, V codes 0..50
+    kl = _lengths_with_max(21, target, lambda h: h)
+    vl = _lengths_with_max(51, target, lambda h: h)
+    k = kv.generate_synthetic(kv.SyntheticSpec(ctx, H, 128, seed=61)).values.astype(np.float16)
+    v = kv.generate_synthetic(kv.SyntheticSpec(ctx, H, 128, seed=62)).values.astype(np.float16)
+    ck = kv.QuantConfig(kv.QuantMode.K_BLOCK, rel_quant_scale=rel_k)
+    cv = kv.QuantConfig(kv.QuantMode.V_TOKEN, rel_quant_scale=rel_v)
+    st = kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v), ck, cv,
+                                    codebooks=(codebook_from_lengths(kl), codebook_from_lengths(vl)))
+    assert max(st.k_codebook.max_code_length, st.v_codebook.max_code_length) == target
+    o = oracle.OracleState.prefill(k, v, rel_k=rel_k, rel_v=rel_v, codebooks=(kl, vl))
+    assert st.k_arena.snapshot() == o.arena_bytes("k")
+    assert st.v_arena.snapshot() == o.arena_bytes("v")
+    q = np.random.default_rng(7).standard_normal((H, 128), dtype=np.float32)
+    res = kv.attention_step(st, q)
+    ref_out, ref_scores = o.attention_step(q)
+    assert max_relative_error(res.out.cpu().numpy(), ref_out) <= 1e-5
+    assert max_relative_error(res.scores.cpu().numpy(), ref_scores) <= 1e-5
+    if target == 13:
+        import torch
+        l14 = _lengths_with_max(51, 14, lambda h: h)
+        st14 = kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v), ck, cv,
+                                          codebooks=(codebook_from_lengths(kl),
+                                                     codebook_from_lengths(l14)))
+        batch = [st, st14, st]
+        qb = torch.from_numpy(np.stack([q, q * 0.5, -q])).cuda()
+        out, _, err = kv.attention_batched(batch, qb)
+        assert int(err.item()) == 0
+        for i, s in enumerate(batch):
+            ref = kv.attention_step(s, qb[i]).out
+            assert max_relative_error(out[i].cpu().numpy(), ref.cpu().numpy()) <= 1e-6

@@ -29,15 +29,23 @@ def main():
     ap.add_argument("--ctx", type=int, default=None)
     ap.add_argument("--heads", type=int, default=None)
     ap.add_argument("--variants", default="base")
+    ap.add_argument("--rel-k", type=str, default=None, help="float, or 1/255")
+    ap.add_argument("--rel-v", type=str, default=None)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--check", action="store_true", help="compare every variant's output with base")
     a = ap.parse_args()
+    frac = lambda x: None if x is None else (1.0 / 255.0 if x == "1/255" else float(x))
+    a.rel_k, a.rel_v = frac(a.rel_k), frac(a.rel_v)
     p = dict(bench.PRESETS[a.config])
     B = a.batch or p["batch"]
     T = a.ctx or p["ctx"]
     H, G = a.heads or p["heads"], p["group"]
     dev = torch.device("cuda", 0)
-    states, _, _ = bench.build_cache(kv, torch, 1, B, T, H, 0, H, dev)
+    states, _, _ = bench.build_cache(kv, torch, 1, B, T, H, 0, H, dev, rel_k=a.rel_k,
+                                     rel_v=a.rel_v)
+    s0 = states[0][0]
+    print(f"k max len {s0.k_codebook.max_code_length}, v max len {s0.v_codebook.max_code_length}, "
+          f"stage bytes {s0.stage_bytes()}", flush=True)
     row = states[0]
     comp = sum(s.k_arena.size_bytes + s.v_arena.size_bytes for s in row)
     eq = 2 * T * H * 128 * 2 * B
