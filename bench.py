@@ -514,6 +514,38 @@ def main():
     lay_ms = float(np.mean([ev[l].elapsed_time(ev[l + 1]) for ev in lev for l in range(L)]))
     hbm_peak, peak_kind = _peaks()
     ach = float(np.mean(comp_bytes_layer)) / (lay_ms * 1e-3) / 1e9
+    # N > 1: the realistic decode gathers each layer's head outputs before the
+    # next layer (its q depends on them); the headline step gathers once per
+    # step.  Both are reported.
+    layer_gather = None
+    if world > 1:
+        gl = torch.empty((world, B, hl * G, 128), device=device)
+
+        def step_layer_gather():
+            for layer in range(L):
+                layer_call(layer)
+                if share:
+                    dist.all_gather(list(gl.unbind(0)), outs[layer])
+                else:
+                    dist.all_gather_into_tensor(gl, outs[layer])
+
+        for _ in range(2):
+            step_layer_gather()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_layer_gather()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        lg_ms = e0.elapsed_time(e1) / args.steps
+        t = torch.tensor([lg_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        lg_ms = float(t.item())
+        layer_gather = {"ms_per_step": round(lg_ms, 4),
+                        "value": round(eq_bytes_step * world / (lg_ms * 1e-3) / 1e9, 2),
+                        "unit": UNIT, "note": "all-gather of each layer's head outputs after "
+                                              "that layer's attention (max over ranks)"}
     # the paper's two kernel comparisons (reference
     # bench.py:165-177, :297-321) on one (seq, layer) state of this workload:
     # the fused pass vs the multistage pass (decode -> dequantise -> dense
@@ -654,6 +686,9 @@ def main():
             line["paper_comparisons"] = paper
         if streaming:
             line["streaming"] = streaming
+        if layer_gather:
+            line["per_layer_gather"] = layer_gather
+            line["config"]["gather"] = "headline: one all-gather per step; per_layer_gather: one per layer"
         if args.config == 5:
             line["quant_sweep"] = quant_sweep(kv, torch, device, T, H, B)
         print(json.dumps(line), flush=True)

@@ -49,6 +49,17 @@ class _HistRing:
 _HIST_RING = None
 
 
+class _Done:
+    """An already-completed event (host data that is ready)."""
+
+    @staticmethod
+    def synchronize() -> None:
+        return None
+
+
+_DONE = _Done()
+
+
 def _hist_readback(hist: torch.Tensor):
     global _HIST_RING
     if _HIST_RING is None:
@@ -168,6 +179,23 @@ class LayerCacheState:
         calling prefill() on each item."""
         items = list(items)
         out = []
+        group = kw.get("process_group")
+        if group is not None and kw.get("codebooks") is None and len(items) > 1:
+            # head-sharded prefill: every item's pass A first, then ONE all-reduce
+            # of the stacked [n_items, 2 x 256] histograms (SURVEY §8e), then the
+            # codebook builds and pass B
+            kw1 = dict(kw, process_group=None, _defer_hist=True)
+            begun = [cls._prefill_begin(k, v, cfg_k, cfg_v, **kw1) for k, v in items]
+            hists = torch.stack([c["hist"] for c in begun])
+            torch.distributed.all_reduce(hists, group=group)
+            hh = hists.cpu()  # one readback for the whole batch
+            for c, h in zip(begun, hh.unbind(0)):
+                c["hist_host"], c["ev"] = h, _DONE
+            out = [cls._prefill_finish(c, False) for c in begun]
+            if check:
+                for st in out:
+                    st.check()
+            return out
         nxt = cls._prefill_begin(*items[0], cfg_k, cfg_v, **kw) if items else None
         for i in range(len(items)):
             cur = nxt
@@ -182,7 +210,8 @@ class LayerCacheState:
     @classmethod
     def _prefill_begin(cls, k, v, cfg_k, cfg_v, codebooks=None, k_channel_ranges=None,
                        device=None, process_group=None, head_base: int = 0,
-                       head_total: Optional[int] = None, capacity: Optional[int] = None):
+                       head_total: Optional[int] = None, capacity: Optional[int] = None,
+                       _defer_hist: bool = False):
         """Pass A and every allocation that does not depend on the histogram;
         the histogram is copied to pinned host memory behind an event."""
         kv = k.values if isinstance(k, CacheTensor) else k
@@ -269,7 +298,7 @@ class LayerCacheState:
         pre_ws = (torch.empty(lib.kvc_store_workspace_bytes(n_chunks, H, D, bs), dtype=torch.uint8,
                               device=kt.device) if n_full and fused else None)
         hist_host = ev = None
-        if codebooks is None:
+        if codebooks is None and not _defer_hist:
             if process_group is not None:
                 torch.distributed.all_reduce(hist, group=process_group)
             hist_host, ev = _hist_readback(hist)
@@ -277,7 +306,7 @@ class LayerCacheState:
                     k_channel_ranges=k_channel_ranges, head_base=head_base,
                     head_total=head_total, capacity=capacity, src_dtype=src_dtype, ctx=ctx,
                     H=H, D=D, bs=bs, n_chunks=n_chunks, n_full=n_full, fused=fused,
-                    hist_host=hist_host, ev=ev, blk_hist=blk_hist, blk_codes=blk_codes,
+                    hist=hist, hist_host=hist_host, ev=ev, blk_hist=blk_hist, blk_codes=blk_codes,
                     kcodes=kcodes, kmetas=kmetas, vcodes=vcodes, vmetas=vmetas, pre=pre,
                     pre_ws=pre_ws)
 
