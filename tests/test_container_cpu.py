@@ -40,10 +40,31 @@ def test_bad_magic_and_short_file(tmp_path):
         read_header(p)
 
 
-def test_arena_counters_from_blocks():
-    """Counters rebuilt from block headers equal the reference's running totals."""
-    from paper_2509_00579_b200.container import _arena_counters
+def test_cursor_bounds_and_config_codes():
+    """The bounds-checked reader and the config / dtype code tables."""
+    import struct
+    from paper_2509_00579_b200 import ContainerFormatError, QuantConfig, QuantMode
+    from paper_2509_00579_b200.container import (_QCFG, _Cursor, _config_fields, _config_from,
+                                                 _dtype_code)
+    cur = _Cursor(b"\x01\x02\x03")
+    assert bytes(cur.take(2, "x")) == b"\x01\x02"
+    with pytest.raises(ContainerFormatError):
+        cur.take(2, "x")
+    for cfg in (QuantConfig(QuantMode.K_BLOCK), QuantConfig(QuantMode.K_CHANNEL, 8, 0.3, 16),
+                QuantConfig(QuantMode.V_TOKEN, 64, 1 / 255)):
+        raw = _QCFG.pack(*_config_fields(cfg))
+        assert _config_from(_QCFG.unpack(raw)) == cfg
+    with pytest.raises(ContainerFormatError):
+        _config_from((7, 64, 128, 0.05))
+    assert _dtype_code(np.float16) == 0 and _dtype_code(np.float32) == 1
+    with pytest.raises(ContainerFormatError):
+        _dtype_code(np.float64)
+
+
+def test_truncated_reference_file(tmp_path):
+    from paper_2509_00579_b200 import ContainerFormatError, read_header
     g = load("c_fp16_d128")
-    c = _arena_counters(g["fin_k_arena"].tobytes(), g["fin_k_offsets"], 128)
-    assert [c.payload_bits, c.payload_bytes] == g["fin_counters"][3:5].tolist()
-    assert c.cursor == g["fin_k_arena"].size
+    p = tmp_path / "t.kvcz"
+    p.write_bytes(g["kvcz"].tobytes()[:40])
+    with pytest.raises(ContainerFormatError):
+        read_header(p)

@@ -327,6 +327,25 @@ def test_container_bytes_match_reference(kv, case, tmp_path):
     assert p2.read_bytes() == g["kvcz"].tobytes()
 
 
+def test_container_rejects_corruption(kv, tmp_path):
+    """A block header disagreeing with its extent (validated on the device by
+    kvc_arena_restore), trailing bytes and a truncated arena raise
+    ContainerFormatError (the reference's container.py:175-212 checks)."""
+    g = load("c_fp16_d128")
+    raw = bytearray(g["kvcz"].tobytes())
+    arena = g["fin_k_arena"].tobytes()
+    at = bytes(raw).find(arena)
+    assert at > 0
+    bad = bytearray(raw)
+    bad[at + 4] ^= 0x01  # first K block: n_slices 64 -> 65
+    cases = {"header": bytes(bad), "trailing": bytes(raw) + b"\0", "truncated": bytes(raw[:-9])}
+    for name, blob in cases.items():
+        p = tmp_path / f"{name}.kvcz"
+        p.write_bytes(blob)
+        with pytest.raises(kv.ContainerFormatError):
+            kv.load_state(p)
+
+
 @pytest.mark.parametrize("group,T", [(2, 3000), (4, 3000), (8, 3000), (4, 33001)])
 def test_dense_fp16_gqa(kv, group, T):
     """The tensor-core GQA comparator (dense_attn_mma_kernel: f16 hi/lo split
