@@ -54,7 +54,10 @@ def full(path):
                   "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
                   "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
                   "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
-                  "smsp__issue_active.avg.pct_of_peak_sustained_active"):
+                  "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                  "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                  "gpu__time_duration.sum", "launch__registers_per_thread",
+                  "sm__warps_active.avg.pct_of_peak_sustained_active"):
             if m in hdr:
                 i = hdr.index(m)
                 res[m] = f"{vals[i]} {units[i]}"
