@@ -332,13 +332,17 @@ class DeviceArena:
         self._bound += worst_bytes
         if n_blocks:
             self._ext_worst = max(self._ext_worst, block_worst or worst_bytes)
-            if self.device.type == "cuda":
-                self._ext_pending = _counters_readback(self._counters)
+            self._ext_stale = True  # a readback starts at the next bound query
 
     def max_extent_bound(self) -> int:
         """An upper bound of every block extent, without synchronising: the
         exact device value once known, else the worst case of the blocks
-        appended since it was last read."""
+        appended since it was last read (and an asynchronous readback of the
+        counters is started)."""
+        if getattr(self, "_ext_stale", False):
+            self._ext_stale = False
+            if self.device.type == "cuda":
+                self._ext_pending = _counters_readback(self._counters)
         if self._ext_pending is not None:
             buf, ev = self._ext_pending
             if ev.query():
@@ -396,6 +400,7 @@ class DeviceArena:
         c = _lib.ArenaCounters.from_buffer_copy(raw)
         self._bound = int(c.cursor)
         self._ext_host, self._ext_worst, self._ext_pending = int(c.max_extent), 0, None
+        self._ext_stale = False
         return c
 
     def check(self, what: str = "arena") -> None:

@@ -560,18 +560,19 @@ class LayerCacheState:
         self.v_arena.check("V arena")
 
     def extents_ready(self) -> bool:
-        """True when no max-extent readback is in flight (non-blocking)."""
+        """True when no max-extent readback is pending or in flight
+        (non-blocking; starts the readback of stale arenas)."""
         for a in (self.k_arena, self.v_arena):
+            a.max_extent_bound()
             if a._ext_pending is not None:
-                a.max_extent_bound()
-                if a._ext_pending is not None:
-                    return False
+                return False
         return True
 
     def settle(self) -> None:
         """Wait for the arenas' in-flight max-extent readbacks (after appends)
         so stage_bytes() is exact again; waits on those copies only."""
         for a in (self.k_arena, self.v_arena):
+            a.max_extent_bound()
             if a._ext_pending is not None:
                 a._ext_pending[1].synchronize()
                 a.max_extent_bound()
