@@ -214,7 +214,7 @@ class DeviceArena:
     # (TMA over-reads of the last block's rounded extent and the decoder's window
     # tail are don't-care bits), so the buffers are allocated without a memset.
     def __init__(self, device, capacity: Optional[int] = None, initial_bytes: int = 1 << 16,
-                 initial_blocks: int = 256):
+                 initial_blocks: int = 256, counters: Optional[torch.Tensor] = None):
         self.device = torch.device(device)
         self.capacity = capacity  # user limit (None = grow on demand)
         alloc = initial_bytes if capacity is None else capacity
@@ -224,8 +224,11 @@ class DeviceArena:
         # allocations otherwise grow the caching allocator's small pool (a
         # cudaMalloc per few states)
         self._offsets, self._off_ext = self._pooled(max(initial_blocks, 1) * 4, torch.int32)
-        self._counters, self._cnt_ext = self._pooled(ctypes.sizeof(_lib.ArenaCounters),
-                                                     torch.uint8, zero=True)
+        if counters is not None:  # zeroed device bytes owned by the caller (the state)
+            self._counters, self._cnt_ext = counters, None
+        else:
+            self._counters, self._cnt_ext = self._pooled(ctypes.sizeof(_lib.ArenaCounters),
+                                                         torch.uint8, zero=True)
         self.n_blocks = 0          # host mirror (deterministic)
         self._bound = 0            # host upper bound on the cursor
         # host mirror of counters.max_extent (the fused fetch sizes its

@@ -119,10 +119,17 @@ class LayerCacheState:
         # arena_bytes: initial allocations sized by the caller (prefill knows a
         # tight bound), so the prefill does not grow 64 KB arenas by a copy
         ka, va = arena_bytes if arena_bytes is not None else (1 << 16, 1 << 16)
+        # the two arenas' counters and the live {n_chunks, buffered} pair share
+        # one zeroed pool allocation (one allocation and one fill per state)
+        if self.device.type == "cuda":
+            small, ext = pooled_zeros((128,), torch.uint8, self.device)
+            weakref.finalize(self, ext.release)
+        else:
+            small = torch.zeros(128, dtype=torch.uint8, device=self.device)
         self.k_arena = DeviceArena(self.device, capacity, initial_bytes=ka,
-                                   initial_blocks=arena_blocks)
+                                   initial_blocks=arena_blocks, counters=small[0:40])
         self.v_arena = DeviceArena(self.device, capacity, initial_bytes=va,
-                                   initial_blocks=arena_blocks)
+                                   initial_blocks=arena_blocks, counters=small[48:88])
         cap = cfg_k.buffer_size + 1
         if _pre is not None:  # allocated by prefill while its pass A ran
             self._k_buffer, self._v_buffer = _pre["k_buffer"], _pre["v_buffer"]
@@ -139,11 +146,7 @@ class LayerCacheState:
         # growing-cache kernels update it, the fetch kernels read it, so the
         # descriptor stays the same across decode steps; the host keeps
         # deterministic mirrors (compressed_tokens, buffered)
-        if self.device.type == "cuda":
-            self._live, ext = pooled_zeros((2,), torch.int32, self.device)
-            weakref.finalize(self, ext.release)
-        else:
-            self._live = torch.zeros(2, dtype=torch.int32, device=self.device)
+        self._live = small[96:104].view(torch.int32)
         self.context_len = 0
         self.compressed_tokens = 0
         self.buffered = 0

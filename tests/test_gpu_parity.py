@@ -778,4 +778,5 @@ def test_fused_single_symbol_long_codes_match_oracle(kv, target):
         assert int(err.item()) == 0
         for i, s in enumerate(batch):
             ref = kv.attention_step(s, qb[i]).out
-            assert max_relative_error(out[i].cpu().numpy(), ref.cpu().numpy()) <= 1e-6
+            # different split plans (batch of 2 vs 1 state): summation order only
+            assert max_relative_error(out[i].cpu().numpy(), ref.cpu().numpy()) <= 1e-5
