@@ -270,6 +270,24 @@ int kvc_dequantize(const kvc_seq_desc *seq_dev, int H, int D, int bs, int which 
                    int n_chunks, float *out_dev, int *err_dev, void *stream);
 
 /* ---------------------------------------------------------------- */
+/* Paged arena memory: CUDA virtual memory      */
+/* ---------------------------------------------------------------- */
+/* An arena reserves a virtual range once and maps fixed-size physical pages
+ * (from a shared pool) as it grows, so it stays contiguous for the kernels
+ * while physical memory is paged and shared between sequences.
+ * kvc_vmm_granularity: the minimum page size; reserve/free_va: a virtual
+ * range; create/release: one physical page; map/unmap: a page at a
+ * page-aligned address (read/write for `device`).  Out of memory ->
+ * KVC_ERR_ARENA_FULL. */
+int kvc_vmm_granularity(int device, size_t *bytes);
+int kvc_vmm_reserve(size_t bytes, uint64_t *va);
+int kvc_vmm_free_va(uint64_t va, size_t bytes);
+int kvc_vmm_create(int device, size_t bytes, uint64_t *handle);
+int kvc_vmm_release(uint64_t handle);
+int kvc_vmm_map(uint64_t va, size_t bytes, uint64_t handle, int device);
+int kvc_vmm_unmap(uint64_t va, size_t bytes);
+
+/* ---------------------------------------------------------------- */
 /* Growing cache, device side — kvcache.py:150-177 without host syncs */
 /* ---------------------------------------------------------------- */
 

@@ -21,6 +21,7 @@ from .errors import (ArenaFullError, CodebookError, CodecError, ConfigError,
                      ContainerFormatError, KvpackError, TensorFormatError)
 from .decode_loop import DecodeLoop
 from .kvcache import LayerCacheState, append_batched
+from .paged import PagedArena, PagePool
 from .metrics import (BenchRow, CompressionStats, SimulationResult, SimulationSettings,
                       collect_stats, config_label, equivalent_decompression_throughput,
                       median_time, run_ratio_sweep, run_simulation, write_csv)

@@ -114,6 +114,13 @@ SIGNATURES = {
     "kvc_buffer_append": (I, [P, I, I, I, I, P, P, I, L, P, P]),
     "kvc_buffer_shift": (I, [P, I, I, I, I, I, I, P]),
     "kvc_set_live": (I, [P, I, I, P]),
+    "kvc_vmm_granularity": (I, [I, P]),
+    "kvc_vmm_reserve": (I, [SZ, P]),
+    "kvc_vmm_free_va": (I, [U64, SZ]),
+    "kvc_vmm_create": (I, [I, SZ, P]),
+    "kvc_vmm_release": (I, [U64]),
+    "kvc_vmm_map": (I, [U64, SZ, U64, I]),
+    "kvc_vmm_unmap": (I, [U64, SZ]),
 }
 
 _lib = None

@@ -311,7 +311,7 @@ class DeviceArena:
         buf = torch.zeros(cap + TMA_SLACK, dtype=torch.uint8)
         buf[:n] = torch.frombuffer(bytearray(data), dtype=torch.uint8) if n else buf[:0]
         self._set_buf(cap + TMA_SLACK)
-        self._buf.copy_(buf)
+        self._buf[: buf.numel()].copy_(buf)
         nb = len(offsets)
         offs = torch.zeros(max(nb, 1), dtype=torch.int32)
         if nb:

@@ -85,7 +85,7 @@ class LayerCacheState:
                  k_channel_ranges=None, device=None, head_base: int = 0,
                  head_total: Optional[int] = None, capacity: Optional[int] = None,
                  arena_bytes: Optional[Tuple[int, int]] = None, arena_blocks: int = 256,
-                 _pre: Optional[dict] = None):
+                 page_pool=None, _pre: Optional[dict] = None):
         if not cfg_k.mode.is_key:
             raise ConfigError("cfg_k must use a K quantization mode")
         if cfg_v.mode is not QuantMode.V_TOKEN:
@@ -126,10 +126,19 @@ class LayerCacheState:
             weakref.finalize(self, ext.release)
         else:
             small = torch.zeros(128, dtype=torch.uint8, device=self.device)
-        self.k_arena = DeviceArena(self.device, capacity, initial_bytes=ka,
-                                   initial_blocks=arena_blocks, counters=small[0:40])
-        self.v_arena = DeviceArena(self.device, capacity, initial_bytes=va,
-                                   initial_blocks=arena_blocks, counters=small[48:88])
+        # page_pool: the arenas map pages of a shared PagePool (paged.py)
+        # instead of slab-pool extents
+        if page_pool is not None:
+            from .paged import PagedArena
+            mk = lambda nb, cnt: PagedArena(self.device, capacity, initial_bytes=nb,  # noqa: E731
+                                            initial_blocks=arena_blocks, counters=cnt,
+                                            pool=page_pool)
+        else:
+            mk = lambda nb, cnt: DeviceArena(self.device, capacity, initial_bytes=nb,  # noqa: E731
+                                             initial_blocks=arena_blocks, counters=cnt)
+        self.page_pool = page_pool
+        self.k_arena = mk(ka, small[0:40])
+        self.v_arena = mk(va, small[48:88])
         cap = cfg_k.buffer_size + 1
         if _pre is not None:  # allocated by prefill while its pass A ran
             self._k_buffer, self._v_buffer = _pre["k_buffer"], _pre["v_buffer"]
@@ -162,14 +171,15 @@ class LayerCacheState:
                 codebooks: Optional[Tuple[HuffmanCodebook, HuffmanCodebook]] = None,
                 k_channel_ranges=None, device=None, process_group=None, head_base: int = 0,
                 head_total: Optional[int] = None, capacity: Optional[int] = None,
-                check: bool = True) -> "LayerCacheState":
+                check: bool = True, page_pool=None) -> "LayerCacheState":
         """kvcache.py:76-145.  k, v: CacheTensor / ndarray / torch tensor
         [ctx, H, D] f16|f32.  With ``process_group`` this rank holds heads
         [head_base, head_base+H) of head_total, and the code histograms are
-        all-reduced so every rank builds the same codebooks."""
+        all-reduced so every rank builds the same codebooks.  With
+        ``page_pool`` (paged.PagePool) the arenas are paged."""
         return cls._prefill_finish(cls._prefill_begin(
             k, v, cfg_k, cfg_v, codebooks, k_channel_ranges, device, process_group, head_base,
-            head_total, capacity), check)
+            head_total, capacity, page_pool=page_pool), check)
 
     @classmethod
     def prefill_many(cls, items, cfg_k: QuantConfig, cfg_v: QuantConfig,
@@ -214,7 +224,7 @@ class LayerCacheState:
     def _prefill_begin(cls, k, v, cfg_k, cfg_v, codebooks=None, k_channel_ranges=None,
                        device=None, process_group=None, head_base: int = 0,
                        head_total: Optional[int] = None, capacity: Optional[int] = None,
-                       _defer_hist: bool = False):
+                       page_pool=None, _defer_hist: bool = False):
         """Pass A and every allocation that does not depend on the histogram;
         the histogram is copied to pinned host memory behind an event."""
         kv = k.values if isinstance(k, CacheTensor) else k
@@ -306,6 +316,7 @@ class LayerCacheState:
                 torch.distributed.all_reduce(hist, group=process_group)
             hist_host, ev = _hist_readback(hist)
         return dict(cls=cls, kt=kt, vt=vt, cfg_k=cfg_k, cfg_v=cfg_v, codebooks=codebooks,
+                    page_pool=page_pool,
                     k_channel_ranges=k_channel_ranges, head_base=head_base,
                     head_total=head_total, capacity=capacity, src_dtype=src_dtype, ctx=ctx,
                     H=H, D=D, bs=bs, n_chunks=n_chunks, n_full=n_full, fused=fused,
@@ -354,7 +365,7 @@ class LayerCacheState:
         st = cls(H, D, cfg_k, cfg_v, k_cb, v_cb, dtype=src_dtype, device=kt.device,
                  head_base=head_base, head_total=head_total, capacity=capacity,
                  k_channel_ranges=k_channel_ranges, arena_bytes=arena_bytes,
-                 arena_blocks=max(nb + 4 * H, 256), _pre=pre)
+                 arena_blocks=max(nb + 4 * H, 256), page_pool=c.get("page_pool"), _pre=pre)
         if pre_ws is not None:
             st._ws = pre_ws
         if n_full:
