@@ -70,3 +70,24 @@ def test_generate_end_to_end():
     assert cache.get_seq_length() in (307, 308)
     for layer in cache.layers:
         layer.check()
+
+
+@pytest.mark.gpu
+def test_generate_bf16_across_an_overflow_event():
+    """A bf16 model (the Llama default): prefill takes bf16 KV (stored as a
+    2-byte original), and 100 decode tokens after a 300-token prompt cross one
+    growing-cache overflow event (44 buffered + 100 > buffer 128)."""
+    from paper_2509_00579_b200.hf_cache import KVCompCache, enable_kvcomp_attention
+    model = _model(2).to(torch.bfloat16)
+    enable_kvcomp_attention(model)
+    ids = torch.randint(0, 512, (2, 300), device="cuda")
+    cache = KVCompCache(model.config)
+    with torch.no_grad():
+        out = model.generate(ids, past_key_values=cache, max_new_tokens=100, do_sample=False)
+    assert out.shape == (2, 400)
+    for layer in cache.layers:
+        layer.check()
+        for st in layer.states:
+            assert st.compressed_tokens == 384 and st.context_len in (399, 400)
+    comp, orig = cache.compression_stats()
+    assert comp < orig
