@@ -58,6 +58,9 @@ PRESETS = {
             workload="cfg3: Llama-3-8B GQA KV (8 KV heads x group 4), fused fetch decode step"),
     5: dict(layers=32, batch=64, ctx=8192, heads=32, group=1,
             workload="cfg5: Llama-2-7B KV batch 64, fused fetch decode step + quant sweep"),
+    4: dict(layers=32, batch=1, ctx=4096, heads=32, group=1,
+            workload="cfg4: Llama-2-7B KV, 4K prefill then 8K decode steps, each appending one "
+                     "token per layer (growing-cache Store) and attending (fused fetch)"),
 }
 SWEEP = [(1 / 255, 1 / 255), (0.01, 0.02), (0.02, 0.05), (0.05, 0.15), (0.06, 0.2),
          (0.1, 0.25), (0.25, 0.5), (0.5, 1.0)]
@@ -333,8 +336,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5],
-                    help="BASELINE config: 2 (default headline), 3 (GQA), 5 (batch-64 + sweep)")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
+                    help="BASELINE config: 2 (default headline), 3 (GQA), 4 (streaming decode), "
+                         "5 (batch-64 + sweep)")
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--ctx", type=int, default=None)
@@ -387,6 +391,11 @@ def main():
     hl = args.heads // world
     hb = rank * hl
     L, B, T, H, G = args.layers, args.batch, args.ctx, args.heads, args.group
+    if args.config == 4:
+        run_streaming_config(args, kv, torch, dist, world, rank, local, device, share, hb, hl)
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     # dense fp16 comparator on one layer (B x hl x T x 128), head-major.  Timed
     # first, on a fresh allocator: measured after the compressed cache and its
@@ -732,6 +741,137 @@ def quant_sweep(kv, torch, device, T, H, B):
                      "fetch_ms": round(ms, 4)})
         del states
     return rows
+
+
+def run_streaming_config(args, kv, torch, dist, world, rank, local, device, share, hb, hl):
+    """BASELINE config 4 as a stream: a Llama-2-7B-shaped cache (32 layers x 32
+    heads x 128) prefilled with 4K tokens, then 8K decode steps, each appending
+    one token per layer through the growing-cache Store and attending with the
+    fused fetch (DecodeLoop, one CUDA graph per inter-event stretch).  value =
+    equivalent fp16 KV bytes attended over the timed steps / device time."""
+    L, B, T, H = args.layers, args.batch, args.ctx, args.heads
+    n_total = args.stream_steps if args.stream_steps != 128 else 8192
+    kv.reserve_arena_pool(int(1.3 * 0.3 * 2 * L * B * (T + n_total) * hl * 128 * 2), device)
+    states, store_times, store_bytes = build_cache(kv, torch, L, B, T, H, hb, hl, device,
+                                                   group=dist.group.WORLD if world > 1 else None)
+    gc.collect()
+    gc.freeze()
+    from paper_2509_00579_b200 import tensor_io
+    pool_n = 256
+    kpool = torch.empty((pool_n, L, B, hl, 128), device=device, dtype=torch.float16)
+    vpool = torch.empty_like(kpool)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(4)
+    for l in range(L):
+        for b in range(B):
+            for pool, seed in ((kpool, l * 8 + b), (vpool, (l * 8 + b) ^ 0x9E3779B9)):
+                spec = kv.SyntheticSpec(1, H, 128, seed=seed)
+                scale = torch.ones((H, 128))
+                scale[torch.from_numpy(tensor_io._outlier_mask(spec))] = spec.outlier_magnitude
+                x = torch.randn((pool_n, hl, 128), generator=gen, device=device)
+                pool[:, l, b] = (x * scale[hb: hb + hl].to(device)).to(torch.float16)
+    kn = torch.empty((L, B, hl, 128), device=device, dtype=torch.float16)
+    vn = torch.empty_like(kn)
+    q = torch.randn((L, B, hl, 128), device=device)
+    outs = torch.empty_like(q)
+    stream = torch.cuda.current_stream()
+    idx = [0]
+
+    def stage():
+        i = idx[0] % pool_n
+        idx[0] += 1
+        kn.copy_(kpool[i])
+        vn.copy_(vpool[i])
+
+    loop = kv.DecodeLoop(states, group=1, use_graph=True)
+    warm = max(args.warmup, 3)
+    for _ in range(warm):
+        stage()
+        loop.step(kn, vn, q, outs)
+    n_timed = n_total - warm
+    ctx0 = states[0][0].context_len
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0 = loop.events
+    with ClockSampler(local) as clk:
+        a.record(stream)
+        for _ in range(n_timed):
+            stage()
+            loop.step(kn, vn, q, outs)
+        b_.record(stream)
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(b_)
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    for row in states:
+        for st in row:
+            st.check()
+    # equivalent fp16 bytes attended: context grows by one token per step
+    tok_sum = sum(ctx0 + 1 + i for i in range(n_timed))
+    eq = 2 * tok_sum * hl * 128 * 2 * L * B * world
+    value = eq / (ms * 1e-3) / 1e9
+    # eager loop over a shorter stretch, for the graph's host-launch saving
+    eager = kv.DecodeLoop(states, group=1, use_graph=False)
+    n_e = min(512, n_timed)
+    torch.cuda.synchronize()
+    a.record(stream)
+    t0 = time.perf_counter()
+    for _ in range(n_e):
+        stage()
+        eager.step(kn, vn, q, outs)
+    b_.record(stream)
+    torch.cuda.synchronize()
+    eager_ms = a.elapsed_time(b_) / n_e
+    eager_host = (time.perf_counter() - t0) * 1e3 / n_e
+    # e2e through the API with host buffers: q in from pinned memory, out back
+    qh = torch.empty_like(q, device="cpu").pin_memory()
+    oh = torch.empty_like(outs, device="cpu").pin_memory()
+    n_x = min(512, n_timed)
+    ctx_x = states[0][0].context_len
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(n_x):
+        q.copy_(qh, non_blocking=True)
+        stage()
+        loop.step(kn, vn, q, outs)
+        oh.copy_(outs, non_blocking=True)
+    b_.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b_) / n_x
+    e2e_eq = 2 * sum(ctx_x + 1 + i for i in range(n_x)) * hl * 128 * 2 * L * B * world
+    ratio = float(np.mean([kv.collect_stats(s).compression_ratio for s in states[0]]))
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": n_timed, "warmup": warm, "ms_per_step": round(ms / n_timed, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u8 Huffman codes -> f32 accumulate",
+            "data": "synthetic (reference generator distribution, device RNG), random q",
+            "config": {"workload": PRESETS[4]["workload"], "layers": L, "batch": B,
+                       "prefill_ctx": T, "appended_tokens": n_total, "kv_heads": H,
+                       "head_dim": 128, "block_size": 64, "buffer": 128,
+                       "parallelism": f"kv-head shard x{world}",
+                       "l2": "compressed cache 0.8-2.3 GB over the stream, > L2 only at the end; "
+                             "every step reads the whole cache"},
+            "tokens_per_s": round(B * n_timed / (ms * 1e-3), 1),
+            "overflow_event_steps": loop.events - ev0,
+            "graph_captures": loop.captures,
+            "eager": {"ms_per_step": round(eager_ms, 4), "host_ms_per_step": round(eager_host, 4),
+                      "steps": n_e},
+            "compression_ratio": round(ratio, 4),
+            "store": {"prefill_gbs": round(store_bytes / float(np.median(store_times)) / 1e9, 3),
+                      "unit": "GB/s fp16 K+V in"},
+            "e2e": {"value": round(e2e_eq / (e2e_ms * n_x * 1e-3) / 1e9, 2), "unit": UNIT,
+                    "ms_per_step": round(e2e_ms, 4), "steps": n_x,
+                    "h2d_bytes_per_step": int(q.numel() * 4),
+                    "d2h_bytes_per_step": int(outs.numel() * 4)},
+            "gpu_launches": int(n_timed * L * 3),
+            "clocks": clk.summary(),
+        }), flush=True)
 
 
 def streaming_block(kv, torch, dist, states, G, q, outs, stream, n_steps, world, device,

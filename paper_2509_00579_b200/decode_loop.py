@@ -117,12 +117,10 @@ class DecodeLoop:
             return out
         io = (k_new.data_ptr(), v_new.data_ptr(), q.data_ptr(), out.data_ptr())
         if self.graph is None or io != self.graph_io:
-            # after an event, stay eager until the arenas' max-extent readbacks
-            # have landed (exact stage sizes without draining the stream)
-            if not all(s.extents_ready() for r in self.states for s in r):
-                self._reserve_workspace()
-                self._eager(k_new, v_new, q, out)
-                return out
+            # re-capture with exact stage sizes: _capture waits for the arenas'
+            # max-extent readbacks (the host is usually far ahead of the device
+            # here, so the wait overlaps queued work; the device idles only
+            # during the capture itself)
             self._capture(k_new, v_new, q, out)
         self.graph.replay()
         for r in self.states:
