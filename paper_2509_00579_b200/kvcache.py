@@ -761,6 +761,8 @@ def append_batched(states, k_rows: torch.Tensor, v_rows: torch.Tensor,
         if (s.head_num, s.head_dim, s.cfg_k.buffer_size, s.device) != (
                 H, D, s0.cfg_k.buffer_size, s0.device):
             raise ConfigError("batched states must share head_num, head_dim, buffer and device")
+    if len(set(map(id, states))) != B:  # one CTA per state advances its live count
+        raise ConfigError("a state appears twice in the batch")
     kd, vd = k_rows, v_rows
     if kd.dtype not in (torch.float16, torch.float32) or kd.dtype != vd.dtype:
         kd, vd = kd.to(torch.float32), vd.to(torch.float32)

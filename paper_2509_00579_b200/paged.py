@@ -128,7 +128,9 @@ class _Mapping:
         return len(self.pages) * self.pool.page_bytes
 
     def close(self) -> None:
-        if self.va:
+        if not self.va:
+            return
+        try:
             if self.pages:
                 torch.cuda.synchronize(self.pool.device)  # no kernel still reads the pages
             self.shrink(0)
@@ -137,7 +139,9 @@ class _Mapping:
                 _lib.lib().kvc_vmm_unmap(self.va, self.pool.page_bytes)
                 self.pool.give(h)
             _lib.lib().kvc_vmm_free_va(self.va, VA_BYTES)
-            self.va = 0
+        except Exception:  # interpreter / CUDA context teardown: the driver reclaims it
+            pass
+        self.va = 0
 
 
 class PagedArena(DeviceArena):
