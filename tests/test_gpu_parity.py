@@ -363,10 +363,13 @@ def test_dense_fp16_gqa(kv, group, T):
     assert max_relative_error(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-5
 
 
-@pytest.mark.parametrize("group", [2, 4, 3])
-def test_fused_gqa_matches_per_member_steps(kv, group):
+@pytest.mark.parametrize("group,impl", [(2, "mma"), (4, "mma"), (3, "mma"), (2, "ffma"),
+                                        (4, "ffma")])
+def test_fused_gqa_matches_per_member_steps(kv, group, impl, monkeypatch):
     """Config-3 style: 2 KV heads x group G; each query head attends its KV head
-    (G = 2, 4: decode-once GQA kernel; G = 3: per-member launches)."""
+    (G = 2, 4: decode-once GQA kernel, tensor-core or CUDA-core; G = 3:
+    per-member launches)."""
+    monkeypatch.setenv("KVC_GQA_IMPL", impl)
     H = 2
     k = kv.generate_synthetic(kv.SyntheticSpec(2000, H, 128, seed=40)).values.astype(np.float16)
     v = kv.generate_synthetic(kv.SyntheticSpec(2000, H, 128, seed=41)).values.astype(np.float16)
@@ -386,9 +389,12 @@ def test_fused_gqa_matches_per_member_steps(kv, group):
                                       r.out.cpu().numpy()) <= 1e-5
 
 
-def test_fused_gqa_ragged_batch_multi_split(kv):
+@pytest.mark.parametrize("impl", ["mma", "ffma"])
+def test_fused_gqa_ragged_batch_multi_split(kv, impl, monkeypatch):
     """Two sequences of different lengths (one with buffered tokens) in one
-    decode-once GQA launch, long enough for several context splits per head."""
+    decode-once GQA launch, long enough for several context splits per head;
+    the tensor-core kernel (default) and the CUDA-core one (KVC_GQA_IMPL=ffma)."""
+    monkeypatch.setenv("KVC_GQA_IMPL", impl)
     H, G = 2, 4
     states, qs = [], []
     for b, (ctx, extra) in enumerate(((9000, 0), (20000, 45))):
