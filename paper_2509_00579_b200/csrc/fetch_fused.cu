@@ -146,6 +146,14 @@ __device__ __forceinline__ float sym_hi_byte(uint32_t e, uint32_t sel) {
 //   MODE 1  shared 4096-entry pair LUT (codes <= 6 bits): one lookup decodes
 //           two symbols; entry = (l0+l1) | s0<<16 | s1<<24.
 //   MODE 2  shared 4096-entry single-symbol LUT (codes <= 12 bits), float|len.
+//   MODE 6  512-entry single-symbol LUT (codes <= 9 bits), float|len, in 16
+//           copies: entry i of copy c at word i*16+c, lane l reads copy l&15,
+//           so only lanes l and l+16 can collide (~2 wavefronts per lookup
+//           instead of ~3.3 for MODE 2's random 12-bit indices).
+//   MODE 7  256-entry single-symbol LUT (codes <= 8 bits) in 32 copies, one
+//           per lane: every lookup is bank-conflict-free.
+//   MODE 8  1024-entry single-symbol LUT (codes <= 10 bits) in 8 copies
+//           (lanes l, l+8, l+16, l+24 share one).
 // In every format the low 4 bits are the bits consumed and bits 4..15 are
 // zero, so `win <<= e` (funnel shift masks to 5 bits) and `p += e` need no
 // field extraction.
@@ -153,9 +161,16 @@ __device__ __forceinline__ float sym_hi_byte(uint32_t e, uint32_t sel) {
 template <int MODE>
 struct Dec {
     // MODE 5: single-symbol LUT over 13-bit windows (books with 13-bit codes)
-    static constexpr int kLutWords = MODE == 0 ? 64 * 32 : (MODE == 5 ? 8192 : (1 << KVC_LUT_BITS));
-    static constexpr int kSymBits = MODE == 5 ? 13 : 12;   // single-symbol window
-    static constexpr int kReload = MODE == 5 ? 4 : 5;      // symbols per 64-bit window
+    static constexpr int kLutWords = MODE == 0 ? 64 * 32 : (MODE >= 5 ? 8192 : (1 << KVC_LUT_BITS));
+    // single-symbol window and symbols per 64-bit window
+    static constexpr int kSymBits =
+        MODE == 5 ? 13 : (MODE == 6 ? 9 : (MODE == 7 ? 8 : (MODE == 8 ? 10 : 12)));
+    static constexpr int kReload =
+        MODE == 5 ? 4 : (MODE == 6 ? 7 : (MODE == 7 ? 8 : (MODE == 8 ? 6 : 5)));
+    static constexpr int kCopies =
+        MODE == 6 ? 16 : (MODE == 7 ? 32 : (MODE == 8 ? 8 : 1));  // lane copies
+    static constexpr bool kDyn = MODE >= 5;  // LUT in the dynamic shared region
+    static constexpr bool kSingle = MODE == 2 || MODE >= 5;
     static constexpr bool kPair = MODE == 1 || MODE == 3 || MODE == 4;  // the 4096-entry pair LUT (TMA-loaded)
     // symbols decodable from one 32-bit window; MODE 0 uses 4 (not 5) so the
     // reload cadence divides the unrolled loop (24 of 32 bits)
@@ -177,6 +192,22 @@ __device__ void build_lut(uint32_t *dst, const kvc_codebook_dev *cb) {
         else if (MODE == 2) e12 = cb->lut[i];
         else { dst[i] = cb->fetch_lut[i & 4095]; continue; }
         dst[i] = __float_as_uint((float)(e12 & 0xFF)) | ((e12 >> 8) & 0xF);
+    }
+}
+
+// MODE 6 / 7 tables: entry i (float(sym) | len, from the 12-bit table's
+// entry i << (12 - BITS): codes are <= BITS bits) in R copies, word i*R + c.
+// A warp loads 32 entries and writes them out with consecutive lanes storing
+// consecutive words.
+template <int BITS, int R>
+__device__ void build_lut_copies(uint32_t *dst, const kvc_codebook_dev *cb) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int kb = 32 * warp; kb < (1 << BITS); kb += 32 * nw) {
+        const uint32_t e12 = cb->lut[(kb + lane) << (12 - BITS)];
+        const uint32_t e = __float_as_uint((float)(e12 & 0xFF)) | ((e12 >> 8) & 0xF);
+#pragma unroll 4
+        for (int i = 0; i < R; ++i)
+            dst[kb * R + 32 * i + lane] = __shfl_sync(0xffffffffu, e, i * (32 / R) + lane / R);
     }
 }
 
@@ -525,6 +556,17 @@ __device__ __forceinline__ float cursor2_sym12(Cursor2 &c, uint32_t lut_s) {
     c.p += e;
     return __uint_as_float(e & ~15u);
 }
+// single-symbol step on a lane-copied LUT (MODE 6 / 7): lane_s = the lane's
+// copy, entry i at lane_s + i * 4R
+template <int BITS, int R>
+__device__ __forceinline__ float cursor2_sym_copy(Cursor2 &c, uint32_t lane_s) {
+    constexpr int kShift = 2 + (R == 32 ? 5 : (R == 16 ? 4 : (R == 8 ? 3 : 0)));
+    const uint32_t e = lds32(lane_s + ((c.hi >> (32 - BITS)) << kShift));
+    c.hi = __funnelshift_l(c.lo, c.hi, e);
+    c.lo = __funnelshift_l(0u, c.lo, e);
+    c.p += e;
+    return __uint_as_float(e & ~15u);
+}
 __device__ __forceinline__ float2 cursor2_pair(Cursor2 &c, uint32_t lut_s) {
     const uint32_t e = lds32(lut_s + ((c.hi >> 20) << 2));
     c.hi = __funnelshift_l(c.lo, c.hi, e);
@@ -704,8 +746,10 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
                      const SplitPlan plan, int stage_k, int stage_v, int *err) {
     // the 13-bit LUTs (MODE 5, 2 x 32 KB) exceed the static shared-memory
     // limit: they live in the dynamic region, after the pairs' staging
-    __shared__ __align__(128) uint32_t s_lutK_st[MODE == 5 ? 1 : Dec<MODE>::kLutWords];
-    __shared__ __align__(128) uint32_t s_lutV_st[VMODE == 5 ? 1 : Dec<VMODE>::kLutWords];
+    // (and MODE 6's lane-private tables, 2 x 32 KB)
+    constexpr bool kDynK = Dec<MODE>::kDyn, kDynV = Dec<VMODE>::kDyn;
+    __shared__ __align__(128) uint32_t s_lutK_st[kDynK ? 1 : Dec<MODE>::kLutWords];
+    __shared__ __align__(128) uint32_t s_lutV_st[kDynV ? 1 : Dec<VMODE>::kLutWords];
     __shared__ uint64_t s_lbar[1];
     extern __shared__ __align__(128) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
@@ -713,10 +757,10 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
     const bool is_v = warp >= WS_PAIRS;
     const int pair = warp & (WS_PAIRS - 1);
     const int per_pair = 2 * (stage_k + stage_v) + 1024 + 64;
-    uint32_t *s_lutK = MODE == 5 ? reinterpret_cast<uint32_t *>(smem + WS_PAIRS * per_pair) : s_lutK_st;
-    uint32_t *s_lutV = VMODE == 5 ? reinterpret_cast<uint32_t *>(smem + WS_PAIRS * per_pair) +
-                                        (MODE == 5 ? 8192 : 0)
-                                  : s_lutV_st;
+    uint32_t *s_lutK = kDynK ? reinterpret_cast<uint32_t *>(smem + WS_PAIRS * per_pair) : s_lutK_st;
+    uint32_t *s_lutV = kDynV ? reinterpret_cast<uint32_t *>(smem + WS_PAIRS * per_pair) +
+                                   (kDynK ? 8192 : 0)
+                             : s_lutV_st;
     uint8_t *pb = smem + pair * per_pair;
     uint8_t *kring = pb, *vring = pb + 2 * stage_k;
     float *qf = reinterpret_cast<float *>(pb + 2 * (stage_k + stage_v));
@@ -754,8 +798,14 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
             tma_load_1d(s_lutV, VMODE == 5 ? sd.v_cb->lut13 : (VMODE == 1 ? sd.v_cb->fetch_lut_x : sd.v_cb->fetch_lut),
                         4u * Dec<VMODE>::kLutWords, s_lbar);
     }
-    if (!kPK) build_lut<MODE>(s_lutK, sd.k_cb);
-    if (!kPV) build_lut<VMODE>(s_lutV, sd.v_cb);
+    if (MODE == 6) build_lut_copies<9, 16>(s_lutK, sd.k_cb);
+    else if (MODE == 7) build_lut_copies<8, 32>(s_lutK, sd.k_cb);
+    else if (MODE == 8) build_lut_copies<10, 8>(s_lutK, sd.k_cb);
+    else if (!kPK) build_lut<MODE>(s_lutK, sd.k_cb);
+    if (VMODE == 6) build_lut_copies<9, 16>(s_lutV, sd.v_cb);
+    else if (VMODE == 7) build_lut_copies<8, 32>(s_lutV, sd.v_cb);
+    else if (VMODE == 8) build_lut_copies<10, 8>(s_lutV, sd.v_cb);
+    else if (!kPV) build_lut<VMODE>(s_lutV, sd.v_cb);
     if (!kPK || !kPV) __syncthreads();
 
     const int c_begin = plan.begin[split];
@@ -900,6 +950,41 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
                 }
                 cur[0].p = c2c[0].p;
                 cur[1].p = c2c[1].p;
+            } else if (MODE == 6 || MODE == 7 || MODE == 8) {
+                // codes <= 9 (8) bits: lane-copied LUT, one reload per 7 (8)
+                // symbols; groups of 2R symbols (2 reloads), R = 7: a tail of 2
+                constexpr int R = Dec<MODE>::kReload, SB = Dec<MODE>::kSymBits,
+                              CP = Dec<MODE>::kCopies;
+                const uint32_t copy_s = lut_s + 4 * (lane & (CP - 1));
+                Cursor2 c2c[2];
+                cursor2_init(c2c[0], slot, bit0 + iA - cA);
+                cursor2_init(c2c[1], slot, bit0 + totA + iB - cB);
+                auto grp = [&](int c2base, auto np) {
+                    float fa = 0.f, fb = 0.f;
+#pragma unroll
+                    for (int t = 0; t < 2 * decltype(np)::value; ++t) {
+                        if (t % R == 0) {
+                            cursor2_reload(c2c[0]);
+                            cursor2_reload(c2c[1]);
+                        }
+                        const float xa = cursor2_sym_copy<SB, CP>(c2c[0], copy_s);
+                        const float xb = cursor2_sym_copy<SB, CP>(c2c[1], copy_s);
+                        if (t & 1) {
+                            const float2 q2 = lds64f(qf_s + 8 * (c2base + t / 2));
+                            sA2 = __ffma2_rn(make_float2(fa, xa), q2, sA2);
+                            sB2 = __ffma2_rn(make_float2(fb, xb), q2, sB2);
+                        } else {
+                            fa = xa;
+                            fb = xb;
+                        }
+                    }
+                };
+                constexpr int NG = D / (2 * R), TAIL = D - NG * 2 * R;
+#pragma unroll 1
+                for (int g = 0; g < NG; ++g) grp(R * g, std::integral_constant<int, R>());
+                if (TAIL) grp(R * NG, std::integral_constant<int, (TAIL > 0 ? TAIL / 2 : 1)>());
+                cur[0].p = c2c[0].p;
+                cur[1].p = c2c[1].p;
             } else {
                 decode_two<MODE, false>(cur, lut_s, lane_s, [&](int c2, float2 fA, float2 fB) {
                     const float2 q2 = lds64f(qf_s + 8 * c2);
@@ -1025,6 +1110,33 @@ fused_attn_ws_kernel(const kvc_seq_desc *__restrict__ seqs, int H, const float *
                 }
                 const float xa = cursor2_sym12<SB>(c2c[0], lut_s);
                 const float xb = cursor2_sym12<SB>(c2c[1], lut_s);
+                if (t & 1) {
+                    acc[t / 2] = __ffma2_rn(make_float2(fa, xa), aA2, acc[t / 2]);
+                    acc[t / 2] = __ffma2_rn(make_float2(fb, xb), aB2, acc[t / 2]);
+                } else {
+                    fa = xa;
+                    fb = xb;
+                }
+            }
+            cur[0].p = c2c[0].p;
+            cur[1].p = c2c[1].p;
+        } else if (VMODE == 6 || VMODE == 7 || VMODE == 8) {
+            // codes <= 9 (8) bits: lane-copied LUT, a reload per 7 (8) symbols
+            constexpr int R = Dec<VMODE>::kReload, SB = Dec<VMODE>::kSymBits,
+                          CP = Dec<VMODE>::kCopies;
+            const uint32_t copy_s = lut_s + 4 * (lane & (CP - 1));
+            Cursor2 c2c[2];
+            cursor2_init(c2c[0], slot, bit0 + iA - cA);
+            cursor2_init(c2c[1], slot, bit0 + totA + iB - cB);
+            float fa = 0.f, fb = 0.f;
+#pragma unroll
+            for (int t = 0; t < D; ++t) {
+                if (t % R == 0) {
+                    cursor2_reload(c2c[0]);
+                    cursor2_reload(c2c[1]);
+                }
+                const float xa = cursor2_sym_copy<SB, CP>(c2c[0], copy_s);
+                const float xb = cursor2_sym_copy<SB, CP>(c2c[1], copy_s);
                 if (t & 1) {
                     acc[t / 2] = __ffma2_rn(make_float2(fa, xa), aA2, acc[t / 2]);
                     acc[t / 2] = __ffma2_rn(make_float2(fb, xb), aB2, acc[t / 2]);
@@ -2618,12 +2730,12 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
     if (n_seqs < 1 || H < 1) return kvc_fail(KVC_ERR_CONFIG, "bad shape");
     if (group != 1 && group != 2 && group != 4)
         return kvc_fail(KVC_ERR_CONFIG, "fused GQA supports group 2 or 4");
-    int max_chunks = 0, max_len = 0, stage_k = 0, stage_v = 0;
+    int max_chunks = 0, max_len = 0, max_len_k = 0, max_len_v = 0, stage_k = 0, stage_v = 0;
     for (int i = 0; i < n_seqs; ++i) {
         max_chunks = seqs_host[i].n_chunks > max_chunks ? seqs_host[i].n_chunks : max_chunks;
-        int ml = seqs_host[i].k_max_len > seqs_host[i].v_max_len ? seqs_host[i].k_max_len
-                                                                  : seqs_host[i].v_max_len;
-        max_len = ml > max_len ? ml : max_len;
+        max_len_k = std::max(max_len_k, (int)seqs_host[i].k_max_len);
+        max_len_v = std::max(max_len_v, (int)seqs_host[i].v_max_len);
+        max_len = std::max(max_len_k, max_len_v);
         stage_k = seqs_host[i].stage_bytes_k > stage_k ? seqs_host[i].stage_bytes_k : stage_k;
         stage_v = seqs_host[i].stage_bytes_v > stage_v ? seqs_host[i].stage_bytes_v : stage_v;
     }
@@ -2638,14 +2750,50 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
     Partial *part = static_cast<Partial *>(workspace_dev);
     // decoder: pair LUT12 when every code is <= 6 bits (measured fastest, see
     // profiles/), else single-symbol LUT12; env KVC_FUSED_MODE=0|1 overrides.
-    int mode = max_len <= 6 ? 1 : (max_len <= 12 ? 2 : 5);
+    // Longer codes: single-symbol decoders, chosen per side (K, V) from the
+    // batch's longest code on that side: <= 9 bits the lane-private 9-bit LUT
+    // (MODE 6; KVC_FUSED_LUT9=0 selects MODE 2 instead), <= 12 the shared
+    // 12-bit LUT (MODE 2), 13 the 13-bit LUT (MODE 5).
+    int mode = max_len <= 6 ? 1 : (max_len <= 9 ? 6 : (max_len <= 12 ? 2 : 5));
     if (max_len <= 6) {
         const char *env = getenv("KVC_FUSED_MODE");
         if (env && (env[0] == '0' || env[0] == '1')) mode = env[0] - '0';
     }
+    const char *lut9env = getenv("KVC_FUSED_LUT9");
+    const bool lut9 = !(lut9env && lut9env[0] == '0');
+    auto side_mode = [&](int ml) {
+        if (ml > 12) return 5;
+        if (!lut9 || ml > 10) return 2;
+        return ml <= 8 ? 7 : (ml == 9 ? 6 : 8);
+    };
+    int kside = mode, vside = mode;
+    if (mode != 0 && mode != 1) {
+        kside = side_mode(max_len_k);
+        vside = side_mode(max_len_v);
+        // experiments: KVC_FUSED_KSIDE / KVC_FUSED_VSIDE = 7|6|8|2|5 force a side's
+        // decoder when it covers that side's longest code
+        auto force = [](const char *name, int ml, int cur) {
+            const char *e = getenv(name);
+            if (!e) return cur;
+            const int m = e[0] - '0';
+            const int cap = m == 7 ? 8 : (m == 6 ? 9 : (m == 8 ? 10 : (m == 2 ? 12 : (m == 5 ? 13 : 0))));
+            return ml <= cap ? m : cur;
+        };
+        kside = force("KVC_FUSED_KSIDE", max_len_k, kside);
+        vside = force("KVC_FUSED_VSIDE", max_len_v, vside);
+        // K on the 16-copy table beside a V side on the shared 12/13-bit tables
+        // measured 8-40 % slower than K on the shared table too (config 5 at
+        // (0.01, 0.02) and (0.02, 0.05)); every other pairing is faster
+        if ((kside == 6 || kside == 8) && vside != 6 && vside != 7 && vside != 8) kside = 2;
+        mode = max_len == 13 ? 5 : 2;  // (the fallback kernel's mode)
+    }
     const size_t per_warp = 2 * (size_t)(stage_k + stage_v) + D * 4 + 64;
     size_t smem = NW * per_warp;  // dynamic part (LUTs are static)
     if (smem < NW * sizeof(Partial)) smem = NW * sizeof(Partial);
+    auto dyn = [](int m) { return m >= 5; };  // LUT in the WS kernel's dynamic region
+    const size_t dyn_lut_bytes = (dyn(kside) ? 32768 : 0) + (dyn(vside) ? 32768 : 0);
+    const size_t static_lut_bytes = (dyn(kside) ? 0 : (kside == 0 ? 8192 : 16384)) +
+                                    (dyn(vside) ? 0 : (vside == 0 ? 8192 : 16384));
     const size_t lut_bytes = mode == 0 ? 2 * 8192 : (mode == 5 ? 2 * 32768 : 2 * 16384);
     if (smem + lut_bytes + 256 > 227 * 1024)
         return kvc_fail(KVC_ERR_CONFIG, "block extents too large for staging");
@@ -2741,9 +2889,10 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
     }
     const char *impl = getenv("KVC_FUSED_IMPL");
     const bool use_ws = !(impl && impl[0] == 'i');
-    const size_t ws_smem = WS_PAIRS * (2 * (size_t)(stage_k + stage_v) + 1024 + 64) +
-                           (mode == 5 ? lut_bytes : 0);  // the 13-bit LUTs are dynamic
-    if (use_ws && max_chunks > 0 && ws_smem + (mode == 5 ? 0 : lut_bytes) + 256 <= 227 * 1024) {
+    size_t ws_smem = WS_PAIRS * (2 * (size_t)(stage_k + stage_v) + 1024 + 64) +
+                     dyn_lut_bytes;  // the 13-bit / 9-bit LUTs are dynamic
+    if (const char *pad = getenv("KVC_WS_PAD")) ws_smem += (size_t)atoi(pad);  // experiments
+    if (use_ws && max_chunks > 0 && ws_smem + static_lut_bytes + 256 <= 227 * 1024) {
         int ws_cps = pick_chunks_per_split(max_chunks, (long)n_seqs * H);
         if (const char *cenv = getenv("KVC_FUSED_CPS")) {  // experiments: chunks per split
             const int v = atoi(cenv);
@@ -2764,8 +2913,8 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
         // default: plain pair LUT for K and V.  KVC_FUSED_VMODE / KVC_FUSED_KMODE
         // = 3 select the lane-substituted lookups (-16% smem wavefronts, but +14%
         // instructions and a dependent second LDS: measured 9% slower, profiles/)
-        int vmode = (mode == 2) ? 2 : 1;
-        if (mode != 2 && venv && (venv[0] == '0' || venv[0] == '1' || venv[0] == '3' || venv[0] == '4'))
+        int vmode = (mode == 0 || mode == 1) ? 1 : vside;
+        if ((mode == 0 || mode == 1) && venv && (venv[0] == '0' || venv[0] == '1' || venv[0] == '3' || venv[0] == '4'))
             vmode = venv[0] - '0';
         const char *kenv = getenv("KVC_FUSED_KMODE");
         const int kmode = (mode == 1 && kenv && kenv[0] == '3') ? 3 : mode;
@@ -2778,8 +2927,30 @@ extern "C" int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *s
             seqs_dev, H, q_dev, scores_dev, ctx_stride, part, ws_plan, stage_k, stage_v,     \
             err_dev);                                                                        \
     } while (0)
-        if (mode == 5) KVC_LAUNCH_WS(5, 5);
-        else if (mode == 2) KVC_LAUNCH_WS(2, 2);
+#define KVC_LAUNCH_WS_V(M)                                                                   \
+    do {                                                                                     \
+        if (vside == 7) KVC_LAUNCH_WS(M, 7);                                                 \
+        else if (vside == 6) KVC_LAUNCH_WS(M, 6);                                            \
+        else if (vside == 8) KVC_LAUNCH_WS(M, 8);                                            \
+        else if (vside == 2) KVC_LAUNCH_WS(M, 2);                                            \
+        else KVC_LAUNCH_WS(M, 5);                                                            \
+    } while (0)
+        // (K on the 9- or 10-bit copies only beside V on copies, see above)
+#define KVC_LAUNCH_WS_VC(M)                                                                  \
+    do {                                                                                     \
+        if (vside == 7) KVC_LAUNCH_WS(M, 7);                                                 \
+        else if (vside == 6) KVC_LAUNCH_WS(M, 6);                                            \
+        else KVC_LAUNCH_WS(M, 8);                                                            \
+    } while (0)
+        if (mode != 0 && mode != 1) {
+            if (kside == 7) KVC_LAUNCH_WS_V(7);
+            else if (kside == 6) KVC_LAUNCH_WS_VC(6);
+            else if (kside == 8) KVC_LAUNCH_WS_VC(8);
+            else if (kside == 2) KVC_LAUNCH_WS_V(2);
+            else KVC_LAUNCH_WS_V(5);
+        }
+#undef KVC_LAUNCH_WS_V
+#undef KVC_LAUNCH_WS_VC
         else if (mode == 0) KVC_LAUNCH_WS(0, 0);
         else if (kmode == 3 && vmode == 3) KVC_LAUNCH_WS(3, 3);
         else if (vmode == 0) KVC_LAUNCH_WS(1, 0);

@@ -744,11 +744,12 @@ def _lengths_with_max(n_symbols, target, hk_fn):
     raise AssertionError("no histogram found")
 
 
-@pytest.mark.parametrize("target", [12, 13])
+@pytest.mark.parametrize("target", [8, 9, 10, 11, 12, 13])
 def test_fused_single_symbol_long_codes_match_oracle(kv, target):
-    """Codes of 12 and 13 bits on the hot shape (D 128, bs 64): the fused
-    fetch's single-symbol decoders (12-bit LUT, MODE 2; 13-bit LUT, MODE 5)
-    against the oracle with the same injected codebooks, ragged tail
+    """Codes of 8-13 bits on the hot shape (D 128, bs 64): the fused fetch's
+    single-symbol decoders (lane-copied 8-, 9- and 10-bit LUTs, MODES 7, 6
+    and 8; the shared 12-bit LUT, MODE 2; 13-bit, MODE 5) against the oracle
+    with the same injected codebooks, ragged tail
     included; and a batch mixing 13-bit books with a 14-bit one (the latter on
     the generic kernels) equals per-state attention_step."""
     import oracle
@@ -786,3 +787,46 @@ def test_fused_single_symbol_long_codes_match_oracle(kv, target):
             ref = kv.attention_step(s, qb[i]).out
             # different split plans (batch of 2 vs 1 state): summation order only
             assert max_relative_error(out[i].cpu().numpy(), ref.cpu().numpy()) <= 1e-5
+
+
+@pytest.mark.parametrize("rels", [(0.01, 0.02), (0.02, 0.05)])
+def test_lane_private_lut9_equals_shared_lut12(kv, rels, monkeypatch):
+    """Fine scales with codes of 7-10 bits: the lane-private 9-bit decoder
+    (MODE 6, default, on each side whose codes are <= 9 bits) and the shared
+    12-bit one (MODE 2, KVC_FUSED_LUT9=0)
+    decode the same symbols in the same order, so a batched launch is
+    bit-identical; and it matches the oracle."""
+    import oracle
+    import torch
+    H, ctx = 4, 64 * 30 + 17
+    rel_k, rel_v = rels
+    ck = kv.QuantConfig(kv.QuantMode.K_BLOCK, rel_quant_scale=rel_k)
+    cv = kv.QuantConfig(kv.QuantMode.V_TOKEN, rel_quant_scale=rel_v)
+    sts, data = [], []
+    for b in range(3):
+        k = oracle.generate_synthetic(ctx - 40 * b, H, 128, seed=300 + 2 * b).astype(np.float16)
+        v = oracle.generate_synthetic(ctx - 40 * b, H, 128, seed=301 + 2 * b).astype(np.float16)
+        sts.append(kv.LayerCacheState.prefill(kv.CacheTensor(k), kv.CacheTensor(v), ck, cv))
+        data.append((k, v))
+    # the decoder is chosen per side from the batch's longest code on that side
+    mk = max(s.k_codebook.max_code_length for s in sts)
+    mv = max(s.v_codebook.max_code_length for s in sts)
+    assert 7 <= min(mk, mv) <= 9 and max(mk, mv) <= 12, (mk, mv)
+    q = torch.from_numpy(np.random.default_rng(3).standard_normal((3, H, 128), dtype=np.float32)).cuda()
+    out9, _, e9 = kv.attention_batched(sts, q)
+    monkeypatch.setenv("KVC_FUSED_LUT9", "0")
+    out12, _, e12 = kv.attention_batched(sts, q)
+    assert int(e9.item()) == 0 and int(e12.item()) == 0
+    assert torch.equal(out9, out12)
+    # every pairing of side decoders the sides' code lengths allow
+    for ks in "7682":
+        for vs in "7682":
+            monkeypatch.setenv("KVC_FUSED_LUT9", "1")
+            monkeypatch.setenv("KVC_FUSED_KSIDE", ks)
+            monkeypatch.setenv("KVC_FUSED_VSIDE", vs)
+            o, _, e = kv.attention_batched(sts, q)
+            assert int(e.item()) == 0 and torch.equal(o, out12), (ks, vs)
+    k, v = data[1]
+    o = oracle.OracleState.prefill(k, v, rel_k=rel_k, rel_v=rel_v)
+    ref_out, _ = o.attention_step(q[1].cpu().numpy())
+    assert max_relative_error(out9[1].cpu().numpy(), ref_out) <= 1e-5
