@@ -159,11 +159,26 @@ __device__ __forceinline__ uint32_t code_fast_flag(float x, float lo, float r32,
     return __float_as_uint(m) & 0xFFu;
 }
 
-template <typename T, bool ENCODE, int MODE>
+// code_fast_flag for a column pair with packed f32x2 arithmetic (same
+// roundings, so the same codes): returns a | b << 8 (the low byte of each
+// RD(v + 2^23); byte 2 of that float is zero), `g` = frac(v) - 1/2 per lane.
+__device__ __forceinline__ uint32_t code_pair_fast(float2 x, float2 nlo, float2 r, float2 &g) {
+    const float2 t = __fmul2_rn(__fadd2_rn(x, nlo), r);
+    const float2 v = __fadd2_rn(t, make_float2(0.5f, 0.5f));
+    const float2 m = __fadd2_rd(v, make_float2(8388608.0f, 8388608.0f));
+    const float2 d = __fadd2_rn(m, make_float2(-8388607.5f, -8388607.5f));  // floor(v) + 1/2, exact
+    g = __ffma2_rn(d, make_float2(-1.0f, -1.0f), v);                         // v - d, exact
+    return __byte_perm(__float_as_uint(m.x), __float_as_uint(m.y), 0x2240u);
+}
+constexpr float kNearBand = 0.5f - (1.0f / 4096.0f);
+
+// OUT: pass A writes the codes for pass B (codes_out); SMALL: per-warp 32-bin
+// histograms (alphabet < 32) instead of the shared 256-bin one.
+template <typename T, bool ENCODE, int MODE, bool OUT, bool SMALL>
 __device__ __forceinline__ void quantize_hot(const T *stage, uint8_t *codes, const float *u_lo,
                                              const float *u_sc, const float *u_r, int max_code,
-                                             bool small_alpha, uint32_t *whist, uint32_t *sh_hist,
-                                             int tid, uint8_t *codes_out) {
+                                             uint32_t *whist, uint32_t *sh_hist, int tid,
+                                             uint8_t *codes_out) {
     constexpr int D = 128, BS = 64;
     const int j = tid & 63, q = tid >> 6;  // column pair, row phase (0..3)
     const int c0 = 2 * j;
@@ -172,6 +187,8 @@ __device__ __forceinline__ void quantize_hot(const T *stage, uint8_t *codes, con
         klo0 = u_lo[c0]; klo1 = u_lo[c0 + 1];
         kr0 = u_r[c0]; kr1 = u_r[c0 + 1];
     }
+    uint32_t *hist = SMALL ? whist : sh_hist;
+    uint16_t *out16 = reinterpret_cast<uint16_t *>((ENCODE ? codes : codes_out) + c0);
 #pragma unroll 4
     for (int k = 0; k < BS / 4; ++k) {
         const int r = q + 4 * k;
@@ -184,10 +201,11 @@ __device__ __forceinline__ void quantize_hot(const T *stage, uint8_t *codes, con
             const float2 f = *reinterpret_cast<const float2 *>(stage + r * D + c0);
             x0 = f.x; x1 = f.y;
         }
-        uint32_t a, b;
+        uint32_t pair;
         if (MODE == KVC_K_CHANNEL) {
-            a = code_clamped(x0, klo0, u_sc[c0], kr0, max_code);
-            b = code_clamped(x1, klo1, u_sc[c0 + 1], kr1, max_code);
+            const uint32_t a = code_clamped(x0, klo0, u_sc[c0], kr0, max_code);
+            const uint32_t b = code_clamped(x1, klo1, u_sc[c0 + 1], kr1, max_code);
+            pair = a | (b << 8);
         } else {
             // branch-free fast codes; near-ties (~0.05 % of fp16 values) are redone
             // exactly behind one warp-uniform branch per pair (taken ~3 % of the time)
@@ -195,27 +213,20 @@ __device__ __forceinline__ void quantize_hot(const T *stage, uint8_t *codes, con
             const float lo1 = MODE == KVC_V_TOKEN ? lo0 : klo1;
             const float r0 = MODE == KVC_V_TOKEN ? u_r[r] : kr0;
             const float r1 = MODE == KVC_V_TOKEN ? r0 : kr1;
-            bool near_a, near_b;
-            a = code_fast_flag(x0, lo0, r0, near_a);
-            b = code_fast_flag(x1, lo1, r1, near_b);
-            if (__any_sync(0xffffffffu, near_a || near_b)) {
+            float2 g;
+            pair = code_pair_fast(make_float2(x0, x1), make_float2(-lo0, -lo1), make_float2(r0, r1), g);
+            if (__any_sync(0xffffffffu, fmaxf(fabsf(g.x), fabsf(g.y)) >= kNearBand)) {
                 const int ua = MODE == KVC_V_TOKEN ? r : c0, ub = MODE == KVC_V_TOKEN ? r : c0 + 1;
-                if (near_a) a = u_sc[ua] > 0.f ? code_f64(x0, lo0, u_sc[ua]) : 0u;
-                if (near_b) b = u_sc[ub] > 0.f ? code_f64(x1, lo1, u_sc[ub]) : 0u;
+                uint32_t a = pair & 0xFFu, b = pair >> 8;
+                if (fabsf(g.x) >= kNearBand) a = u_sc[ua] > 0.f ? code_f64(x0, lo0, u_sc[ua]) : 0u;
+                if (fabsf(g.y) >= kNearBand) b = u_sc[ub] > 0.f ? code_f64(x1, lo1, u_sc[ub]) : 0u;
+                pair = a | (b << 8);
             }
         }
-        if (ENCODE) {
-            *reinterpret_cast<uint16_t *>(codes + r * D + c0) = (uint16_t)(a | (b << 8));
-        } else if (codes_out) {
-            *reinterpret_cast<uint16_t *>(codes_out + r * D + c0) = (uint16_t)(a | (b << 8));
-        }
-        if (ENCODE) {
-        } else if (small_alpha) {
-            atomicAdd(&whist[a], 1u);
-            atomicAdd(&whist[b], 1u);
-        } else {
-            atomicAdd(&sh_hist[a], 1u);
-            atomicAdd(&sh_hist[b], 1u);
+        if (ENCODE || OUT) out16[r * (D / 2)] = (uint16_t)pair;
+        if (!ENCODE) {
+            atomicAdd(&hist[pair & 0xFFu], 1u);
+            atomicAdd(&hist[pair >> 8], 1u);
         }
     }
 }
@@ -518,15 +529,29 @@ store_kernel(StoreParams P, int stage_words) {
         else atomicAdd(&sh_hist[code], 1u);
     };
     if constexpr (DT == 128 && BST == 64) {
-        if (is_kc)
-            quantize_hot<T, ENCODE, KVC_K_CHANNEL>(stage, codes, u_lo, u_sc, u_r, S.max_code,
-                                                   small_alpha, whist, sh_hist, tid, cout);
-        else if (is_v)
-            quantize_hot<T, ENCODE, KVC_V_TOKEN>(stage, codes, u_lo, u_sc, u_r, S.max_code,
-                                                 small_alpha, whist, sh_hist, tid, cout);
-        else
-            quantize_hot<T, ENCODE, KVC_K_BLOCK>(stage, codes, u_lo, u_sc, u_r, S.max_code,
-                                                 small_alpha, whist, sh_hist, tid, cout);
+        // (out, small) specialised so the loop carries no per-pair branches
+#define KVC_QH(M)                                                                               \
+    do {                                                                                        \
+        if (ENCODE)                                                                             \
+            quantize_hot<T, ENCODE, M, false, false>(stage, codes, u_lo, u_sc, u_r, S.max_code, \
+                                                     whist, sh_hist, tid, cout);                \
+        else if (cout && small_alpha)                                                           \
+            quantize_hot<T, ENCODE, M, true, true>(stage, codes, u_lo, u_sc, u_r, S.max_code,   \
+                                                   whist, sh_hist, tid, cout);                  \
+        else if (cout)                                                                          \
+            quantize_hot<T, ENCODE, M, true, false>(stage, codes, u_lo, u_sc, u_r, S.max_code,  \
+                                                    whist, sh_hist, tid, cout);                 \
+        else if (small_alpha)                                                                   \
+            quantize_hot<T, ENCODE, M, false, true>(stage, codes, u_lo, u_sc, u_r, S.max_code,  \
+                                                    whist, sh_hist, tid, cout);                 \
+        else                                                                                    \
+            quantize_hot<T, ENCODE, M, false, false>(stage, codes, u_lo, u_sc, u_r, S.max_code, \
+                                                     whist, sh_hist, tid, cout);                \
+    } while (0)
+        if (is_kc) KVC_QH(KVC_K_CHANNEL);
+        else if (is_v) KVC_QH(KVC_V_TOKEN);
+        else KVC_QH(KVC_K_BLOCK);
+#undef KVC_QH
     } else if (D <= kThreads) {
         // thread -> fixed column c (one division per thread, none per element)
         const int rstep = kThreads / D;
