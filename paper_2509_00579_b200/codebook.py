@@ -10,7 +10,9 @@ append (SPEC: codebooks are immutable after prefill).
 from __future__ import annotations
 
 import ctypes
+import threading
 import weakref
+from collections import OrderedDict
 from dataclasses import dataclass, field
 from typing import Dict
 
@@ -193,18 +195,41 @@ def _upload(tables, dev: torch.device) -> torch.Tensor:
     return out, ext
 
 
+# Codebooks by code lengths (a canonical code is a function of its lengths):
+# the sequences and layers of a batch mostly end up with the same books, so a
+# prefill reuses the host tables and their device copy instead of rebuilding
+# and uploading ~100 KB per state and tensor.  Shared books are immutable.
+_BOOKS: "OrderedDict[bytes, HuffmanCodebook]" = OrderedDict()
+_BOOKS_MAX = 64
+_BOOKS_LOCK = threading.Lock()
+
+
 def codebook_from_lengths(lengths) -> HuffmanCodebook:
     """codebook.py:179-208 via kvc_codebook_build_tables."""
     lens = np.ascontiguousarray(np.asarray(lengths).astype(np.uint8))
     if lens.shape != (ALPHABET,):
         raise CodebookError(f"expected {ALPHABET} code lengths, got shape {lens.shape}")
+    key = lens.tobytes()
+    with _BOOKS_LOCK:
+        cb = _BOOKS.get(key)
+        if cb is not None:
+            _BOOKS.move_to_end(key)
+            return cb
     tables = _lib.CodebookTables()
     st = _lib.lib().kvc_codebook_build_tables(lens.ctypes.data_as(ctypes.c_void_p),
                                               ctypes.byref(tables))
     _lib.check(st, "codebook_from_lengths")
     words = np.frombuffer(bytes(tables.words), dtype=np.uint32).copy()
-    return HuffmanCodebook(code_lengths=lens.copy(), code_words=words,
-                           max_code_length=int(tables.max_len), tables=tables)
+    lens = lens.copy()
+    lens.setflags(write=False)
+    words.setflags(write=False)
+    cb = HuffmanCodebook(code_lengths=lens, code_words=words,
+                         max_code_length=int(tables.max_len), tables=tables)
+    with _BOOKS_LOCK:
+        _BOOKS[key] = cb
+        while len(_BOOKS) > _BOOKS_MAX:
+            _BOOKS.popitem(last=False)
+    return cb
 
 
 def build_codebook(h) -> HuffmanCodebook:
