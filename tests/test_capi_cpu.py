@@ -107,3 +107,22 @@ def test_decode_tree_matches_reference(case):
         t = codebook_from_lengths(g[f"fin_{w}_lengths"]).decode_tree
         assert np.array_equal(t.children, g[f"fin_{w}_tree_children"])
         assert t.n_nodes == len(g[f"fin_{w}_tree_children"])
+
+
+def test_codebooks_shared_by_code_lengths():
+    """codebook_from_lengths returns one immutable book per distinct length
+    table (the tables and their device copy are reused across states); other
+    lengths give a different book."""
+    import numpy as np
+    import pytest
+    from paper_2509_00579_b200 import codebook_from_lengths
+    lens = np.zeros(256, np.uint8)
+    lens[:4] = [1, 2, 3, 3]
+    a, b = codebook_from_lengths(lens), codebook_from_lengths(lens.copy())
+    assert a is b
+    with pytest.raises(ValueError):
+        a.code_lengths[0] = 2
+    lens[:4] = [2, 2, 2, 2]
+    c = codebook_from_lengths(lens)
+    assert c is not a and c.code_lengths[:4].tolist() == [2, 2, 2, 2]
+    assert a.code_lengths[:4].tolist() == [1, 2, 3, 3]
