@@ -1923,12 +1923,10 @@ fused_attn_gqa_mma_kernel(const kvc_seq_desc *__restrict__ seqs, int H,
             lsum[g] += pA[g] + pB[g];
         }
         {   // rescale the accumulators: column n = 2tig + c belongs to member n % G
-            float a0 = alpha[0], a1 = alpha[1 % G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                a0 = (2 * tig) % G == g ? alpha[g] : a0;
-                a1 = (2 * tig + 1) % G == g ? alpha[g] : a1;
-            }
+            // (explicit selects: a select loop over g was lowered to a local array)
+            const bool odd = (tig & 1) != 0;
+            const float a0 = (G == 4 && odd) ? alpha[2 % G] : alpha[0];
+            const float a1 = (G == 4 && odd) ? alpha[3 % G] : alpha[1 % G];
 #pragma unroll
             for (int s = 0; s < 8; ++s) {
                 acc[s][0] *= a0; acc[s][1] *= a1; acc[s][2] *= a0; acc[s][3] *= a1;
