@@ -256,8 +256,12 @@ size_t kvc_v_output_workspace_bytes(int n_seqs, int H, int D);
  * softmax -> .V, decompressed KV never leaves shared memory/registers),
  * split over the context and combined.  scores_dev may be NULL.  q_dev
  * [n_seqs, H*group, D]; GQA: `group` query heads per KV head.
- * Falls back to the generic kernels (same device) for shapes the fused
- * kernel does not cover. */
+ * Covers head_dim 128, block 64 and codes of at most 13 bits (GQA groups 2
+ * and 4: at most 6); the decoder is chosen per side from the batch's longest
+ * code (pair LUT <= 6 bits, lane-copied single-symbol LUTs 7-10, shared
+ * 12- and 13-bit LUTs).  Other shapes or books return KVC_ERR_CONFIG: the
+ * caller runs kvc_k_scores / kvc_softmax_rows / kvc_v_output for them (as
+ * attention.py does, per state). */
 int kvc_attention(const kvc_seq_desc *seqs_dev, const kvc_seq_desc *seqs_host, int n_seqs,
                   int H, int D, int bs, int group, const float *q_dev, float *out_dev,
                   float *scores_dev, long ctx_stride, void *workspace_dev,
