@@ -23,10 +23,10 @@ def _data(ctx, extra, H, seed):
     return k, v
 
 
-def _prefill(kv, k, v, ctx):
+def _prefill(kv, k, v, ctx, rels=(None, None)):
     return kv.LayerCacheState.prefill(kv.CacheTensor(k[:ctx]), kv.CacheTensor(v[:ctx]),
-                                      kv.QuantConfig(kv.QuantMode.K_BLOCK),
-                                      kv.QuantConfig(kv.QuantMode.V_TOKEN))
+                                      kv.QuantConfig(kv.QuantMode.K_BLOCK, rel_quant_scale=rels[0]),
+                                      kv.QuantConfig(kv.QuantMode.V_TOKEN, rel_quant_scale=rels[1]))
 
 
 def test_append_batched_matches_append_token_and_oracle(kv):
@@ -90,11 +90,14 @@ def test_attention_right_after_an_event_is_exact(kv):
     assert np.abs(got - ref).max() / np.abs(ref).max() <= 1e-5
 
 
-@pytest.mark.parametrize("group", [1, 4])
-def test_decode_loop_graph_matches_eager(kv, group):
+@pytest.mark.parametrize("group,rels", [(1, (None, None)), (4, (None, None)), (1, (0.02, 0.05)),
+                                        (1, (0.01, 0.02))])
+def test_decode_loop_graph_matches_eager(kv, group, rels):
+    """Default scales (pair decoders; G = 4 on the GQA kernel) and fine scales
+    (lane-copied single-symbol decoders, 7-10-bit codes)."""
     import torch
     L, B, H, ctx, steps = 3, 2, 2, 64 * 4 + 60, 140   # one overflow event inside
-    mk = lambda: [[_prefill(kv, *_data(ctx, 0, H, 50 + 7 * l + b), ctx) for b in range(B)]
+    mk = lambda: [[_prefill(kv, *_data(ctx, 0, H, 50 + 7 * l + b), ctx, rels) for b in range(B)]
                   for l in range(L)]
     sa, sb = mk(), mk()
     ga = kv.DecodeLoop(sa, group=group, use_graph=True)
@@ -112,6 +115,9 @@ def test_decode_loop_graph_matches_eager(kv, group):
         gb.step(kn, vn, q, ob)
         assert torch.equal(oa, ob), f"step {i}"
     assert ga.events == gb.events == 1 and ga.captures >= 2
+    if rels[0] is not None:
+        assert all(max(x.k_codebook.max_code_length, x.v_codebook.max_code_length) >= 7
+                   for r in sa for x in r)
     for ra, rb in zip(sa, sb):
         for x, y in zip(ra, rb):
             x.check()
