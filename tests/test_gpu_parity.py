@@ -830,3 +830,36 @@ def test_lane_private_lut9_equals_shared_lut12(kv, rels, monkeypatch):
     o = oracle.OracleState.prefill(k, v, rel_k=rel_k, rel_v=rel_v)
     ref_out, _ = o.attention_step(q[1].cpu().numpy())
     assert max_relative_error(out9[1].cpu().numpy(), ref_out) <= 1e-5
+
+
+@pytest.mark.parametrize("rels", [(0.02, 0.05), (0.01, 0.02)])
+def test_kchannel_fine_scales_fused_matches_oracle(kv, rels):
+    """K_CHANNEL (whole-context ranges, clipped codes) at fine scales on the
+    hot shape: arenas bit-exact with the oracle and the fused fetch on the
+    single-symbol decoders (lane-copied and, for 12-bit K codes, shared)
+    within 1e-5 of it, ragged tail and appends across an overflow event
+    included."""
+    import oracle
+    H, ctx, extra = 4, 64 * 12 + 9, 140
+    rel_k, rel_v = rels
+    k = oracle.generate_synthetic(ctx + extra, H, 128, seed=71).astype(np.float16)
+    v = oracle.generate_synthetic(ctx + extra, H, 128, seed=72).astype(np.float16)
+    kf = k[:ctx].astype(np.float32)
+    ranges = (kf.min(axis=0), kf.max(axis=0))
+    ck = kv.QuantConfig(kv.QuantMode.K_CHANNEL, rel_quant_scale=rel_k)
+    cv = kv.QuantConfig(kv.QuantMode.V_TOKEN, rel_quant_scale=rel_v)
+    st = kv.LayerCacheState.prefill(kv.CacheTensor(k[:ctx]), kv.CacheTensor(v[:ctx]), ck, cv,
+                                    k_channel_ranges=ranges)
+    o = oracle.OracleState.prefill(k[:ctx], v[:ctx], rel_k=rel_k, rel_v=rel_v, k_mode="kchannel")
+    for t in range(ctx, ctx + extra):
+        st.append_token(k[t].astype(np.float32), v[t].astype(np.float32))
+        o.append_token(k[t].astype(np.float32), v[t].astype(np.float32))
+    st.check()
+    assert 7 <= max(st.k_codebook.max_code_length, st.v_codebook.max_code_length) <= 12
+    assert st.k_arena.snapshot() == o.arena_bytes("k")
+    assert st.v_arena.snapshot() == o.arena_bytes("v")
+    q = np.random.default_rng(11).standard_normal((H, 128), dtype=np.float32)
+    res = kv.attention_step(st, q)
+    ref_out, ref_scores = o.attention_step(q)
+    assert max_relative_error(res.out.cpu().numpy(), ref_out) <= 1e-5
+    assert max_relative_error(res.scores.cpu().numpy(), ref_scores) <= 1e-5
