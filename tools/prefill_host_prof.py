@@ -39,6 +39,7 @@ def main():
     torch.cuda.synchronize()
     pr.disable()
     pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+    pstats.Stats(pr).sort_stats("cumtime").print_stats(40)
 
 
 if __name__ == "__main__":
