@@ -121,7 +121,9 @@ class LayerCacheState:
         ka, va = arena_bytes if arena_bytes is not None else (1 << 16, 1 << 16)
         # the two arenas' counters and the live {n_chunks, buffered} pair share
         # one zeroed pool allocation (one allocation and one fill per state)
-        if self.device.type == "cuda":
+        if _pre is not None and "small" in _pre:  # carved by prefill (released with _pre's extents)
+            small = _pre["small"]
+        elif self.device.type == "cuda":
             small, ext = pooled_zeros((128,), torch.uint8, self.device)
             weakref.finalize(self, ext.release)
         else:
@@ -261,7 +263,20 @@ class LayerCacheState:
         stream = torch.cuda.current_stream(kt.device).cuda_stream
         fused = bool(lib.kvc_store_supported(bs, D, 32 if codebooks is None else max(
             codebooks[0].max_code_length, codebooks[1].max_code_length)))
-        hist = torch.zeros(512, dtype=torch.int64, device=kt.device)
+        # one zeroed slab-pool block per state: [hist 4 KB | counters+live 128 B |
+        # K buffer | V buffer] (one allocation and one fill instead of four)
+        cap = cfg_k.buffer_size + 1
+        pre = None
+        if kt.device.type == "cuda":
+            nbuf = cap * H * D * 4
+            blk, blk_ext = pooled_zeros((4096 + 128 + 2 * nbuf,), torch.uint8, kt.device)
+            hist = blk[:4096].view(torch.int64)
+            pre = {"small": blk[4096:4224],
+                   "k_buffer": blk[4224:4224 + nbuf].view(torch.float32).view(cap, H, D),
+                   "v_buffer": blk[4224 + nbuf:].view(torch.float32).view(cap, H, D),
+                   "extents": (blk_ext,)}
+        else:
+            hist = torch.zeros(512, dtype=torch.int64, device=kt.device)
         kcodes = kmetas = vcodes = vmetas = None
         # small alphabets: pass A also records per-block histograms, so pass B takes
         # its arena offsets from one scan instead of the look-back (store_fused.cu)
@@ -300,12 +315,7 @@ class LayerCacheState:
         # everything that does not depend on the histogram is allocated while
         # pass A runs, so the host work between its completion and pass B is
         # only the codebook build, the table upload and the arena carve-out
-        cap = cfg_k.buffer_size + 1
-        if kt.device.type == "cuda":  # long-lived: from the slab pool
-            kb, ke = pooled_zeros((cap, H, D), torch.float32, kt.device)
-            vb, ve = pooled_zeros((cap, H, D), torch.float32, kt.device)
-            pre = {"k_buffer": kb, "v_buffer": vb, "extents": (ke, ve)}
-        else:
+        if pre is None:
             pre = {"k_buffer": torch.zeros((cap, H, D), dtype=torch.float32, device=kt.device)}
             pre["v_buffer"] = torch.zeros_like(pre["k_buffer"])
         pre_ws = (torch.empty(lib.kvc_store_workspace_bytes(n_chunks, H, D, bs), dtype=torch.uint8,
