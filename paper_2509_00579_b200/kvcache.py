@@ -59,6 +59,22 @@ class _Done:
 
 _DONE = _Done()
 
+_EMPTY = {}
+
+
+def _empty_ws(device: torch.device) -> torch.Tensor:
+    """A shared zero-size workspace placeholder (replaced, never written,
+    when a state first needs scratch)."""
+    t = _EMPTY.get(device)
+    if t is None:
+        t = _EMPTY[device] = torch.empty(0, dtype=torch.uint8, device=device)
+    return t
+
+
+@functools.lru_cache(maxsize=256)
+def _store_supported(bs: int, D: int, max_len: int) -> bool:
+    return bool(_lib.lib().kvc_store_supported(bs, D, max_len))
+
 
 def _hist_readback(hist: torch.Tensor):
     global _HIST_RING
@@ -152,7 +168,7 @@ class LayerCacheState:
             self._v_buffer = torch.zeros_like(self._k_buffer)
         self._k_tab = k_codebook.device_tables(self.device)
         self._v_tab = v_codebook.device_tables(self.device)
-        self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self._ws = _empty_ws(self.device)
         # live {n_chunks, buffered} on the device (kvc_seq_desc.live): the
         # growing-cache kernels update it, the fetch kernels read it, so the
         # descriptor stays the same across decode steps; the host keeps
@@ -163,9 +179,9 @@ class LayerCacheState:
         self.buffered = 0
         self._desc_dev = None
         self._desc_key = None
-        self._fused_store = bool(_lib.lib().kvc_store_supported(
-            cfg_k.block_size, head_dim, max(k_codebook.max_code_length,
-                                             v_codebook.max_code_length)))
+        self._fused_store = _store_supported(cfg_k.block_size, head_dim,
+                                             max(k_codebook.max_code_length,
+                                                 v_codebook.max_code_length))
 
     # ------------------------------------------------------------------
     @classmethod
@@ -261,8 +277,8 @@ class LayerCacheState:
             kt, vt = kt.to(torch.float32), vt.to(torch.float32)
         lib = _lib.lib()
         stream = torch.cuda.current_stream(kt.device).cuda_stream
-        fused = bool(lib.kvc_store_supported(bs, D, 32 if codebooks is None else max(
-            codebooks[0].max_code_length, codebooks[1].max_code_length)))
+        fused = _store_supported(bs, D, 32 if codebooks is None else max(
+            codebooks[0].max_code_length, codebooks[1].max_code_length))
         # one zeroed slab-pool block per state: [hist 4 KB | counters+live 128 B |
         # K buffer | V buffer] (one allocation and one fill instead of four)
         cap = cfg_k.buffer_size + 1
@@ -392,7 +408,7 @@ class LayerCacheState:
                 st._encode(kcodes, kmetas, vcodes, vmetas, n_chunks)
         # the prefill workspace goes back to the allocator's cache for the next
         # prefill; appends size their own
-        st._ws = torch.empty(0, dtype=torch.uint8, device=st.device)
+        st._ws = _empty_ws(st.device)
         r = ctx - n_full
         if r:
             st._k_buffer[:r] = kt[n_full:].to(torch.float32)
