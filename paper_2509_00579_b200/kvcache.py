@@ -76,6 +76,26 @@ def _store_supported(bs: int, D: int, max_len: int) -> bool:
     return bool(_lib.lib().kvc_store_supported(bs, D, max_len))
 
 
+@functools.lru_cache(maxsize=256)
+def _prefill_supported(bs: int, D: int, rel_k: float, rel_v: float) -> bool:
+    return bool(_lib.lib().kvc_store_prefill_supported(bs, D, rel_k, rel_v))
+
+
+@functools.lru_cache(maxsize=256)
+def _store_ws_bytes(n_chunks: int, H: int, D: int, bs: int) -> int:
+    return int(_lib.lib().kvc_store_workspace_bytes(n_chunks, H, D, bs))
+
+
+@functools.lru_cache(maxsize=256)
+def _prefill_scratch_bytes(n_chunks: int, H: int, D: int, bs: int):
+    """(per-block histograms, codes, workspace) bytes, each rounded to 256."""
+    lib = _lib.lib()
+    r = lambda x: (int(x) + 255) & ~255  # noqa: E731
+    codes = lib.kvc_store_codes_bytes(n_chunks, H) if (D == 128 and bs == 64) else 0
+    return (r(lib.kvc_store_blk_hist_bytes(n_chunks, H)), r(codes),
+            r(lib.kvc_store_workspace_bytes(n_chunks, H, D, bs)))
+
+
 def _hist_readback(hist: torch.Tensor):
     global _HIST_RING
     if _HIST_RING is None:
@@ -296,15 +316,16 @@ class LayerCacheState:
         kcodes = kmetas = vcodes = vmetas = None
         # small alphabets: pass A also records per-block histograms, so pass B takes
         # its arena offsets from one scan instead of the look-back (store_fused.cu)
-        blk_hist = blk_codes = None
+        blk_hist = blk_codes = pre_ws = None
         if (n_full and codebooks is None and fused
-                and lib.kvc_store_prefill_supported(bs, D, cfg_k.rel_quant_scale,
-                                                    cfg_v.rel_quant_scale)):
-            blk_hist = torch.empty(lib.kvc_store_blk_hist_bytes(n_chunks, H) // 2,
-                                   dtype=torch.int16, device=kt.device)
-            # hot shape: pass A also leaves the codes for pass B (no re-quantisation)
-            blk_codes = (torch.empty(lib.kvc_store_codes_bytes(n_chunks, H), dtype=torch.uint8,
-                                     device=kt.device) if (D == 128 and bs == 64) else None)
+                and _prefill_supported(bs, D, cfg_k.rel_quant_scale, cfg_v.rel_quant_scale)):
+            # one scratch allocation: per-block histograms | pass A's codes (hot
+            # shape: pass B encodes them, no re-quantisation) | pass B workspace
+            hb, cb_, wb = _prefill_scratch_bytes(n_chunks, H, D, bs)
+            scratch = torch.empty(hb + cb_ + wb, dtype=torch.uint8, device=kt.device)
+            blk_hist = scratch[:hb].view(torch.int16)
+            blk_codes = scratch[hb:hb + cb_] if cb_ else None
+            pre_ws = scratch[hb + cb_:]
             _lib.check(lib.kvc_store_hist_blocks(kt.data_ptr(), vt.data_ptr(), dtype_code(kt),
                                                  H * D, n_chunks, H, D, bs, cfg_k.mode.abi,
                                                  cfg_k.rel_quant_scale, cfg_v.rel_quant_scale,
@@ -334,8 +355,9 @@ class LayerCacheState:
         if pre is None:
             pre = {"k_buffer": torch.zeros((cap, H, D), dtype=torch.float32, device=kt.device)}
             pre["v_buffer"] = torch.zeros_like(pre["k_buffer"])
-        pre_ws = (torch.empty(lib.kvc_store_workspace_bytes(n_chunks, H, D, bs), dtype=torch.uint8,
-                              device=kt.device) if n_full and fused else None)
+        if pre_ws is None and n_full and fused:
+            pre_ws = torch.empty(_store_ws_bytes(n_chunks, H, D, bs), dtype=torch.uint8,
+                                 device=kt.device)
         hist_host = ev = None
         if codebooks is None and not _defer_hist:
             if process_group is not None:
