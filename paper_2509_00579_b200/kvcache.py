@@ -42,11 +42,12 @@ class _HistRing:
 
     def __init__(self, slots: int = 8):
         self.bufs = [torch.empty(512, dtype=torch.int64, pin_memory=True) for _ in range(slots)]
-        self.events = [None] * slots
+        self.events = [torch.cuda.Event() for _ in range(slots)]  # re-recorded per use
+        self.used = [False] * slots
         self.i = 0
 
 
-_HIST_RING = None
+_HIST_RINGS = {}
 
 
 class _Done:
@@ -97,19 +98,19 @@ def _prefill_scratch_bytes(n_chunks: int, H: int, D: int, bs: int):
 
 
 def _hist_readback(hist: torch.Tensor):
-    global _HIST_RING
-    if _HIST_RING is None:
-        _HIST_RING = _HistRing()
-    r = _HIST_RING
+    r = _HIST_RINGS.get(hist.device)  # per device: the slots' events are re-recorded
+    if r is None:
+        with torch.cuda.device(hist.device):
+            r = _HIST_RINGS[hist.device] = _HistRing()
     i = r.i
     r.i = (i + 1) % len(r.bufs)
-    if r.events[i] is not None:
-        r.events[i].synchronize()
+    ev = r.events[i]
+    if r.used[i]:
+        ev.synchronize()
     buf = r.bufs[i]
     buf.copy_(hist, non_blocking=True)
-    ev = torch.cuda.Event()
     ev.record(torch.cuda.current_stream(hist.device))
-    r.events[i] = ev
+    r.used[i] = True
     return buf, ev
 
 
