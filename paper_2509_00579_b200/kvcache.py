@@ -18,6 +18,7 @@ from __future__ import annotations
 from typing import Optional, Tuple
 
 import functools
+import threading
 import weakref
 
 import numpy as np
@@ -85,6 +86,38 @@ def _prefill_supported(bs: int, D: int, rel_k: float, rel_v: float) -> bool:
 @functools.lru_cache(maxsize=256)
 def _store_ws_bytes(n_chunks: int, H: int, D: int, bs: int) -> int:
     return int(_lib.lib().kvc_store_workspace_bytes(n_chunks, H, D, bs))
+
+
+class _SharedRelease:
+    """One slab-pool extent shared by the states of a grouped prefill: given
+    back when the last of them is released."""
+    __slots__ = ("ext", "n", "lock")
+
+    def __init__(self, ext, n: int):
+        self.ext, self.n, self.lock = ext, n, threading.Lock()
+
+    def release(self) -> None:
+        with self.lock:
+            self.n -= 1
+            last = self.n == 0
+        if last:
+            self.ext.release()
+
+
+class _GroupRing:
+    """Pinned [group, 512] slots for the grouped histogram readback (events
+    re-recorded; at most two groups are in flight)."""
+
+    def __init__(self, rows: int, slots: int = 4):
+        self.bufs = [torch.empty((rows, 512), dtype=torch.int64, pin_memory=True)
+                     for _ in range(slots)]
+        self.events = [torch.cuda.Event() for _ in range(slots)]
+        self.used = [False] * slots
+        self.i = 0
+
+
+_GROUP_RINGS = {}
+PREFILL_GROUP = 8  # items per grouped prefill launch batch
 
 
 @functools.lru_cache(maxsize=256)
@@ -248,6 +281,22 @@ class LayerCacheState:
                 for st in out:
                     st.check()
             return out
+        if cls._prefill_group_ok(items, cfg_k, cfg_v, kw):
+            # many equal slices (the sequences of a batch): pass A, allocations
+            # and the histogram readback per group of PREFILL_GROUP items, the
+            # next group's launched before this group's codebooks and pass B
+            hk = {k: kw[k] for k in ("head_base", "head_total") if k in kw}
+            groups = [items[i:i + PREFILL_GROUP] for i in range(0, len(items), PREFILL_GROUP)]
+            nxt = cls._prefill_begin_group(groups[0], cfg_k, cfg_v, **hk)
+            for gi in range(len(groups)):
+                cur = nxt
+                nxt = (cls._prefill_begin_group(groups[gi + 1], cfg_k, cfg_v, **hk)
+                       if gi + 1 < len(groups) else None)
+                out.extend(cls._prefill_finish(c, False) for c in cur)
+            if check:
+                for st in out:
+                    st.check()
+            return out
         nxt = cls._prefill_begin(*items[0], cfg_k, cfg_v, **kw) if items else None
         for i in range(len(items)):
             cur = nxt
@@ -257,6 +306,103 @@ class LayerCacheState:
         if check:  # one synchronisation for the whole batch, after every launch
             for st in out:
                 st.check()
+        return out
+
+    @staticmethod
+    def _prefill_group_ok(items, cfg_k, cfg_v, kw) -> bool:
+        """The grouped prefill covers the common serving case: device fp16/f32
+        tensors of one shape, K_BLOCK, codebooks from the data, the fused
+        hot-path Store with per-block histograms, default arena placement."""
+        if len(items) < 2 or any(kw.get(k) is not None for k in (
+                "codebooks", "k_channel_ranges", "process_group", "capacity", "page_pool",
+                "device")):
+            return False
+        if set(kw) - {"head_base", "head_total", "codebooks", "k_channel_ranges",
+                      "process_group", "capacity", "page_pool", "device"}:
+            return False
+        if cfg_k.mode is not QuantMode.K_BLOCK:
+            return False
+        k0 = items[0][0]
+        if not (isinstance(k0, torch.Tensor) and k0.is_cuda and k0.dim() == 3
+                and k0.dtype in (torch.float16, torch.float32)):
+            return False
+        for k, v in items:
+            if not (isinstance(k, torch.Tensor) and isinstance(v, torch.Tensor)
+                    and k.shape == k0.shape and v.shape == k0.shape and k.dtype == k0.dtype
+                    and v.dtype == k0.dtype and k.device == k0.device and v.device == k0.device
+                    and k.is_contiguous() and v.is_contiguous()):
+                return False
+        ctx, H, D = k0.shape
+        bs = cfg_k.block_size
+        return (ctx >= bs and cfg_k.block_size == cfg_v.block_size
+                and cfg_k.buffer_size == cfg_v.buffer_size
+                and _store_supported(bs, D, 32)
+                and _prefill_supported(bs, D, cfg_k.rel_quant_scale, cfg_v.rel_quant_scale))
+
+    @classmethod
+    def _prefill_begin_group(cls, items, cfg_k, cfg_v, head_base: int = 0,
+                             head_total: Optional[int] = None) -> list:
+        """_prefill_begin for a group of equal slices (see _prefill_group_ok):
+        one zeroed slab-pool block [histograms | per state: counters, K and V
+        token buffers] shared by the group's states, one scratch allocation,
+        pass A per item and ONE histogram readback for the group."""
+        k0 = items[0][0]
+        dev = k0.device
+        ctx, H, D = k0.shape
+        bs = cfg_k.block_size
+        n_chunks = ctx // bs
+        n_full = n_chunks * bs
+        G = len(items)
+        cap = cfg_k.buffer_size + 1
+        nbuf = cap * H * D * 4
+        per = 128 + 2 * nbuf
+        blk, ext = pooled_zeros((G * 4096 + G * per,), torch.uint8, dev)
+        shared = _SharedRelease(ext, G)
+        hists = blk[:G * 4096].view(torch.int64).view(G, 512)
+        hb, cb_, wb = _prefill_scratch_bytes(n_chunks, H, D, bs)
+        one = hb + cb_ + wb
+        scratch = torch.empty(G * one, dtype=torch.uint8, device=dev)
+        lib = _lib.lib()
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        src_dtype = np.dtype(np.float16) if k0.dtype == torch.float16 else np.dtype(np.float32)
+        code = dtype_code(k0)
+        out = []
+        for g, (k, v) in enumerate(items):
+            b0 = G * 4096 + g * per
+            pre = {"small": blk[b0:b0 + 128],
+                   "k_buffer": blk[b0 + 128:b0 + 128 + nbuf].view(torch.float32).view(cap, H, D),
+                   "v_buffer": blk[b0 + 128 + nbuf:b0 + per].view(torch.float32).view(cap, H, D),
+                   "extents": (shared,)}
+            s0 = g * one
+            blk_hist = scratch[s0:s0 + hb].view(torch.int16)
+            blk_codes = scratch[s0 + hb:s0 + hb + cb_] if cb_ else None
+            _lib.check(lib.kvc_store_hist_blocks(
+                k.data_ptr(), v.data_ptr(), code, H * D, n_chunks, H, D, bs, cfg_k.mode.abi,
+                cfg_k.rel_quant_scale, cfg_v.rel_quant_scale, None, hists[g].data_ptr(),
+                blk_hist.data_ptr(), blk_codes.data_ptr() if blk_codes is not None else None,
+                stream), "kvc_store_hist_blocks")
+            out.append(dict(cls=cls, kt=k, vt=v, cfg_k=cfg_k, cfg_v=cfg_v, codebooks=None,
+                            page_pool=None, k_channel_ranges=None, head_base=head_base,
+                            head_total=head_total, capacity=None, src_dtype=src_dtype, ctx=ctx,
+                            H=H, D=D, bs=bs, n_chunks=n_chunks, n_full=n_full, fused=True,
+                            hist=hists[g], hist_host=None, ev=None, blk_hist=blk_hist,
+                            blk_codes=blk_codes, kcodes=None, kmetas=None, vcodes=None,
+                            vmetas=None, pre=pre, pre_ws=scratch[s0 + hb + cb_:s0 + one]))
+        ring = _GROUP_RINGS.get(dev)
+        if ring is None:
+            with torch.cuda.device(dev):
+                ring = _GROUP_RINGS[dev] = _GroupRing(PREFILL_GROUP)
+        i = ring.i
+        ring.i = (i + 1) % len(ring.bufs)
+        ev = ring.events[i]
+        if ring.used[i]:
+            ev.synchronize()
+        host = ring.bufs[i]
+        host[:G].copy_(hists, non_blocking=True)
+        ev.record(torch.cuda.current_stream(dev))
+        ring.used[i] = True
+        for g, c in enumerate(out):
+            c["hist_host"], c["ev"] = host[g], ev
         return out
 
     @classmethod

@@ -532,6 +532,47 @@ def test_prefill_many_matches_prefill(kv):
         assert (st.context_len, st.buffered) == (ref.context_len, ref.buffered)
 
 
+def test_prefill_many_grouped_matches_prefill(kv):
+    """Equal device slices take the grouped prefill (pass A, allocations and
+    one histogram readback per group of PREFILL_GROUP, a ragged last group):
+    byte-identical to per-item prefill, and the states' token buffers (views
+    of one shared block) append and attend like independent states."""
+    from paper_2509_00579_b200 import kvcache
+    n, ctx, H, extra = kvcache.PREFILL_GROUP * 2 + 3, 64 * 20 + 37, 4, 100
+    ck, cv = kv.QuantConfig(kv.QuantMode.K_BLOCK), kv.QuantConfig(kv.QuantMode.V_TOKEN)
+    dev = torch.device("cuda")
+    kb = torch.empty((n, ctx + extra, H, 128), dtype=torch.float16, device=dev)
+    vb = torch.empty_like(kb)
+    for b in range(n):
+        kv.generate_synthetic_device(kv.SyntheticSpec(ctx + extra, H, 128, seed=900 + b), dev,
+                                     out=kb[b])
+        kv.generate_synthetic_device(kv.SyntheticSpec(ctx + extra, H, 128, seed=950 + b), dev,
+                                     out=vb[b])
+    items = [(kb[b, :ctx], vb[b, :ctx]) for b in range(n)]
+    assert kvcache.LayerCacheState._prefill_group_ok(items, ck, cv, {})
+    many = kv.LayerCacheState.prefill_many(items, ck, cv)
+    refs = [kv.LayerCacheState.prefill(k, v, ck, cv) for k, v in items]
+    for st, ref in zip(many, refs):
+        for a, b in ((st.k_arena, ref.k_arena), (st.v_arena, ref.v_arena)):
+            assert a.snapshot() == b.snapshot()
+            assert np.array_equal(a.block_offsets, b.block_offsets)
+        assert (st.context_len, st.buffered) == (ref.context_len, ref.buffered)
+        assert torch.equal(st._k_buffer[:st.buffered], ref._k_buffer[:ref.buffered])
+    cg, cr = kv.kvcache._BatchDesc(), kv.kvcache._BatchDesc()
+    for t in range(ctx, ctx + extra):  # an overflow event for every state
+        kv.append_batched(many, kb[:, t], vb[:, t], desc_cache=cg)
+        kv.append_batched(refs, kb[:, t], vb[:, t], desc_cache=cr)
+    q = torch.randn((n, H, 128), device=dev)
+    og, _, eg = kv.attention_batched(many, q)
+    orf, _, er = kv.attention_batched(refs, q)
+    assert int(eg.item()) == 0 and int(er.item()) == 0
+    assert torch.equal(og, orf)
+    for st, ref in zip(many, refs):
+        st.check()
+        assert st.k_arena.snapshot() == ref.k_arena.snapshot()
+        assert st.v_arena.snapshot() == ref.v_arena.snapshot()
+
+
 def test_decode_loop_entry_points(kv):
     """The bench/decode-loop variants write the same results: attention_gqa
     into a caller buffer (out=), attention_batched without the per-call error
