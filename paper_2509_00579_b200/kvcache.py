@@ -286,7 +286,11 @@ class LayerCacheState:
             # and the histogram readback per group of PREFILL_GROUP items, the
             # next group's launched before this group's codebooks and pass B
             hk = {k: kw[k] for k in ("head_base", "head_total") if k in kw}
-            groups = [items[i:i + PREFILL_GROUP] for i in range(0, len(items), PREFILL_GROUP)]
+            # at most PREFILL_GROUP items and ~1 GiB of pass-A scratch per group
+            ctx, H, D = items[0][0].shape
+            one = sum(_prefill_scratch_bytes(ctx // cfg_k.block_size, H, D, cfg_k.block_size))
+            G = max(1, min(PREFILL_GROUP, (1 << 30) // max(one, 1)))
+            groups = [items[i:i + G] for i in range(0, len(items), G)]
             nxt = cls._prefill_begin_group(groups[0], cfg_k, cfg_v, **hk)
             for gi in range(len(groups)):
                 cur = nxt
