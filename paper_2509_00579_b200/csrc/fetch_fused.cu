@@ -2096,67 +2096,101 @@ fused_attn_gqa_mma_kernel(const kvc_seq_desc *__restrict__ seqs, int H,
 
 // Merge split partials + the f32 buffered tokens (attention.py:103-107,
 // :160-164) into out = O / L; also writes buffered scores when requested.
-__global__ void __launch_bounds__(128)
+// Latency-shaped (it runs once per (seq, query head) per layer, between two
+// long kernels; in a batch-1 decode step its time is on the critical path):
+// each warp takes buffered rows w, w+4, .. and issues the K and V rows of up
+// to 8 of them (float4 per lane: coalesced 512-B rows) before any use, then
+// runs its own online softmax over them (scores by shuffle reduction); the
+// 4 warps' (m, l, o) and the split partials merge once at the end.  At most
+// 128 registers, so a large batch's thousands of these CTAs still run 4+ per SM.
+__global__ void __launch_bounds__(128, 4)
 combine_kernel(const kvc_seq_desc *__restrict__ seqs, int H, int bs, const float *__restrict__ q,
                const Partial *__restrict__ partial, int n_splits, float *__restrict__ out,
                float *__restrict__ scores, long ctx_stride, int group = 1) {
-    __shared__ float sh_p[1024];
-    __shared__ float sh_red[8];
-    __shared__ float sh_m, sh_l;
+    static_assert(D == 128, "a float4 per lane covers one head row");
+    constexpr int R = 8;  // rows per warp per pass (K and V: 16 float4 registers)
+    __shared__ __align__(16) float sh_o[4][D];
+    __shared__ float sh_m[4], sh_l[4];
     const int hq = blockIdx.y, sidx = blockIdx.z, h = hq / group, HQ = H * group;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const kvc_seq_desc sd = kvc_load_desc(seqs, sidx);
-    const float *qh = q + ((long)sidx * HQ + hq) * D;
     const float sm_scale = kLog2e / sqrtf((float)D), inv_sqrt = 1.0f / sqrtf((float)D);
     const int nbuf = sd.buffered;
     const long t0 = (long)sd.n_chunks * bs;
-    // buffered scores (log2 units)
-    float bmax = -INFINITY;
-    for (int t = threadIdx.x; t < nbuf; t += blockDim.x) {
-        const float *kv = sd.k_buffer + ((long)t * H + h) * D;
-        float a = 0.f;
-        for (int c = 0; c < D; ++c) a = fmaf(kv[c], qh[c], a);
-        if (scores) scores[((long)sidx * HQ + hq) * ctx_stride + t0 + t] = a * inv_sqrt;
-        sh_p[t] = a * sm_scale;
-        bmax = fmaxf(bmax, a * sm_scale);
-    }
-    bmax = kvc_warp_max(bmax);
-    if ((threadIdx.x & 31) == 0) sh_red[threadIdx.x >> 5] = bmax;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float M = -INFINITY;
-        for (int w = 0; w < 4; ++w) M = fmaxf(M, sh_red[w]);
-        const Partial *p = partial + ((long)sidx * HQ + hq) * n_splits;
-        for (int s = 0; s < n_splits; ++s) M = fmaxf(M, p[s].m);
-        sh_m = M;
-    }
-    __syncthreads();
-    const float M = sh_m;
-    float lpart = 0.f;
-    for (int t = threadIdx.x; t < nbuf; t += blockDim.x) {
-        float e = exp2f(sh_p[t] - M);
-        sh_p[t] = e;
-        lpart += e;
-    }
-    lpart = kvc_warp_sum(lpart);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) sh_red[threadIdx.x >> 5] = lpart;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float L = sh_red[0] + sh_red[1] + sh_red[2] + sh_red[3];
-        const Partial *p = partial + ((long)sidx * HQ + hq) * n_splits;
-        for (int s = 0; s < n_splits; ++s)
-            if (p[s].m != -INFINITY) L += p[s].l * exp2f(p[s].m - M);
-        sh_l = L;
-    }
-    __syncthreads();
     const Partial *p = partial + ((long)sidx * HQ + hq) * n_splits;
-    for (int c = threadIdx.x; c < D; c += blockDim.x) {
-        float o = 0.f;
-        for (int s = 0; s < n_splits; ++s)
-            if (p[s].m != -INFINITY) o += p[s].o[c] * exp2f(p[s].m - M);
-        for (int t = 0; t < nbuf; ++t) o = fmaf(sh_p[t], sd.v_buffer[((long)t * H + h) * D + c], o);
-        out[((long)sidx * HQ + hq) * D + c] = o / sh_l;
+    const float4 q4 = reinterpret_cast<const float4 *>(q + ((long)sidx * HQ + hq) * D)[lane];
+    float m = -INFINITY, l = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int tb = warp; tb < nbuf; tb += 4 * R) {
+        float4 k4[R], v4[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const int t = tb + 4 * j;
+            const long row = ((long)t * H + h) * D;
+            k4[j] = t < nbuf ? reinterpret_cast<const float4 *>(sd.k_buffer + row)[lane]
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+            v4[j] = t < nbuf ? reinterpret_cast<const float4 *>(sd.v_buffer + row)[lane]
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float sc[R];
+        float bm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const int t = tb + 4 * j;
+            float a = k4[j].x * q4.x;
+            a = fmaf(k4[j].y, q4.y, a);
+            a = fmaf(k4[j].z, q4.z, a);
+            a = fmaf(k4[j].w, q4.w, a);
+            a = kvc_warp_sum(a);  // every lane holds the row's score
+            if (t < nbuf && lane == 0 && scores)
+                scores[((long)sidx * HQ + hq) * ctx_stride + t0 + t] = a * inv_sqrt;
+            sc[j] = t < nbuf ? a * sm_scale : -INFINITY;
+            bm = fmaxf(bm, sc[j]);
+        }
+        if (bm > m) {  // warp-uniform
+            const float alpha = exp2f(m - bm);
+            l *= alpha;
+            acc.x *= alpha; acc.y *= alpha; acc.z *= alpha; acc.w *= alpha;
+            m = bm;
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const float e = exp2f(sc[j] - m);  // 0 for rows past nbuf
+            l += e;
+            acc.x = fmaf(e, v4[j].x, acc.x);
+            acc.y = fmaf(e, v4[j].y, acc.y);
+            acc.z = fmaf(e, v4[j].z, acc.z);
+            acc.w = fmaf(e, v4[j].w, acc.w);
+        }
     }
+    reinterpret_cast<float4 *>(sh_o[warp])[lane] = acc;
+    if (lane == 0) {
+        sh_m[warp] = m;
+        sh_l[warp] = l;
+    }
+    __syncthreads();
+    // merge: the 4 warps' buffered partials and the split partials
+    float M = fmaxf(fmaxf(sh_m[0], sh_m[1]), fmaxf(sh_m[2], sh_m[3]));
+    for (int sp = 0; sp < n_splits; ++sp) M = fmaxf(M, p[sp].m);
+    const int c = tid;  // blockDim == D
+    float L = 0.f, o = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+        if (sh_m[w] != -INFINITY) {
+            const float sw = exp2f(sh_m[w] - M);
+            L += sh_l[w] * sw;
+            o += sh_o[w][c] * sw;
+        }
+    }
+    for (int sp = 0; sp < n_splits; ++sp) {
+        const float ms = p[sp].m;
+        if (ms != -INFINITY) {
+            const float sw = exp2f(ms - M);
+            L += p[sp].l * sw;
+            o += p[sp].o[c] * sw;
+        }
+    }
+    out[((long)sidx * HQ + hq) * D + c] = o / L;
 }
 
 // ---------------------------------------------------------------------------
