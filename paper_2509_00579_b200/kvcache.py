@@ -803,10 +803,14 @@ class LayerCacheState:
     def stage_bytes(self) -> Tuple[int, int]:
         """Shared-memory staging size per K / V extent for the fused fetch,
         from the arenas' host max-extent bounds (no synchronisation)."""
+        # a block's TMA copy is its 16-B aligned superset: offsets and extents
+        # are 4-B aligned, so at most 12 bytes before and 12 after the block.
+        # (Tight on purpose: two fetch CTAs per SM need K + V stages <= ~9.8 KB,
+        # and config-2 data sits within ~100 B of that.)
         out = []
         for arena in (self.k_arena, self.v_arena):
             ext = arena.max_extent_bound() if arena.n_blocks else 16
-            out.append(((ext + 15) // 16) * 16 + 48)
+            out.append(((ext + 24 + 15) // 16) * 16)
         return out[0], out[1]
 
     def desc(self) -> _lib.SeqDesc:
