@@ -14,7 +14,7 @@ from .codebook import (DecodeTree, HuffmanCodebook, build_codebook, build_histog
                        build_smoothed_codebook, codebook_from_lengths, deserialize_codebook,
                        histogram_entropy, serialize_codebook, smooth_histogram)
 from .codec import (CompressedArena, CompressedBlock, DataMovement, DeviceArena, compress_block, decode_slice,
-                    decode_slices, decompress_block, encode_slice, metadata_overhead,
+                    decode_slices, decompress_block, encode_slice, iter_decoded_blocks, metadata_overhead,
                     reserve_arena_pool, scan_offsets, units_per_block)
 from .container import load_state, read_header, save_state
 from .errors import (ArenaFullError, CodebookError, CodecError, ConfigError,
@@ -27,6 +27,8 @@ from .metrics import (BenchRow, CompressionStats, SimulationResult, SimulationSe
                       median_time, run_ratio_sweep, run_simulation, write_csv)
 from .quantizer import (DEFAULT_REL_SCALE, MIN_REL_SCALE, QuantConfig, QuantizedBlock, QuantMode,
                         QuantUnitMeta, dequantize_block, quantize_block, quantize_unit)
-from .tensor_io import CacheTensor, SyntheticSpec, generate_synthetic, generate_synthetic_device
+from .tensor_io import (CacheTensor, SyntheticSpec, generate_synthetic, generate_synthetic_device,
+                        read_tensor, write_tensor)
+from . import bench  # noqa: F401  (kvpack.bench)
 
 __version__ = "0.1.0"

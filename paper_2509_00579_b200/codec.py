@@ -715,6 +715,66 @@ def decompress_block(arena: "DeviceArena", ordinal: int, cb, *, mode, head_num: 
                           ctx_start=(block_index // head_num) * block_size)
 
 
+DECODE_GROUP_SLICES = 8192  # codec.py:38
+
+
+def iter_decoded_blocks(arena: "DeviceArena", cb, *, n_units: int, head_dim: int, ordinals=None,
+                        group_slices: int = DECODE_GROUP_SLICES, movement=None):
+    """codec.py:394-452 on the device: arena blocks decoded by
+    kvc_decode_blocks in groups of about ``group_slices`` slices (one launch
+    per group, so scratch stays bounded).  Yields ``(ordinal, block_index,
+    codes [n_slices, head_dim] u8, mins, scales)`` in the order of
+    ``ordinals``; tensors live on the arena's device.  A block whose header,
+    counters or payload disagree with the codebook raises CodecError."""
+    n = len(arena)
+    if n == 0:
+        return
+    which = list(range(n)) if ordinals is None else [int(o) for o in ordinals]
+    if not which:
+        return
+    offs = arena.block_offsets
+    cursor = arena.write_cursor
+
+    def extent(o: int) -> Tuple[int, int]:
+        if not 0 <= o < n:
+            raise CodecError(f"block ordinal {o} out of range")
+        return int(offs[o]), (int(offs[o + 1]) if o + 1 < n else cursor)
+
+    # slices per block: the u16 after the block index in the first header
+    s0, e0 = extent(which[0])
+    if e0 - s0 < 6:
+        raise CodecError("block extent shorter than its header")
+    bs = int.from_bytes(arena.raw_tensor()[s0 + 4: s0 + 6].cpu().numpy().tobytes(), "little")
+    if bs < 1:
+        raise CodecError("block with zero slices")
+    dev = arena.device
+    tables = cb.device_tables(dev)
+    per_group = max(1, -(-group_slices // bs))
+    for g in range(0, len(which), per_group):
+        grp = which[g: g + per_group]
+        for o in grp:
+            s, e = extent(o)
+            if movement is not None:
+                movement.add_read(e - s)
+        m = len(grp)
+        codes = torch.empty((m, bs, head_dim), dtype=torch.uint8, device=dev)
+        metas = torch.empty((m, n_units, 2), dtype=torch.float32, device=dev)
+        bidx = torch.zeros(m, dtype=torch.int32, device=dev)  # u32 block indices
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        ords = torch.tensor(grp, dtype=torch.int32, device=dev)
+        st = _lib.lib().kvc_decode_blocks(arena.buf_ptr, arena.offsets_ptr, arena.counters_ptr,
+                                          ords.data_ptr(), m, bs, n_units, head_dim,
+                                          tables.data_ptr(), codes.data_ptr(), metas.data_ptr(),
+                                          bidx.data_ptr(), err.data_ptr(), _stream(dev))
+        _lib.check(st, "iter_decoded_blocks")
+        _lib.raise_device_error(int(err.item()), "iter_decoded_blocks")
+        if movement is not None:
+            movement.note_scratch(codes.numel())
+        block_ids = bidx.cpu().numpy().view(np.uint32).tolist()
+        for i, o in enumerate(grp):
+            yield o, int(block_ids[i]), codes[i], metas[i, :, 0], metas[i, :, 1]
+
+
 def metadata_overhead(cblocks, head_dim: int) -> Tuple[float, float]:
     """codec.py:455-472: 16-bit slice counters as fractions of the payload and
     of the original 16-bit values."""
@@ -814,3 +874,8 @@ class CompressedArena(DeviceArena):
                  initial_blocks: int = 256):
         super().__init__(_dev(device), capacity, initial_bytes=initial_bytes,
                          initial_blocks=initial_blocks)
+
+
+# names the reference's codec module also carries (codec.py:19-36 imports)
+from .codebook import DecodeTree, HuffmanCodebook  # noqa: E402
+from .quantizer import QuantizedBlock, QuantMode  # noqa: E402

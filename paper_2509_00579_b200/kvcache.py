@@ -981,3 +981,8 @@ def append_batched(states, k_rows: torch.Tensor, v_rows: torch.Tensor,
         n = s._after_append()
         if n is not None:
             s._overflow(n)
+
+
+# names the reference's kvcache module also carries (kvcache.py:14-27 imports)
+from .codebook import build_codebook, build_histogram, smooth_histogram  # noqa: E402
+from .quantizer import quantize_block  # noqa: E402

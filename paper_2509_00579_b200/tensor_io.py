@@ -4,7 +4,9 @@
 PCG64 streams, float32 normals, outlier channels) so oracle-checked inputs
 are identical; ``generate_synthetic_device`` draws the same distribution on
 the GPU (torch RNG, not bit-identical) for full-size benchmark inputs.
-KVTN file I/O is out of scope for the hot path.
+``write_tensor`` / ``read_tensor`` handle the reference's KVTN files
+(tensor_io.py:100-143): a 30-byte little-endian header (b"KVTN", version 1,
+dtype code 0 = f16 / 1 = f32, three u64 dimensions) and the raw values.
 """
 
 from __future__ import annotations
@@ -121,3 +123,58 @@ def generate_synthetic_device(spec: SyntheticSpec, device="cuda", dtype=torch.fl
                         dtype=torch.float32)
         out[t0:t1] = (x * scale).to(dtype)
     return out
+
+
+# KVTN header (tensor_io.py:22-26) as a packed little-endian record
+_KVTN = np.dtype([("magic", "S4"), ("version", "u1"), ("code", "u1"), ("dims", "<u8", (3,))])
+_KVTN_VERSION = 1
+_KVTN_TYPES = (np.dtype("<f2"), np.dtype("<f4"))  # indexed by the dtype code
+
+
+def write_tensor(t: CacheTensor, path) -> None:
+    """tensor_io.py:100-111: header + C-order values.  Device tensors are
+    copied to the host first."""
+    v = t.values
+    if isinstance(v, torch.Tensor):
+        v = v.detach().cpu().numpy()
+    v = np.asarray(v)
+    if v.dtype not in (np.float16, np.float32):
+        raise TensorFormatError(f"cannot write dtype {v.dtype}")
+    code = 0 if v.dtype == np.float16 else 1
+    hdr = np.zeros((), _KVTN)
+    hdr["magic"], hdr["version"], hdr["code"] = b"KVTN", _KVTN_VERSION, code
+    hdr["dims"] = v.shape
+    with open(path, "wb") as fh:
+        fh.write(hdr.tobytes())
+        fh.write(np.ascontiguousarray(v, dtype=_KVTN_TYPES[code]).tobytes())
+
+
+def read_tensor(path) -> CacheTensor:
+    """tensor_io.py:114-143: the inverse of write_tensor, validating the
+    header, the payload length and finiteness (TensorFormatError)."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if len(blob) < _KVTN.itemsize:
+        raise TensorFormatError(f"KVTN header needs {_KVTN.itemsize} bytes, file has {len(blob)}")
+    hdr = np.frombuffer(blob, _KVTN, count=1)[0]
+    if bytes(hdr["magic"]) != b"KVTN":
+        raise TensorFormatError(f"not a KVTN file (magic {bytes(hdr['magic'])!r})")
+    if int(hdr["version"]) != _KVTN_VERSION:
+        raise TensorFormatError(f"KVTN version {int(hdr['version'])} is not supported")
+    code = int(hdr["code"])
+    if code >= len(_KVTN_TYPES):
+        raise TensorFormatError(f"KVTN dtype code {code} is not supported")
+    dims = tuple(int(d) for d in hdr["dims"])
+    if min(dims) < 1:
+        raise TensorFormatError(f"KVTN dimensions {dims} must be positive")
+    dt = _KVTN_TYPES[code]
+    need = dims[0] * dims[1] * dims[2] * dt.itemsize
+    have = len(blob) - _KVTN.itemsize
+    if have < need:
+        raise TensorFormatError(f"truncated KVTN payload ({have} of {need} bytes)")
+    if have > need:
+        raise TensorFormatError(f"{have - need} trailing bytes after the KVTN payload")
+    vals = np.frombuffer(blob, dt, offset=_KVTN.itemsize).reshape(dims).copy()
+    if not np.isfinite(vals).all():
+        raise TensorFormatError("KVTN payload holds NaN/Inf")
+    return CacheTensor(vals)

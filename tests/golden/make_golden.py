@@ -307,6 +307,19 @@ def blockapi_cases():
                                        rcodec.units_per_block(mode, D, bs))
         out[nm + "_restore_counters"] = np.array([r.payload_bits, r.payload_bytes, r.n_slices,
                                                   r.size_bytes, len(r)], np.int64)
+    # iter_decoded_blocks (codec.py:394-452): out-of-order ordinals, groups of two blocks
+    for nm, ar, cb, mode in (("k", st.k_arena, st.k_codebook, kv.QuantMode.K_BLOCK),
+                             ("v", st.v_arena, st.v_codebook, kv.QuantMode.V_TOKEN)):
+        mv = rcodec.DataMovement()
+        it = list(rcodec.iter_decoded_blocks(ar, cb, n_units=rcodec.units_per_block(mode, D, bs),
+                                             head_dim=D, ordinals=[5, 0, 3, 1], group_slices=100,
+                                             movement=mv))
+        out[nm + "_iter_ords"] = np.array([r[0] for r in it], np.int64)
+        out[nm + "_iter_bidx"] = np.array([r[1] for r in it], np.int64)
+        out[nm + "_iter_codes"] = np.stack([r[2] for r in it])
+        out[nm + "_iter_mins"] = np.stack([r[3] for r in it])
+        out[nm + "_iter_scales"] = np.stack([r[4] for r in it])
+        out[nm + "_iter_movement"] = np.array([mv.bytes_read, mv.peak_scratch_values], np.int64)
     # CompressedArena.append: K block, V block, K block again, then a capacity refusal
     a = kv.CompressedArena()
     ords_app = [a.append(blocks[0]), a.append(blocks[1]), a.append(blocks[0])]
@@ -433,6 +446,24 @@ def big_digests(do_cfg2=False):
         json.dump(res, fh, indent=1)
 
 
+def kvtn_cases():
+    """KVTN files (tensor_io.py:100-143) written by the reference's
+    write_tensor, for tests/test_kvtn_cpu.py."""
+    rng = np.random.default_rng(19)
+    out = {}
+    for nm, dt, shape in (("f16", np.float16, (5, 3, 7)), ("f32", np.float32, (4, 2, 9))):
+        vals = rng.standard_normal(shape).astype(dt)
+        path = os.path.join(tempfile.mkdtemp(), "t.kvtn")
+        kv.write_tensor(kv.CacheTensor(vals), path)
+        with open(path, "rb") as fh:
+            out[nm + "_file"] = np.frombuffer(fh.read(), np.uint8).copy()
+        out[nm + "_values"] = vals
+        back = kv.read_tensor(path).values
+        assert np.array_equal(back.view(np.uint8), vals.view(np.uint8))
+    np.savez_compressed(os.path.join(HERE, "kvtn.npz"), **out)
+    print("kvtn: written")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
@@ -444,6 +475,7 @@ def main():
         return
     kat_cases()
     blockapi_cases()
+    kvtn_cases()
     make_case("c_fp16_d128", ctx=64 * 3 + 37, H=2, D=128, bs=64, seed=3, appended=100)
     make_case("c_f32_d32_bs16", ctx=16 * 5 + 3, H=4, D=32, bs=16, dtype=np.float32,
               synthetic=False, seed=7, appended=40)

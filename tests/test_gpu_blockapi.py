@@ -227,3 +227,27 @@ def test_run_simulation(kv, g):
     assert sim.summary.config == str(g["sim_label"])
     assert sim.max_divergence <= 1e-4
     assert sim.summary.fused_time > 0 and sim.summary.equivalent_decompression_throughput
+
+
+def test_iter_decoded_blocks(kv, g, state):
+    """codec.py:394-452: ordinals out of order, groups of two blocks (100
+    slices), movement counters equal to the reference's."""
+    for nm, ar, mode in (("k", state.k_arena, kv.QuantMode.K_BLOCK),
+                         ("v", state.v_arena, kv.QuantMode.V_TOKEN)):
+        mv = kv.DataMovement()
+        rows = list(kv.iter_decoded_blocks(ar, _cb(state, nm), n_units=kv.units_per_block(mode, 128, 64),
+                                           head_dim=128, ordinals=[5, 0, 3, 1], group_slices=100,
+                                           movement=mv))
+        assert [r[0] for r in rows] == list(g[nm + "_iter_ords"])
+        assert [r[1] for r in rows] == list(g[nm + "_iter_bidx"])
+        assert np.array_equal(np.stack([_np(r[2]) for r in rows]), g[nm + "_iter_codes"])
+        assert np.array_equal(np.stack([_np(r[3]) for r in rows]), g[nm + "_iter_mins"])
+        assert np.array_equal(np.stack([_np(r[4]) for r in rows]), g[nm + "_iter_scales"])
+        assert [mv.bytes_read, mv.peak_scratch_values] == list(g[nm + "_iter_movement"])
+        # all blocks in arena order, one group
+        full = list(kv.iter_decoded_blocks(ar, _cb(state, nm), n_units=kv.units_per_block(mode, 128, 64),
+                                           head_dim=128))
+        assert [r[0] for r in full] == list(range(len(ar)))
+        with pytest.raises(kv.CodecError):
+            list(kv.iter_decoded_blocks(ar, _cb(state, nm), n_units=kv.units_per_block(mode, 128, 64),
+                                        head_dim=128, ordinals=[len(ar)]))
