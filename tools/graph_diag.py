@@ -16,13 +16,18 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--layers", type=int, default=8)
     ap.add_argument("--steps", type=int, default=128)
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--ctx", type=int, default=32768)
+    ap.add_argument("--heads", type=int, default=40)
+    ap.add_argument("--profile-capture", action="store_true",
+                    help="cProfile each re-capture (top functions by cumulative time)")
     a = ap.parse_args()
     import torch
     import bench
     import paper_2509_00579_b200 as kv
     from paper_2509_00579_b200 import decode_loop
     dev = torch.device("cuda", 0)
-    L, B, T, H = a.layers, 8, 32768, 40
+    L, B, T, H = a.layers, a.batch, a.ctx, a.heads
     kv.reserve_arena_pool(int(1.1 * 0.3 * 2 * L * B * T * H * 128 * 2), dev)
     states, _, _ = bench.build_cache(kv, torch, L, B, T, H, 0, H, dev)
     q = torch.randn((L, B, H, 128), device=dev)
@@ -36,7 +41,16 @@ def main():
     def cap(self, *args):
         torch.cuda.synchronize()
         t = time.perf_counter()
-        orig(self, *args)
+        if a.profile_capture:
+            import cProfile
+            import pstats
+            pr = cProfile.Profile()
+            pr.enable()
+            orig(self, *args)
+            pr.disable()
+            pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
+        else:
+            orig(self, *args)
         torch.cuda.synchronize()
         cap_t.append(time.perf_counter() - t)
     decode_loop.DecodeLoop._capture = cap
