@@ -486,6 +486,45 @@ def _counters_readback(counters: torch.Tensor):
     return slot, ev
 
 
+# pinned slots of batched readbacks: [host buffer, event, weakrefs of the arenas served]
+_BATCH_SLOTS: list = []
+
+
+def readback_extents(arenas) -> None:
+    """Start one asynchronous counter readback for many arenas at once (a
+    stacked device copy, one D2H copy, one event) instead of one per arena:
+    after a batch's overflow event the per-arena copies were thousands of
+    tiny transfers whose pinned ring also throttled the host.  Arenas without
+    a stale extent are skipped; max_extent_bound() consumes the result."""
+    todo = [a for a in arenas if getattr(a, "_ext_stale", False) and a.device.type == "cuda"]
+    if len(todo) < 2:
+        return
+    rows = torch.stack([a._counters.view(torch.uint8).reshape(-1) for a in todo])
+    nb = rows.numel()
+    slot = None
+    for sl in _BATCH_SLOTS:
+        if sl[0].numel() >= nb and (sl[1] is None or sl[1].query()):
+            slot = sl
+            break
+    if slot is None:
+        slot = [torch.empty(max(nb, 1 << 16), dtype=torch.uint8, pin_memory=True), None, []]
+        _BATCH_SLOTS.append(slot)
+    # arenas that have not read their result from this slot yet do so now
+    # (its copy has completed), before it is overwritten
+    for r in slot[2]:
+        a = r()
+        if a is not None and a._ext_pending is not None and a._ext_pending[1] is slot[1]:
+            a.max_extent_bound()
+    host = slot[0][:nb].view(len(todo), -1)
+    host.copy_(rows, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(todo[0].device))
+    slot[1], slot[2] = ev, [weakref.ref(a) for a in todo]  # weak: arenas may be freed
+    for i, a in enumerate(todo):
+        a._ext_stale = False
+        a._ext_pending = (host[i], ev)
+
+
 def full_error(what="arena"):
     return ArenaFullError(f"{what}: capacity exhausted")
 

@@ -26,7 +26,7 @@ import torch
 
 from . import _lib
 from .codebook import HuffmanCodebook, build_smoothed_codebook
-from .codec import DeviceArena, pooled_zeros, worst_block_bytes
+from .codec import DeviceArena, pooled_zeros, readback_extents, worst_block_bytes
 from .errors import CodecError, ConfigError
 from .quantizer import QuantConfig, QuantMode, as_device_tensor, dtype_code, quantize_tokens
 from .tensor_io import CacheTensor
@@ -977,10 +977,33 @@ def append_batched(states, k_rows: torch.Tensor, v_rows: torch.Tensor,
         ddev.data_ptr(), B, H, D, s0.cfg_k.buffer_size + 1, kd.data_ptr(), vd.data_ptr(),
         dtype_code(kd), H * D, None, torch.cuda.current_stream(s0.device).cuda_stream),
         "kvc_buffer_append")
+    over = []
     for s in states:
         n = s._after_append()
         if n is not None:
+            over.append((s, n))
+    if not over:
+        return
+    bs = s0.cfg_k.block_size
+    if len(over) == B and len({(n, s.buffered - n, s.compressed_tokens + n) for s, n in over}) == 1:
+        # the usual decode-loop event: every state overflows at the same
+        # point, so one batched shift (through the batch descriptors: only
+        # the buffers and live pairs are touched) replaces B per-state
+        # descriptor uploads and shifts
+        for s, n in over:
+            s._compress_buffer(n)
+        n = over[0][1]
+        rem = s0.buffered - n
+        _lib.check(_lib.lib().kvc_buffer_shift(ddev.data_ptr(), B, H, D, n, rem,
+                                               s0.compressed_tokens // bs,
+                                               torch.cuda.current_stream(s0.device).cuda_stream),
+                   "kvc_buffer_shift")
+        for s, _ in over:
+            s.buffered = rem
+    else:
+        for s, n in over:
             s._overflow(n)
+    readback_extents([a for s, _ in over for a in (s.k_arena, s.v_arena)])
 
 
 # names the reference's kvcache module also carries (kvcache.py:14-27 imports)

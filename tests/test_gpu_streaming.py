@@ -128,3 +128,32 @@ def test_decode_loop_graph_matches_eager(kv, group, rels):
     if group == 1:
         ref, _, _ = kv.attention_batched(sa[0], q[0].contiguous())
         assert torch.equal(ref, oa[0]) or float((ref - oa[0]).abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("ctxs", [(64 * 5 + 17, 64 * 7 + 17, 64 * 2 + 17),   # same step, unequal n_chunks
+                                  (64 * 5 + 17, 64 * 5 + 40, 64 * 3 + 90)])  # events at different steps
+def test_append_batched_ragged_events(kv, ctxs):
+    """Batches whose overflow events differ per state take the per-state
+    shift; the arenas, counts and live pairs equal append_token's."""
+    import torch
+    H, extra = 2, 240
+    data = [_data(c, extra, H, 40 + i) for i, c in enumerate(ctxs)]
+    a = [_prefill(kv, k, v, c) for (k, v), c in zip(data, ctxs)]
+    b_ = [_prefill(kv, k, v, c) for (k, v), c in zip(data, ctxs)]
+    cache = kv.kvcache._BatchDesc()
+    for j in range(extra):
+        kd = torch.from_numpy(np.stack([d[0][c + j] for d, c in zip(data, ctxs)])).cuda()
+        vd = torch.from_numpy(np.stack([d[1][c + j] for d, c in zip(data, ctxs)])).cuda()
+        kv.append_batched(a, kd, vd, desc_cache=cache)
+        for i, st in enumerate(b_):
+            st.append_token(data[i][0][ctxs[i] + j].astype(np.float32),
+                            data[i][1][ctxs[i] + j].astype(np.float32))
+    for i in range(len(ctxs)):
+        a[i].check()
+        assert a[i].k_arena.snapshot() == b_[i].k_arena.snapshot()
+        assert a[i].v_arena.snapshot() == b_[i].v_arena.snapshot()
+        assert (a[i].buffered, a[i].compressed_tokens) == (b_[i].buffered, b_[i].compressed_tokens)
+        assert a[i]._live.tolist() == [a[i].n_chunks, a[i].buffered]
+        a[i].settle()
+        b_[i].settle()
+        assert a[i].stage_bytes() == b_[i].stage_bytes()
