@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--ctx", type=int, default=32768)
     ap.add_argument("--heads", type=int, default=40)
+    ap.add_argument("--side-stream", action="store_true",
+                    help="run both loops on a created (non-default) stream")
     ap.add_argument("--profile-capture", action="store_true",
                     help="cProfile each re-capture (top functions by cumulative time)")
     a = ap.parse_args()
@@ -34,6 +36,8 @@ def main():
     out = torch.empty_like(q)
     kn = (torch.randn((L, B, H, 128), device=dev) * 0.5).half()
     vn = (torch.randn((L, B, H, 128), device=dev) * 0.5).half()
+    if a.side_stream:
+        torch.cuda.set_stream(torch.cuda.Stream(dev))
     stream = torch.cuda.current_stream(dev)
     orig = decode_loop.DecodeLoop._capture
     cap_t = []
