@@ -3,7 +3,7 @@
 live in :mod:`.metrics` (statistics, BenchRow/CSV, the decode-loop simulation
 and the ratio sweep, all on the device)."""
 
-from .metrics import (BenchRow, CompressionStats, SimulationResult, SimulationSettings,  # noqa: F401
+from .metrics import (FUSED_FASTER, BenchRow, CompressionStats, SimulationResult, SimulationSettings,  # noqa: F401
                       collect_stats, config_label, equivalent_decompression_throughput,
                       median_time, run_ratio_sweep, run_simulation, write_csv)
 # names the reference's bench module also carries (bench.py:25-50 imports)

@@ -580,7 +580,8 @@ class CompressedBlock:
     def total_bits(self) -> int:
         if self._total_bits is not None:
             return self._total_bits
-        return int(self.slice_bit_counts.to(torch.int64).sum())
+        return int(torch.as_tensor(np.asarray(self.slice_bit_counts) if not isinstance(
+            self.slice_bit_counts, torch.Tensor) else self.slice_bit_counts).to(torch.int64).sum())
 
 
 def _encode_one_block(codes: torch.Tensor, metas: torch.Tensor, block_index: int, cb):
@@ -591,7 +592,7 @@ def _encode_one_block(codes: torch.Tensor, metas: torch.Tensor, block_index: int
     n_units = metas.shape[0]
     lib = _lib.lib()
     arena = DeviceArena(dev, None, initial_bytes=worst_block_bytes(bs, n_units, D,
-                                                                   cb.max_code_length),
+                                                                   cb.max_code_length) + TMA_SLACK,
                         initial_blocks=1)
     ws = torch.empty(lib.kvc_encode_workspace_bytes(1, bs), dtype=torch.uint8, device=dev)
     st = lib.kvc_encode_append(codes.data_ptr(), metas.data_ptr(), 1, 1, 1, 0, int(block_index),
@@ -831,7 +832,7 @@ def _block_image(cb: CompressedBlock) -> torch.Tensor:
     """_serialize_block (codec.py:229-244) of a block built from its fields."""
     if cb._image is not None:
         return cb._image
-    dev = cb.payload.device if cb.payload.is_cuda else _dev()
+    dev = cb.payload.device if isinstance(cb.payload, torch.Tensor) and cb.payload.is_cuda else _dev()
     hdr = np.zeros(6, np.uint8)
     hdr[:4] = np.frombuffer(np.uint32(cb.block_index).tobytes(), np.uint8)
     hdr[4:6] = np.frombuffer(np.uint16(cb.n_slices).tobytes(), np.uint8)
@@ -843,6 +844,12 @@ def _block_image(cb: CompressedBlock) -> torch.Tensor:
     raw = sum(p.numel() for p in parts)
     parts.append(torch.zeros((-raw) % 4, dtype=torch.uint8, device=dev))
     return torch.cat(parts)
+
+
+def _serialize_block(cblock: CompressedBlock) -> bytes:
+    """codec.py:229-244 as bytes (the reference's tests compare block images
+    through this helper)."""
+    return _block_image(cblock).cpu().numpy().tobytes()
 
 
 def _arena_append(self: "DeviceArena", cblock: CompressedBlock) -> int:

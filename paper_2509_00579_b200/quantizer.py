@@ -85,8 +85,8 @@ class QuantizedBlock:
 
 def as_device_tensor(x, device=None) -> torch.Tensor:
     """f16/f32 torch tensor on the CUDA device (numpy input is copied over)."""
-    if isinstance(x, np.ndarray):
-        x = torch.from_numpy(np.ascontiguousarray(x))
+    if not isinstance(x, torch.Tensor):  # numpy arrays, nested lists
+        x = torch.from_numpy(np.ascontiguousarray(np.asarray(x)))
     if x.dtype not in (torch.float16, torch.float32):
         x = x.to(torch.float32)
     dev = torch.device(device) if device is not None else (
@@ -190,9 +190,9 @@ def quantize_block(block, mode: QuantMode, cfg: QuantConfig, head_index: int, ct
 
 def dequantize_block(q: QuantizedBlock, mode: QuantMode) -> torch.Tensor:
     """quantizer.py:212-223: min + code * scale in float64."""
-    codes = q.codes.to(torch.float64)
-    mins = q.unit_mins.to(torch.float64)
-    scales = q.unit_scales.to(torch.float64)
+    codes = torch.as_tensor(q.codes).to(torch.float64)
+    mins = torch.as_tensor(q.unit_mins).to(torch.float64)
+    scales = torch.as_tensor(q.unit_scales).to(torch.float64)
     if mode is QuantMode.V_TOKEN:
         if mins.shape[0] != codes.shape[0]:
             raise CodecError("token-mode metadata count must equal block_size")
